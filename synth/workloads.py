@@ -1,0 +1,134 @@
+"""Seeded synthetic workloads.
+
+Configs (BASELINE.json):
+  1 IntV 1D tiny   l_I=8,  M=4,      l_S=8   x ~ U[0,2^8); (lo,hi) sorted pair of U[0,2^8) draws
+  2 IntV 1D        l_I=16, M=1024,   l_S=16  widths round(2^u), u ~ U[4,12]; K in {0,1,2..4} forced hits
+  3 rectangle      l_I=16, M=4096,   l_S=32  d=2, sides round(2^u), u ~ U[6,12] per axis; K forced hits
+  4 IdM            l_I=20, M=65536,  l_S=32  distinct U[0,2^20) ids; query id present or absent by seed
+  5 NAND sweep     2^10 / 2^14 / 2^17 / 2^20 pairs of U{0,1} bits
+Seeds: keys 1000 + cfg, data 2000 + cfg (overridable).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+MODE_INTV, MODE_COV, MODE_IDM = 0, 1, 2
+F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE = 1, 2, 4, 8, 16
+CONFIG_FLAGS = F_CLOSED_UPPER | F_UNSIGNED | F_EQ_TREE | F_SUM_TREE
+
+
+@dataclass
+class Workload:
+    cfg: int
+    mode: int
+    M: int
+    l_I: int
+    l_S: int
+    d: int
+    flags: int
+    query: list            # query words (x) / (x, y) / (id)
+    records: np.ndarray    # (M, W) uint64 record words
+    payloads: np.ndarray   # (M,) uint64
+    key_seed: int
+    data_seed: int
+    forced: list = field(default_factory=list)  # indices of records forced to match
+
+    @property
+    def name(self):
+        return CONFIGS[self.cfg]["name"]
+
+
+CONFIGS = {
+    1: dict(name="intv1d_tiny", mode=MODE_INTV, M=4, l_I=8, l_S=8, d=1),
+    2: dict(name="intv1d_1024", mode=MODE_INTV, M=1024, l_I=16, l_S=16, d=1),
+    3: dict(name="rect2d_4096", mode=MODE_INTV, M=4096, l_I=16, l_S=32, d=2),
+    4: dict(name="idm_65536", mode=MODE_IDM, M=65536, l_I=20, l_S=32, d=1),
+}
+
+
+def _interval_containing(rng, x, w, top):
+    lo_min = max(0, x - w + 1)
+    lo_max = min(x, top - w)
+    lo = int(rng.integers(lo_min, lo_max + 1))
+    return lo, lo + w - 1
+
+
+def _interval_random(rng, w, top):
+    lo = int(rng.integers(0, top - w + 1))
+    return lo, lo + w - 1
+
+
+def _hit_count(rng):
+    k = int(rng.integers(0, 3))
+    return k if k < 2 else int(rng.integers(2, 5))
+
+
+def make_workload(cfg: int, data_seed: int | None = None, key_seed: int | None = None,
+                  M: int | None = None, flags: int = CONFIG_FLAGS, hits: int | None = None) -> Workload:
+    """Draw the plaintext inputs of config ``cfg`` (1-4).  ``M`` overrides the record count (tests),
+    ``hits`` the number of records forced to match."""
+    c = CONFIGS[cfg]
+    data_seed = 2000 + cfg if data_seed is None else data_seed
+    key_seed = 1000 + cfg if key_seed is None else key_seed
+    M = c["M"] if M is None else M
+    rng = np.random.default_rng(data_seed)
+    l_I, l_S, d, mode = c["l_I"], c["l_S"], c["d"], c["mode"]
+    top = 1 << l_I
+    payloads = rng.integers(0, 1 << l_S, size=M, dtype=np.uint64)
+    forced = []
+    if cfg == 1:
+        x = int(rng.integers(0, top))
+        recs = np.zeros((M, 2), np.uint64)
+        for i in range(M):
+            a, b = sorted(int(v) for v in rng.integers(0, top, size=2))
+            recs[i] = (a, b)
+        query = [x]
+    elif cfg in (2, 3):
+        lo_u, hi_u = (4, 12) if cfg == 2 else (6, 12)
+        query = [int(rng.integers(0, top)) for _ in range(d)]
+        K = _hit_count(rng) if hits is None else hits
+        forced = sorted(int(i) for i in rng.choice(M, size=min(K, M), replace=False))
+        recs = np.zeros((M, 2 * d), np.uint64)
+        for i in range(M):
+            while True:
+                row = []
+                inside = True
+                for a in range(d):
+                    w = int(round(2.0 ** rng.uniform(lo_u, hi_u)))
+                    if i in forced:
+                        lo, hi = _interval_containing(rng, query[a], w, top)
+                    else:
+                        lo, hi = _interval_random(rng, w, top)
+                    inside = inside and lo <= query[a] <= hi
+                    row += [lo, hi]
+                if i in forced or not inside:
+                    break
+            recs[i] = row
+    elif cfg == 4:
+        ids = rng.choice(top, size=M, replace=False).astype(np.uint64)
+        recs = ids.reshape(M, 1)
+        present = bool(rng.integers(0, 2)) if hits is None else hits > 0
+        if present:
+            k = int(rng.integers(0, M))
+            query = [int(ids[k])]
+            forced = [k]
+        else:
+            idset = set(int(v) for v in ids)
+            while True:
+                q = int(rng.integers(0, top))
+                if q not in idset:
+                    break
+            query = [q]
+    else:
+        raise ValueError(f"config {cfg} is not a circuit config")
+    return Workload(cfg, mode, M, l_I, l_S, d, flags, query, recs, payloads, key_seed, data_seed, forced)
+
+
+def nand_inputs(count: int, data_seed: int = 2005):
+    """Config 5: ``count`` pairs of U{0,1} plaintext bits (a, b)."""
+    rng = np.random.default_rng(data_seed)
+    a = rng.integers(0, 2, size=count, dtype=np.uint8)
+    b = rng.integers(0, 2, size=count, dtype=np.uint8)
+    return a, b
