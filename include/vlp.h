@@ -1,0 +1,188 @@
+/*
+ * vlp.h -- C ABI of the B200 VeLoPIR gate-bootstrapping engine (libvlp.so).
+ *
+ * Citation key: P:n = /root/reference/PAPER.md line n; Rk = DESIGN.md section 3 reading k.
+ * The calls follow the paper's problem statement: keygen, encrypt query, server
+ * evaluation (alg:VeLoPIR P:307-329), decrypt; plus the preprocessing the paper's
+ * server performs (alg:PubKeyGen P:194-219, alg:ServerEnc P:223-247) and the raw gate batch of
+ * BASELINE.json config 5.
+ *
+ * Conventions
+ *  - Every call returns an int status: VLP_OK (0) or a negative VLP_E* code; no exceptions cross the
+ *    ABI.  vlp_last_error() returns a thread-local description of the last failure.
+ *  - Handles (vlp_sk, vlp_evk, vlp_pk, vlp_server, vlp_program) are opaque and library-owned; free them
+ *    with the matching vlp_free_* call.
+ *  - Ciphertext buffers are caller-owned arrays uint32_t[count][VLP_CT_STRIDE] (632 words: a[0..629],
+ *    b at word 630, one zero pad word), little-endian.  Arguments ending in _dev are device pointers
+ *    (CUDA, on the given stream, passed as plain pointers); all others are host pointers.
+ *  - Device memory belongs to the caller (PyTorch tensors): the library asks for sizes
+ *    (vlp_server_evk_bytes, vlp_program_info) and never allocates device memory itself.
+ *  - Streams are passed as uint64_t (a cudaStream_t value; 0 = legacy default stream).  Device calls
+ *    are asynchronous on that stream unless stated.
+ *  - Everything is deterministic in its seeds (R3).  The library's keys and encryptions are
+ *    byte-identical to the test oracle's for the same seeds (tested, not shared code).
+ */
+#ifndef VLP_H
+#define VLP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VLP_N_LWE 630       /* TLWE dimension n, tab:tfhe_params P:1236 */
+#define VLP_N_RING 1024     /* ring dimension N */
+#define VLP_CT_STRIDE 632   /* words per TLWE ciphertext buffer row (631 + pad) */
+#define VLP_NLWE_STRIDE 1028 /* words per N-LWE row (1025 + pad) */
+
+enum {
+  VLP_OK = 0,
+  VLP_EINVAL = -1,   /* bad argument (null pointer, size out of range) */
+  VLP_EMODE = -2,    /* mode / meta mismatch */
+  VLP_EWIDTH = -3,   /* width mismatch or l < 2 */
+  VLP_ERANGE = -4,   /* plaintext value >= 2^l */
+  VLP_EPKUSED = -5,  /* public-key samples already consumed (alg:PubKeyGen samples are single-use) */
+  VLP_ECUDA = -6,    /* CUDA runtime error (see vlp_last_error) */
+  VLP_ENOMEM = -7,   /* host allocation failed or caller buffer too small */
+  VLP_ENODEV = -8    /* no CUDA device / kernel image for this device */
+};
+
+/* Modes and flags (readings R11, R12, R14, R15, R19). */
+enum { VLP_MODE_INTV = 0, VLP_MODE_COV = 1, VLP_MODE_IDM = 2 };
+enum {
+  VLP_F_CLOSED_UPPER = 1, /* R12: lo <= x <= hi (CompLE on the right bound) instead of x < hi */
+  VLP_F_UNSIGNED = 2,     /* R11: unsigned comparators (final MUX selects ct2[l-1]) */
+  VLP_F_EQ_TREE = 4,      /* R14: alg:HomEqOPT pairwise AND tree instead of the serial HomEQ */
+  VLP_F_SUM_TREE = 8,     /* R15: outermost XOR tree instead of the serial HomSum */
+  VLP_F_OR_REDUCE = 16    /* R19: OR instead of XOR in the aggregation */
+};
+#define VLP_CONFIG_FLAGS (VLP_F_CLOSED_UPPER | VLP_F_UNSIGNED | VLP_F_EQ_TREE | VLP_F_SUM_TREE)
+
+/* Gate opcodes (R10). */
+enum { VLP_AND = 0, VLP_NAND = 1, VLP_OR = 2, VLP_XOR = 3, VLP_XNOR = 4, VLP_MUX = 5 };
+
+/* tab:tfhe_params plus R2's fresh-encryption sigma. */
+typedef struct {
+  uint32_t n, N, k, bg_bits, ell, ks_base_bits, ks_t;
+  double sigma_lwe, sigma_bk, sigma_ks;
+} vlp_params;
+
+/* Session meta: M records, l_I location bits, l_S payload bits, d coordinates. */
+typedef struct {
+  uint32_t mode, M, l_I, l_S, d, flags;
+} vlp_meta;
+
+typedef struct vlp_sk vlp_sk;
+typedef struct vlp_evk vlp_evk;
+typedef struct vlp_pk vlp_pk;
+typedef struct vlp_server vlp_server;
+typedef struct vlp_program vlp_program;
+
+/* Program description (sizes the caller allocates; counts of the compiled level schedule). */
+typedef struct {
+  uint32_t levels;          /* circuit levels (one BR launch + one KS launch each) */
+  uint64_t br, ks;          /* blind rotations (MUX = 2) and key switches per evaluation */
+  uint64_t gates;           /* gates (MUX = 1) */
+  uint64_t in0_cts, in1_cts; /* ciphertexts read from in0 (query / a) and in1 (DB / b) */
+  uint64_t out_cts;         /* ciphertexts written to out */
+  uint64_t scratch_bytes;   /* device scratch the caller must provide */
+  uint64_t max_level_br;    /* widest level */
+  uint32_t kernel_launches; /* kernels launched per evaluation */
+} vlp_program_info;
+
+const char* vlp_last_error(void);
+
+/* Fills the 128-bit parameter set of tab:tfhe_params; sigma_lwe = 2^-15 (R2). */
+int vlp_params_tfhe128(vlp_params* out);
+
+/* KeyGen.  Host.  s in B^630, ring key z in B^1024 (R4), bsk (630 TRGSW,
+ * rows r = u*3 + j, R4) and ksk ([1024][8][3] TLWE samples, R6), all from `seed` (R3).
+ * Only the default parameter set is supported (VLP_EINVAL otherwise). */
+int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk, vlp_evk** evk);
+/* Copies of the key material for the byte-equality tests: s[630], z[1024] as 0/1 words;
+ * bsk[630][6][2][1024] torus32; ksk[1024][8][3][631] torus32.  Any pointer may be NULL. */
+int vlp_sk_export(const vlp_sk* sk, uint32_t* s, uint32_t* z);
+int vlp_evk_export(const vlp_evk* evk, uint32_t* bsk, uint32_t* ksk);
+
+/* TLWE encryption of `count` bits under s with the fresh-encryption domains (R3), objects
+ * obj0 .. obj0+count-1; out: host [count][632]. */
+int vlp_encrypt_bits(const vlp_sk* sk, const uint8_t* bits, size_t count, uint64_t seed, uint64_t obj0,
+                     uint32_t* out);
+/* Query encryption: values[w] for w < query words (IntV: d coordinates; CoV: d; IdM: 1),
+ * l_I bits each, LSB first (R20); object w*l_I + j of the query domains.  out: host [words*l_I][632].
+ * VLP_ERANGE if a value >= 2^l_I. */
+int vlp_encrypt_query(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint64_t seed,
+                      uint32_t* out);
+/* Dec: bit = [int32(b - <a, s>) > 0] (ties -> 0, R18).  Host. */
+int vlp_decrypt_bits(const vlp_sk* sk, const uint32_t* ct, size_t count, uint8_t* bits_out);
+
+/* alg:PubKeyGen for records [first, first+count): single-use TLWE(0) samples, pk^I
+ * (R17 counts: words W = 2d interval, d CoV, 1 IdM; bit j outer, word k inner as in the listing)
+ * then pk^S, materialised on the host (the client sends them to the server).  Multi-threaded. */
+int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                  vlp_pk** pk);
+/* Ciphertexts per record in the encrypted DB: W * l_I + l_S. */
+int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);
+/* alg:ServerEnc for the pk's records: ct = (0, Ecd(bit)) + pk sample.
+ * words: [count][W] plaintext bound words (IntV: lo,hi per axis; CoV: loc per axis; IdM: id);
+ * payloads: [count] values (< 2^l_S).  out: host [count][per_record][632] in the order word-major
+ * location bits (word k bit j at row k*l_I + j) then payload bits (row W*l_I + j).  Consumes the pk:
+ * a second call returns VLP_EPKUSED.  Server side: needs no secret key. */
+int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* out);
+
+/* Server: the evaluation key on one device.  evk_dev must hold vlp_server_evk_bytes() bytes (device
+ * memory on `device`); the bootstrapping key is uploaded and converted to the NTT domain in place
+ * (kernel vlp_bsk_convert_kernel), the key-switching key uploaded.  Synchronous. */
+size_t vlp_server_evk_bytes(void);
+int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_bytes, uint64_t stream,
+                      vlp_server** out);
+
+/* Compile VeLoPIR (alg:VeLoPIR with the readings of `meta->flags`) for records [first, first+count)
+ * into a level schedule (one BR launch + one KS launch per level, every independent gate of a level
+ * across all records in one batch; MUX halves hoisted).  The shard's XOR tree stops at its root; the
+ * l_S root ciphertexts are written to `out`.  in0 = query ciphertexts (vlp_encrypt_query layout),
+ * in1 = the shard's encrypted DB (vlp_server_encrypt_db layout, record `first` at row 0).
+ * `server` may be NULL to compile only (vlp_program_get_info works; vlp_program_eval fails). */
+int vlp_program_create(vlp_server* server, const vlp_meta* meta, size_t first, size_t count,
+                       vlp_program** out);
+/* A single level of `count` independent gates `op` (config 5): out[i] = op(in0[i], in1[i]); for
+ * VLP_MUX, out[i] = MUX(in0[i], in1[i], in2[i]) where in2 = in1 + count rows. */
+int vlp_program_create_gates(vlp_server* server, int op, size_t count, vlp_program** out);
+/* The top log2(G) levels of the aggregation tree over G shard roots (in0: [G][l_S][632], shards in
+ * rank order; G a power of two); writes the l_S result ciphertexts to out (R15). */
+int vlp_program_create_combine(vlp_server* server, const vlp_meta* meta, uint32_t G, vlp_program** out);
+int vlp_program_get_info(const vlp_program* prog, vlp_program_info* info);
+/* Device slot (row index in the scratch intermediate region) holding a named node of a circuit
+ * program, for sampled parity dumps: kind 0 = validation bit v of record r (bit ignored), kind 1 =
+ * masked payload bit (r, bit).  Returns VLP_EINVAL if absent. */
+int vlp_program_node_row(const vlp_program* prog, int kind, size_t record, uint32_t bit, uint64_t* row);
+/* Pointer to the intermediate region inside `scratch_dev` (rows of 632 words). */
+int vlp_program_intermediate_offset(const vlp_program* prog, uint64_t* byte_offset);
+
+/* Evaluate the program on `stream` (asynchronous).  scratch_dev: >= info.scratch_bytes of device
+ * memory (job arrays are uploaded into it on the first call with a given scratch pointer). */
+int vlp_program_eval(vlp_program* prog, void* scratch_dev, size_t scratch_bytes, const uint32_t* in0_dev,
+                     const uint32_t* in1_dev, uint32_t* out_dev, uint64_t stream);
+
+/* Debug / parity entry points (device, asynchronous): blind rotation of `count` TLWE inputs
+ * (in_dev [count][632], used as is: no gate linear form) for the first `steps` CMux steps, writing the
+ * raw TRLWE accumulators acc_dev [count][2][1024]; and the key switch of N-LWE rows
+ * (nlwe_dev [count][1028]) into out_dev [count][632].  scratch_dev: >= vlp_debug_scratch_bytes(count). */
+size_t vlp_debug_scratch_bytes(size_t count);
+int vlp_debug_blind_rotate(vlp_server* server, const uint32_t* in_dev, size_t count, int steps,
+                           uint32_t* acc_dev, void* scratch_dev, uint64_t stream);
+int vlp_debug_keyswitch(vlp_server* server, const uint32_t* nlwe_dev, size_t count, uint32_t* out_dev,
+                        void* scratch_dev, uint64_t stream);
+
+void vlp_free_sk(vlp_sk* sk);
+void vlp_free_evk(vlp_evk* evk);
+void vlp_free_pk(vlp_pk* pk);
+void vlp_free_server(vlp_server* server);
+void vlp_free_program(vlp_program* prog);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLP_H */

@@ -1,0 +1,209 @@
+"""Thin Python layer over the C ABI (include/vlp.h).  Argument marshalling only.
+
+PyTorch provides device memory (uint8 / int32 tensors) and streams; every computation of the hot path runs in
+libvlp.so's CUDA kernels.  Host ciphertext arrays are numpy uint32 [count, 632]; device ciphertext
+tensors are torch.int32 [count, 632] (same bytes).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import CT_STRIDE, NLWE_STRIDE, VlpMeta, VlpParams, VlpProgramInfo, check, lib
+
+
+def _u32p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+def meta(mode, M, l_I, l_S, d, flags=L.CONFIG_FLAGS) -> VlpMeta:
+    return VlpMeta(mode, M, l_I, l_S, d, flags)
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Keys:
+    """vlp_keygen: secret key + evaluation key, host side."""
+
+    def __init__(self, seed: int):
+        self.seed = seed
+        sk, evk = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib().vlp_keygen(seed, None, ctypes.byref(sk), ctypes.byref(evk)))
+        self.sk, self.evk = sk, evk
+
+    def __del__(self):
+        try:
+            lib().vlp_free_sk(self.sk)
+            lib().vlp_free_evk(self.evk)
+        except Exception:
+            pass
+
+    def export(self):
+        s = np.zeros(L.n, np.uint32)
+        z = np.zeros(L.N, np.uint32)
+        bsk = np.zeros(L.n * 6 * 2 * L.N, np.uint32)
+        ksk = np.zeros(L.N * 8 * 3 * (L.n + 1), np.uint32)
+        check(lib().vlp_sk_export(self.sk, _u32p(s), _u32p(z)))
+        check(lib().vlp_evk_export(self.evk, _u32p(bsk), _u32p(ksk)))
+        return s, z, bsk.reshape(L.n, 6, 2, L.N), ksk.reshape(L.N, 8, 3, L.n + 1)
+
+    def encrypt_bits(self, bits, seed: int, obj0: int = 0) -> np.ndarray:
+        bits = np.ascontiguousarray(np.asarray(bits, dtype=np.uint8))
+        out = np.zeros((len(bits), CT_STRIDE), np.uint32)
+        check(lib().vlp_encrypt_bits(self.sk, bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), len(bits),
+                                     seed, obj0, _u32p(out)))
+        return out
+
+    def encrypt_query(self, m: VlpMeta, values, seed: int) -> np.ndarray:
+        vals = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
+        words = 1 if m.mode == L.MODE_IDM else m.d
+        out = np.zeros((words * m.l_I, CT_STRIDE), np.uint32)
+        check(lib().vlp_encrypt_query(self.sk, ctypes.byref(m), _u64p(vals), seed, _u32p(out)))
+        return out
+
+    def decrypt_bits(self, ct: np.ndarray) -> np.ndarray:
+        ct = np.ascontiguousarray(ct, dtype=np.uint32).reshape(-1, CT_STRIDE)
+        out = np.zeros(ct.shape[0], np.uint8)
+        check(lib().vlp_decrypt_bits(self.sk, _u32p(ct), ct.shape[0], out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+        return out
+
+    def decrypt_value(self, ct: np.ndarray) -> int:
+        return int(sum(int(b) << j for j, b in enumerate(self.decrypt_bits(ct))))
+
+    def encrypt_db(self, m: VlpMeta, words, payloads, pk_seed: int, first: int = 0, count: int | None = None):
+        """Client PubKeyGen (alg:PubKeyGen) + server ServerEnc (alg:ServerEnc) for records [first, first+count)."""
+        words = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+        payloads = np.ascontiguousarray(np.asarray(payloads, dtype=np.uint64))
+        count = len(payloads) if count is None else count
+        pk = ctypes.c_void_p()
+        check(lib().vlp_pubkeygen(self.sk, ctypes.byref(m), pk_seed, first, count, ctypes.byref(pk)))
+        try:
+            per = record_cts(m)
+            out = np.zeros((count * per, CT_STRIDE), np.uint32)
+            check(lib().vlp_server_encrypt_db(pk, _u64p(words), _u64p(payloads), _u32p(out)))
+        finally:
+            lib().vlp_free_pk(pk)
+        return out
+
+
+def record_cts(m: VlpMeta) -> int:
+    v = ctypes.c_size_t()
+    check(lib().vlp_db_record_cts(ctypes.byref(m), ctypes.byref(v)))
+    return v.value
+
+
+class Server:
+    """vlp_server_create: the evaluation key resident on one GPU (bsk converted to the NTT domain)."""
+
+    def __init__(self, keys: Keys, device: int = 0, stream=None):
+        import torch
+        self.device = device
+        self.keys = keys
+        nbytes = lib().vlp_server_evk_bytes()
+        self.evk_dev = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            check(lib().vlp_server_create(device, keys.evk, ctypes.c_void_p(self.evk_dev.data_ptr()), nbytes,
+                                          _stream_handle(stream), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().vlp_free_server(self.h)
+        except Exception:
+            pass
+
+    def debug_blind_rotate(self, in_dev, steps: int, stream=None):
+        import torch
+        count = in_dev.shape[0]
+        acc = torch.zeros((count, 2 * L.N), dtype=torch.int32, device=in_dev.device)
+        scratch = torch.empty(max(256, lib().vlp_debug_scratch_bytes(count)), dtype=torch.uint8, device=in_dev.device)
+        check(lib().vlp_debug_blind_rotate(self.h, ctypes.c_void_p(in_dev.data_ptr()), count, steps,
+                                           ctypes.c_void_p(acc.data_ptr()), ctypes.c_void_p(scratch.data_ptr()),
+                                           _stream_handle(stream)))
+        return acc
+
+    def debug_keyswitch(self, nlwe_dev, stream=None):
+        import torch
+        count = nlwe_dev.shape[0]
+        out = torch.zeros((count, CT_STRIDE), dtype=torch.int32, device=nlwe_dev.device)
+        scratch = torch.empty(max(256, lib().vlp_debug_scratch_bytes(count)), dtype=torch.uint8, device=nlwe_dev.device)
+        check(lib().vlp_debug_keyswitch(self.h, ctypes.c_void_p(nlwe_dev.data_ptr()), count,
+                                        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(scratch.data_ptr()),
+                                        _stream_handle(stream)))
+        return out
+
+
+class Program:
+    """A compiled level schedule (vlp_program_create*), with its torch-owned scratch."""
+
+    def __init__(self, server: Server, handle: ctypes.c_void_p):
+        import torch
+        self.server = server
+        self.h = handle
+        info = VlpProgramInfo()
+        check(lib().vlp_program_get_info(self.h, ctypes.byref(info)))
+        self.info = info
+        self.scratch = torch.empty(max(256, info.scratch_bytes), dtype=torch.uint8, device=f"cuda:{server.device}")
+
+    @classmethod
+    def velopir(cls, server: Server, m: VlpMeta, first: int = 0, count: int | None = None):
+        count = m.M - first if count is None else count
+        h = ctypes.c_void_p()
+        check(lib().vlp_program_create(server.h, ctypes.byref(m), first, count, ctypes.byref(h)))
+        return cls(server, h)
+
+    @classmethod
+    def gates(cls, server: Server, op: int, count: int):
+        h = ctypes.c_void_p()
+        check(lib().vlp_program_create_gates(server.h, op, count, ctypes.byref(h)))
+        return cls(server, h)
+
+    @classmethod
+    def combine(cls, server: Server, m: VlpMeta, G: int):
+        h = ctypes.c_void_p()
+        check(lib().vlp_program_create_combine(server.h, ctypes.byref(m), G, ctypes.byref(h)))
+        return cls(server, h)
+
+    def __del__(self):
+        try:
+            lib().vlp_free_program(self.h)
+        except Exception:
+            pass
+
+    def eval(self, in0, in1, out, stream=None):
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        check(lib().vlp_program_eval(self.h, ctypes.c_void_p(self.scratch.data_ptr()), self.scratch.numel(),
+                                     p(in0), p(in1), p(out), _stream_handle(stream)))
+
+    def node_row(self, kind: int, record: int, bit: int = 0) -> int:
+        r = ctypes.c_uint64()
+        check(lib().vlp_program_node_row(self.h, kind, record, bit, ctypes.byref(r)))
+        return r.value
+
+    def intermediate(self):
+        """The intermediate-row region of the scratch as an int32 [rows, 632] view (parity dumps)."""
+        off = ctypes.c_uint64()
+        check(lib().vlp_program_intermediate_offset(self.h, ctypes.byref(off)))
+        rows = (self.scratch.numel() - off.value) // (CT_STRIDE * 4)
+        return self.scratch[off.value: off.value + rows * CT_STRIDE * 4].view(dtype=__import__("torch").int32).view(rows, CT_STRIDE)
+
+
+def to_device(ct: np.ndarray, device: int = 0):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(ct, dtype=np.uint32).view(np.int32)).to(f"cuda:{device}")
+
+
+def to_host(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)

@@ -1,0 +1,343 @@
+// api.cu -- the device half of the C ABI (include/vlp.h): server creation (evk upload + NTT conversion),
+// program compilation / binding / evaluation (one BR launch + one KS launch per circuit level),
+// and the debug entry points used by the parity tests.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+
+#include "kernels.cuh"
+
+struct vlp_server {
+  int device = 0;
+  int sm_count = 148;
+  uint8_t* evk_dev = nullptr;
+  uint32_t* bsk_ntt = nullptr;
+  uint32_t* ksk = nullptr;
+  uint2* tw_fwd = nullptr;
+  uint2* tw_inv = nullptr;
+};
+
+struct vlp_program {
+  vlp_server* server = nullptr;
+  vlp::Schedule sched;
+  // scratch layout (byte offsets)
+  size_t off_br = 0, off_ks = 0, off_outslots = 0, off_mid = 0, off_nlwe = 0, bytes = 0;
+  std::vector<size_t> br_first, ks_first;  // per level, index of the level's first job
+  std::vector<uint32_t> copy_slots;        // outputs that are not written in place
+  void* bound = nullptr;
+  uint32_t launches = 0;
+};
+
+namespace vlp {
+namespace {
+
+constexpr size_t kBskNttBytes = kBskNttWords * 4;
+constexpr size_t kKskBytes = static_cast<size_t>(N) * kKsT * 3 * kCt * 4;
+constexpr size_t kTwBytes = static_cast<size_t>(N) * sizeof(uint2);
+constexpr size_t kRawBskBytes = static_cast<size_t>(n) * kRows * 2 * N * 4;
+constexpr size_t kEvkBytes = kBskNttBytes + kKskBytes + 2 * kTwBytes + kRawBskBytes;
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(VLP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+uint64_t mulmod(uint64_t a, uint64_t b) { return a * b % kP; }
+uint64_t powmod(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  b %= kP;
+  while (e) {
+    if (e & 1) r = mulmod(r, b);
+    b = mulmod(b, b);
+    e >>= 1;
+  }
+  return r;
+}
+uint32_t bitrev10(uint32_t x) {
+  uint32_t r = 0;
+  for (int b = 0; b < 10; b++) r |= ((x >> b) & 1u) << (9 - b);
+  return r;
+}
+
+// Twiddles of the negacyclic transform mod p: psi a primitive 2N-th root of unity;
+// fwd[k] = psi^brv(k), inv[k] = psi^-brv(k), each with its Shoup companion floor(w 2^32 / p).
+void make_twiddles(std::vector<uint2>& fwd, std::vector<uint2>& inv) {
+  uint64_t psi = 0;
+  for (uint64_t g = 2; g < 1000; g++) {
+    const uint64_t x = powmod(g, (kP - 1) / (2 * N));
+    if (powmod(x, N) == kP - 1) {
+      psi = x;
+      break;
+    }
+  }
+  const uint64_t psi_inv = powmod(psi, kP - 2);
+  fwd.resize(N);
+  inv.resize(N);
+  for (uint32_t k = 0; k < static_cast<uint32_t>(N); k++) {
+    const uint64_t w = powmod(psi, bitrev10(k)), wi = powmod(psi_inv, bitrev10(k));
+    fwd[k] = make_uint2(static_cast<uint32_t>(w), static_cast<uint32_t>((w << 32) / kP));
+    inv[k] = make_uint2(static_cast<uint32_t>(wi), static_cast<uint32_t>((wi << 32) / kP));
+  }
+}
+
+Regions regions(const vlp_program* p, void* scratch, const uint32_t* in0, const uint32_t* in1, uint32_t* out) {
+  Regions r;
+  r.base[kRegIn0] = const_cast<uint32_t*>(in0);
+  r.base[kRegIn1] = const_cast<uint32_t*>(in1);
+  r.base[kRegMid] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + p->off_mid);
+  r.base[kRegOut] = out;
+  return r;
+}
+
+int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
+  Schedule& s = p->sched;
+  size_t nbr = 0, nks = 0;
+  for (auto& L : s.levels) {
+    p->br_first.push_back(nbr);
+    p->ks_first.push_back(nks);
+    nbr += L.br.size();
+    nks += L.ks.size();
+  }
+  for (uint32_t sl : s.out_slots)
+    if ((sl >> 28) != kRegOut) p->copy_slots.push_back(sl);
+  p->off_br = 0;
+  p->off_ks = align256(p->off_br + nbr * sizeof(BrJob));
+  p->off_outslots = align256(p->off_ks + nks * sizeof(KsJob));
+  p->off_mid = align256(p->off_outslots + p->copy_slots.size() * 4 + 4);
+  p->off_nlwe = align256(p->off_mid + s.mid_rows * kCt * 4);
+  p->bytes = align256(p->off_nlwe + s.nlwe_rows * kNlwe * 4);
+  p->server = server;
+  p->launches = 1 + (p->copy_slots.empty() ? 0 : 1);
+  for (auto& L : s.levels) {
+    const uint32_t tiles = static_cast<uint32_t>((L.ks.size() + kKsCt - 1) / kKsCt);
+    p->launches += (L.br.empty() ? 0 : 1) + (L.ks.empty() ? 0 : (tiles * 2 <= 2 * 148 ? 2 : 1));
+  }
+  return VLP_OK;
+}
+
+}  // namespace
+}  // namespace vlp
+
+using namespace vlp;
+
+extern "C" {
+
+size_t vlp_server_evk_bytes(void) { return kEvkBytes; }
+
+int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_bytes, uint64_t stream,
+                      vlp_server** out) {
+  if (!evk || !evk_dev || !out) return fail(VLP_EINVAL, "null argument");
+  if (evk_bytes < kEvkBytes) return fail(VLP_ENOMEM, "evk buffer too small");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(VLP_ENODEV, "no CUDA device");
+  if (cudaError_t e = cudaSetDevice(device)) return cuda_fail(e, "cudaSetDevice");
+  auto srv = std::make_unique<vlp_server>();
+  srv->device = device;
+  cudaDeviceGetAttribute(&srv->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(evk_dev);
+  srv->evk_dev = base;
+  srv->bsk_ntt = reinterpret_cast<uint32_t*>(base);
+  srv->ksk = reinterpret_cast<uint32_t*>(base + kBskNttBytes);
+  srv->tw_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes);
+  srv->tw_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes);
+  uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + 2 * kTwBytes);
+
+  std::vector<uint2> fwd, inv;
+  make_twiddles(fwd, inv);
+  set_const_twiddles(fwd.data(), inv.data());
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(srv->bsk_ntt, 0, kBskNttBytes, st))) return cuda_fail(e, "memset");
+  if ((e = cudaMemcpyAsync(srv->tw_fwd, fwd.data(), kTwBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "tw");
+  if ((e = cudaMemcpyAsync(srv->tw_inv, inv.data(), kTwBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "tw");
+  if ((e = cudaMemcpyAsync(srv->ksk, evk->ksk.data(), kKskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "ksk");
+  if ((e = cudaMemcpyAsync(raw, evk->bsk.data(), kRawBskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "bsk");
+  // Montgomery factor with N^-1 folded in: c = N^-1 * 2^32 mod p
+  const uint32_t c_mont = static_cast<uint32_t>(mulmod(powmod(N, kP - 2), (1ull << 32) % kP));
+  launch_bsk_convert(raw, srv->bsk_ntt, srv->tw_fwd, c_mont, st);
+  if ((e = cudaGetLastError())) return cuda_fail(e, "bsk convert launch");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server create");
+  *out = srv.release();
+  return VLP_OK;
+}
+
+static int finish_program(vlp_server* server, std::unique_ptr<vlp_program>& p, vlp_program** out) {
+  if (int rc = build_program(server, p)) return rc;
+  *out = p.release();
+  return VLP_OK;
+}
+
+int vlp_program_create(vlp_server* server, const vlp_meta* meta, size_t first, size_t count, vlp_program** out) {
+  if (!meta || !out) return fail(VLP_EINVAL, "null argument");  // server may be NULL: compile only
+  auto p = std::make_unique<vlp_program>();
+  if (int rc = compile_velopir(*meta, first, count, &p->sched)) return rc;
+  return finish_program(server, p, out);
+}
+
+int vlp_program_create_gates(vlp_server* server, int op, size_t count, vlp_program** out) {
+  if (!out) return fail(VLP_EINVAL, "null argument");
+  auto p = std::make_unique<vlp_program>();
+  if (int rc = compile_gates(op, count, &p->sched)) return rc;
+  return finish_program(server, p, out);
+}
+
+int vlp_program_create_combine(vlp_server* server, const vlp_meta* meta, uint32_t G, vlp_program** out) {
+  if (!meta || !out) return fail(VLP_EINVAL, "null argument");
+  auto p = std::make_unique<vlp_program>();
+  if (int rc = compile_combine(*meta, G, &p->sched)) return rc;
+  return finish_program(server, p, out);
+}
+
+int vlp_program_get_info(const vlp_program* p, vlp_program_info* info) {
+  if (!p || !info) return fail(VLP_EINVAL, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->levels = static_cast<uint32_t>(p->sched.levels.size());
+  info->br = p->sched.br;
+  info->ks = p->sched.ks;
+  info->gates = p->sched.gates;
+  info->in0_cts = p->sched.in0_cts;
+  info->in1_cts = p->sched.in1_cts;
+  info->out_cts = p->sched.out_cts;
+  info->scratch_bytes = p->bytes;
+  for (auto& L : p->sched.levels) info->max_level_br = std::max<uint64_t>(info->max_level_br, L.br.size());
+  info->kernel_launches = p->launches;
+  return VLP_OK;
+}
+
+int vlp_program_node_row(const vlp_program* p, int kind, size_t record, uint32_t bit, uint64_t* row) {
+  if (!p || !row) return fail(VLP_EINVAL, "null argument");
+  uint32_t sl;
+  if (kind == 0 && record < p->sched.v_rows.size())
+    sl = static_cast<uint32_t>(p->sched.v_rows[record]);
+  else if (kind == 1 && p->sched.l_S && record * p->sched.l_S + bit < p->sched.mask_rows.size() && bit < p->sched.l_S)
+    sl = static_cast<uint32_t>(p->sched.mask_rows[record * p->sched.l_S + bit]);
+  else
+    return fail(VLP_EINVAL, "no such node");
+  if ((sl >> 28) != kRegMid) return fail(VLP_EINVAL, "node is not in the intermediate region");
+  *row = sl & 0x0FFFFFFFu;
+  return VLP_OK;
+}
+
+int vlp_program_intermediate_offset(const vlp_program* p, uint64_t* off) {
+  if (!p || !off) return fail(VLP_EINVAL, "null argument");
+  *off = p->off_mid;
+  return VLP_OK;
+}
+
+int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const uint32_t* in0,
+                     const uint32_t* in1, uint32_t* out, uint64_t stream) {
+  if (!p || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (!p->server) return fail(VLP_EINVAL, "program was compiled without a server (compile-only)");
+  if (scratch_bytes < p->bytes) return fail(VLP_ENOMEM, "scratch too small");
+  if ((p->sched.in0_cts && !in0) || (p->sched.in1_cts && !in1) || (p->sched.out_cts && !out))
+    return fail(VLP_EINVAL, "missing input / output buffer");
+  vlp_server* s = p->server;
+  cudaError_t e;
+  if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* sc = static_cast<uint8_t*>(scratch);
+  if (p->bound != scratch) {  // upload the job arrays once per scratch buffer
+    for (size_t L = 0; L < p->sched.levels.size(); L++) {
+      const Level& lv = p->sched.levels[L];
+      if (!lv.br.empty() &&
+          (e = cudaMemcpyAsync(sc + p->off_br + p->br_first[L] * sizeof(BrJob), lv.br.data(),
+                               lv.br.size() * sizeof(BrJob), cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "upload br jobs");
+      if (!lv.ks.empty() &&
+          (e = cudaMemcpyAsync(sc + p->off_ks + p->ks_first[L] * sizeof(KsJob), lv.ks.data(),
+                               lv.ks.size() * sizeof(KsJob), cudaMemcpyHostToDevice, st)))
+        return cuda_fail(e, "upload ks jobs");
+    }
+    if (!p->copy_slots.empty() &&
+        (e = cudaMemcpyAsync(sc + p->off_outslots, p->copy_slots.data(), p->copy_slots.size() * 4,
+                             cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "upload out slots");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "upload sync");
+    p->bound = scratch;
+  }
+  const Regions reg = regions(p, scratch, in0, in1, out);
+  if ((e = launch_init_constants(reg.base[kRegMid], st))) return cuda_fail(e, "init constants");
+  uint32_t* nlwe = reinterpret_cast<uint32_t*>(sc + p->off_nlwe);
+  for (size_t L = 0; L < p->sched.levels.size(); L++) {
+    const Level& lv = p->sched.levels[L];
+    BrArgs ba{};
+    ba.jobs = reinterpret_cast<const BrJob*>(sc + p->off_br) + p->br_first[L];
+    ba.njobs = static_cast<uint32_t>(lv.br.size());
+    ba.steps = n;
+    ba.reg = reg;
+    ba.nlwe = nlwe;
+    ba.raw_acc = nullptr;
+    ba.bsk = s->bsk_ntt;
+    ba.tw_fwd = s->tw_fwd;
+    ba.tw_inv = s->tw_inv;
+    if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
+    KsArgs ka{};
+    ka.jobs = reinterpret_cast<const KsJob*>(sc + p->off_ks) + p->ks_first[L];
+    ka.njobs = static_cast<uint32_t>(lv.ks.size());
+    ka.reg = reg;
+    ka.nlwe = nlwe;
+    ka.ksk = s->ksk;
+    if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
+  }
+  if (!p->copy_slots.empty() &&
+      (e = launch_copy_rows(reinterpret_cast<const uint32_t*>(sc + p->off_outslots),
+                            static_cast<uint32_t>(p->copy_slots.size()), reg, out, st)))
+    return cuda_fail(e, "copy out");
+  return VLP_OK;
+}
+
+size_t vlp_debug_scratch_bytes(size_t count) { return align256(count * sizeof(BrJob)) + align256(count * sizeof(KsJob)); }
+
+int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, int steps, uint32_t* acc_dev,
+                           void* scratch, uint64_t stream) {
+  if (!s || !in_dev || !acc_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (steps < 0 || steps > n) return fail(VLP_EINVAL, "steps out of range");
+  cudaError_t e;
+  if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<BrJob> jobs(count);
+  for (size_t i = 0; i < count; i++) jobs[i] = BrJob{slot(kRegIn0, static_cast<uint32_t>(i)), 0, 0, 1, 0, 0, static_cast<uint32_t>(i)};
+  if ((e = cudaMemcpyAsync(scratch, jobs.data(), count * sizeof(BrJob), cudaMemcpyHostToDevice, st)))
+    return cuda_fail(e, "upload");
+  BrArgs ba{};
+  ba.jobs = static_cast<const BrJob*>(scratch);
+  ba.njobs = static_cast<uint32_t>(count);
+  ba.steps = steps;
+  ba.reg.base[kRegIn0] = const_cast<uint32_t*>(in_dev);
+  ba.raw_acc = acc_dev;
+  ba.bsk = s->bsk_ntt;
+  ba.tw_fwd = s->tw_fwd;
+  ba.tw_inv = s->tw_inv;
+  if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
+  return VLP_OK;
+}
+
+int vlp_debug_keyswitch(vlp_server* s, const uint32_t* nlwe_dev, size_t count, uint32_t* out_dev, void* scratch,
+                        uint64_t stream) {
+  if (!s || !nlwe_dev || !out_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  cudaError_t e;
+  if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<KsJob> jobs(count);
+  for (size_t i = 0; i < count; i++)
+    jobs[i] = KsJob{static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u, slot(kRegOut, static_cast<uint32_t>(i))};
+  if ((e = cudaMemcpyAsync(scratch, jobs.data(), count * sizeof(KsJob), cudaMemcpyHostToDevice, st)))
+    return cuda_fail(e, "upload");
+  KsArgs ka{};
+  ka.jobs = static_cast<const KsJob*>(scratch);
+  ka.njobs = static_cast<uint32_t>(count);
+  ka.reg.base[kRegOut] = out_dev;
+  ka.nlwe = nlwe_dev;
+  ka.ksk = s->ksk;
+  if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
+  return VLP_OK;
+}
+
+void vlp_free_server(vlp_server* s) { delete s; }
+void vlp_free_program(vlp_program* p) { delete p; }
+
+}  // extern "C"

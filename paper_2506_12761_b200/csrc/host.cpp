@@ -1,0 +1,280 @@
+// host.cpp -- client-side and preprocessing calls of the C ABI (include/vlp.h): parameters, KeyGen,
+// TLWE encryption / decryption, PubKeyGen, ServerEnc.  Host C++, deterministic in the seeds (R3).
+//
+// Independent of the test oracle (oracle/): same published conventions, separate
+// code.  The ring products a*z of KeyGen are computed here as sums of rotations X^j * a over the
+// support of the binary key z (the oracle uses an NTT), and are exact mod 2^32.
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "vlp_internal.h"
+
+namespace vlp {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+// splitmix64 finalizer of (x + golden gamma); H = mix(mix(mix(seed ^ dom*C1) ^ obj*C2) ^ word*C3)
+static inline uint64_t mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+uint64_t prng(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word) {
+  uint64_t h = mix(seed ^ (dom * 0x9E3779B97F4A7C15ull));
+  h = mix(h ^ (obj * 0xC2B2AE3D27D4EB4Full));
+  return mix(h ^ (word * 0x165667B19E3779F9ull));
+}
+
+// Box-Muller Gaussian, "N(0, sigma)" (R2, R3); scalar glibc libm, no FMA contraction.
+uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
+  const uint64_t w1 = prng(seed, dom, obj, 2 * t), w2 = prng(seed, dom, obj, 2 * t + 1);
+  const double u1 = (static_cast<double>(w1 >> 11) + 1.0) * 0x1p-53;
+  const double u2 = static_cast<double>(w2 >> 11) * 0x1p-53;
+  const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+  const long long e = std::llround(z * (sigma * 4294967296.0));
+  return static_cast<uint32_t>(static_cast<uint64_t>(e));
+}
+
+static inline uint32_t uniform(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word) {
+  return static_cast<uint32_t>(prng(seed, dom, obj, word) >> 32);
+}
+
+// TLWE sample: a_i uniform (dom_a, obj, word i), b = <a, s> + mu + e (dom_e, obj, pair 0).
+static void tlwe_sample(const uint32_t* s, uint32_t mu, double sigma, uint64_t seed, uint64_t dom_a,
+                        uint64_t dom_e, uint64_t obj, uint32_t* ct) {
+  uint32_t b = 0;
+  for (int i = 0; i < n; i++) {
+    ct[i] = uniform(seed, dom_a, obj, i);
+    b += ct[i] * s[i];
+  }
+  ct[n] = b + mu + noise(seed, dom_e, obj, 0, sigma);
+  ct[n + 1] = 0;
+}
+
+template <class F>
+static void parallel_for(size_t count, F&& fn) {
+  unsigned hw = std::thread::hardware_concurrency();
+  size_t nt = std::max<size_t>(1, std::min<size_t>(hw ? hw : 4, (count + 63) / 64));
+  if (nt == 1) {
+    for (size_t i = 0; i < count; i++) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < nt; t++)
+    th.emplace_back([&, t] {
+      for (size_t i = t; i < count; i += nt) fn(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+int check_meta(const vlp_meta* m) {
+  if (!m) return fail(VLP_EINVAL, "meta is NULL");
+  if (m->mode > VLP_MODE_IDM) return fail(VLP_EMODE, "unknown mode");
+  if (m->l_I < 2 || m->l_I > 32 || m->l_S < 1 || m->l_S > 64)
+    return fail(VLP_EWIDTH, "l_I must be in [2, 32] and l_S in [1, 64]");
+  if (m->mode == VLP_MODE_IDM ? m->d != 1 : (m->d < 1 || m->d > 2)) return fail(VLP_EMODE, "bad d for mode");
+  if (m->M < 1) return fail(VLP_EINVAL, "M must be >= 1");
+  return VLP_OK;
+}
+
+}  // namespace vlp
+
+using namespace vlp;
+
+extern "C" {
+
+const char* vlp_last_error(void) { return g_err.c_str(); }
+
+int vlp_params_tfhe128(vlp_params* p) {
+  if (!p) return fail(VLP_EINVAL, "params is NULL");
+  *p = vlp_params{630, 1024, 1, 7, 3, 2, 8, 0x1p-15, 0x1p-25, 0x1p-15};
+  return VLP_OK;
+}
+
+int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk** evk_out) {
+  if (!sk_out || !evk_out) return fail(VLP_EINVAL, "null output");
+  vlp_params p;
+  vlp_params_tfhe128(&p);
+  if (params) {
+    if (params->n != 630 || params->N != 1024 || params->k != 1 || params->bg_bits != 7 || params->ell != 3 ||
+        params->ks_base_bits != 2 || params->ks_t != 8)
+      return fail(VLP_EINVAL, "only the 128-bit parameter set of tab:tfhe_params is supported");
+    p = *params;
+  }
+  vlp_sk* sk = new (std::nothrow) vlp_sk;
+  vlp_evk* evk = new (std::nothrow) vlp_evk;
+  if (!sk || !evk) return fail(VLP_ENOMEM, "out of memory");
+  sk->params = p;
+  evk->params = p;
+  for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(prng(seed, kSkLwe, 0, i) >> 63);
+  for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(prng(seed, kSkRing, 0, j) >> 63);
+  std::vector<int> support;
+  for (int j = 0; j < N; j++)
+    if (sk->z[j]) support.push_back(j);
+
+  // bsk_i row r = u*3 + j: (a, a*z + e) + s_i * g_j on component u's constant term (R4, O7).
+  evk->bsk.assign(static_cast<size_t>(n) * kRows * 2 * N, 0);
+  parallel_for(static_cast<size_t>(n) * kRows, [&](size_t ir) {
+    const uint64_t obj = ir;
+    uint32_t* a = evk->bsk.data() + ir * 2 * N;
+    uint32_t* b = a + N;
+    for (int j = 0; j < N; j++) a[j] = uniform(seed, kBskA, obj, j);
+    // a*z = sum_{k in supp z} X^k * a  (negacyclic: coefficient i moves to i+k, negated past N)
+    for (int j = 0; j < N; j++) b[j] = 0;
+    for (int k : support) {
+      for (int i = 0; i < N - k; i++) b[i + k] += a[i];
+      for (int i = N - k; i < N; i++) b[i + k - N] -= a[i];
+    }
+    for (int j = 0; j < N; j++) b[j] += noise(seed, kBskE, obj, j, p.sigma_bk);
+    const int i = static_cast<int>(ir / kRows), r = static_cast<int>(ir % kRows);
+    if (sk->s[i]) (r / kEll == 0 ? a : b)[0] += 1u << (32 - kBgBits * (r % kEll + 1));
+  });
+
+  // ksk[i][j][v] = TLWE_s(v z_i 2^(32-2(j+1))), sigma_ks (R6, O10).
+  evk->ksk.assign(static_cast<size_t>(N) * kKsT * 3 * kCt, 0);
+  parallel_for(static_cast<size_t>(N) * kKsT * 3, [&](size_t idx) {
+    const int i = static_cast<int>(idx / (kKsT * 3)), j = static_cast<int>((idx / 3) % kKsT);
+    const uint32_t v = static_cast<uint32_t>(idx % 3) + 1;
+    const uint32_t mu = v * sk->z[i] * (1u << (32 - kKsBaseBits * (j + 1)));
+    tlwe_sample(sk->s, mu, p.sigma_ks, seed, kKskA, kKskE, idx, evk->ksk.data() + idx * kCt);
+  });
+  *sk_out = sk;
+  *evk_out = evk;
+  return VLP_OK;
+}
+
+int vlp_sk_export(const vlp_sk* sk, uint32_t* s, uint32_t* z) {
+  if (!sk) return fail(VLP_EINVAL, "sk is NULL");
+  if (s) std::memcpy(s, sk->s, sizeof(sk->s));
+  if (z) std::memcpy(z, sk->z, sizeof(sk->z));
+  return VLP_OK;
+}
+
+int vlp_evk_export(const vlp_evk* evk, uint32_t* bsk, uint32_t* ksk) {
+  if (!evk) return fail(VLP_EINVAL, "evk is NULL");
+  if (bsk) std::memcpy(bsk, evk->bsk.data(), evk->bsk.size() * 4);
+  if (ksk)
+    for (size_t r = 0; r < static_cast<size_t>(N) * kKsT * 3; r++)
+      std::memcpy(ksk + r * (n + 1), evk->ksk.data() + r * kCt, (n + 1) * 4);
+  return VLP_OK;
+}
+
+int vlp_encrypt_bits(const vlp_sk* sk, const uint8_t* bits, size_t count, uint64_t seed, uint64_t obj0,
+                     uint32_t* out) {
+  if (!sk || (!bits && count) || (!out && count)) return fail(VLP_EINVAL, "null argument");
+  parallel_for(count, [&](size_t i) {
+    tlwe_sample(sk->s, bits[i] ? kMu : 0u - kMu, sk->params.sigma_lwe, seed, kFreshA, kFreshE, obj0 + i,
+                out + i * kCt);
+  });
+  return VLP_OK;
+}
+
+int vlp_encrypt_query(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint64_t seed,
+                      uint32_t* out) {
+  if (!sk || !values || !out) return fail(VLP_EINVAL, "null argument");
+  if (int rc = check_meta(meta)) return rc;
+  const size_t W = query_words(*meta), l = meta->l_I;
+  for (size_t w = 0; w < W; w++)
+    if (l < 64 && values[w] >> l) return fail(VLP_ERANGE, "query value >= 2^l_I");
+  parallel_for(W * l, [&](size_t idx) {
+    const size_t w = idx / l, j = idx % l;
+    const uint32_t bit = static_cast<uint32_t>((values[w] >> j) & 1);
+    tlwe_sample(sk->s, bit ? kMu : 0u - kMu, sk->params.sigma_lwe, seed, kQryA, kQryE, idx, out + idx * kCt);
+  });
+  return VLP_OK;
+}
+
+int vlp_decrypt_bits(const vlp_sk* sk, const uint32_t* ct, size_t count, uint8_t* bits) {
+  if (!sk || (count && (!ct || !bits))) return fail(VLP_EINVAL, "null argument");
+  for (size_t c = 0; c < count; c++) {
+    const uint32_t* x = ct + c * kCt;
+    uint32_t dot = 0;
+    for (int i = 0; i < n; i++) dot += x[i] * sk->s[i];
+    bits[c] = static_cast<int32_t>(x[n] - dot) > 0 ? 1 : 0;
+  }
+  return VLP_OK;
+}
+
+int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record) {
+  if (int rc = check_meta(meta)) return rc;
+  if (!per_record) return fail(VLP_EINVAL, "null output");
+  *per_record = record_words(*meta) * meta->l_I + meta->l_S;
+  return VLP_OK;
+}
+
+int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                  vlp_pk** out) {
+  if (!sk || !out) return fail(VLP_EINVAL, "null argument");
+  if (int rc = check_meta(meta)) return rc;
+  if (first + count > meta->M) return fail(VLP_EINVAL, "record range exceeds M");
+  vlp_pk* pk = new (std::nothrow) vlp_pk;
+  if (!pk) return fail(VLP_ENOMEM, "out of memory");
+  pk->meta = *meta;
+  pk->first = first;
+  pk->count = count;
+  const size_t W = record_words(*meta), lI = meta->l_I, lS = meta->l_S, per = W * lI + lS;
+  try {
+    pk->samples.assign(count * per * kCt, 0);
+  } catch (...) {
+    delete pk;
+    return fail(VLP_ENOMEM, "out of memory for pk samples");
+  }
+  // Row order of a record: word k bit j at k*l_I + j, then payload bit j.  PRNG object of each sample:
+  // record i, local index j*W + k (pk^I, bit j outer / word k inner as alg:PubKeyGen P:200-209) or
+  // W*l_I + j (pk^S); obj = i*per + local.
+  parallel_for(count * per, [&](size_t idx) {
+    const size_t rec = idx / per, row = idx % per, i = first + rec;
+    size_t local;
+    if (row < W * lI) {
+      const size_t k = row / lI, j = row % lI;
+      local = j * W + k;
+    } else {
+      local = row;  // W*l_I + j
+    }
+    tlwe_sample(sk->s, 0u, sk->params.sigma_lwe, seed, kPkA, kPkE, i * per + local,
+                pk->samples.data() + idx * kCt);
+  });
+  *out = pk;
+  return VLP_OK;
+}
+
+int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* out) {
+  if (!pk || !out || (pk->count && (!words || !payloads))) return fail(VLP_EINVAL, "null argument");
+  if (pk->used) return fail(VLP_EPKUSED, "public-key samples already used (single-use, alg:PubKeyGen)");
+  const vlp_meta& m = pk->meta;
+  const size_t W = record_words(m), lI = m.l_I, lS = m.l_S, per = W * lI + lS;
+  for (size_t r = 0; r < pk->count; r++) {
+    for (size_t k = 0; k < W; k++)
+      if (lI < 64 && words[r * W + k] >> lI) return fail(VLP_ERANGE, "record word >= 2^l_I");
+    if (lS < 64 && payloads[r] >> lS) return fail(VLP_ERANGE, "payload >= 2^l_S");
+  }
+  parallel_for(pk->count * per, [&](size_t idx) {
+    const size_t rec = idx / per, row = idx % per;
+    uint32_t bit;
+    if (row < W * lI)
+      bit = static_cast<uint32_t>((words[rec * W + row / lI] >> (row % lI)) & 1);
+    else
+      bit = static_cast<uint32_t>((payloads[rec] >> (row - W * lI)) & 1);
+    const uint32_t* s = pk->samples.data() + idx * kCt;
+    uint32_t* d = out + idx * kCt;
+    std::memcpy(d, s, kCt * 4);
+    d[n] += bit ? kMu : 0u - kMu;  // (0, Ecd(bit)) + pk
+  });
+  pk->used = true;
+  pk->samples.clear();
+  pk->samples.shrink_to_fit();
+  return VLP_OK;
+}
+
+void vlp_free_sk(vlp_sk* sk) { delete sk; }
+void vlp_free_evk(vlp_evk* evk) { delete evk; }
+void vlp_free_pk(vlp_pk* pk) { delete pk; }
+
+}  // extern "C"

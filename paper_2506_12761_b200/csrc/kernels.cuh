@@ -1,0 +1,63 @@
+// kernels.cuh -- device-side declarations shared by kernels.cu and api.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "vlp_internal.h"
+
+namespace vlp {
+
+// ---- blind rotation (K2): 4 bootstraps per CTA in lock-step, 64 threads each
+constexpr int kBrBoot = 4;                          // bootstraps per CTA
+constexpr int kBrThreads = 64 * kBrBoot;            // 256
+constexpr int kChunks = 8;                          // bsk chunks per CMux step
+constexpr int kChunkWords = 76;                     // words per thread per chunk (72 used + pad)
+constexpr int kChunkBytes = 64 * kChunkWords * 4;   // 19456
+constexpr int kSlots = 6;                           // smem ring of bsk chunks
+constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * 64 * kChunkWords;  // 24,514,560
+constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
+                             kBrBoot * 640 * 2 + kSlots * 8;
+
+// ---- key switch (K3)
+constexpr int kKsCt = 16;                                 // ciphertexts per CTA
+constexpr int kKsThreads = 160;                           // 158 column quads (632 words)
+constexpr int kKsRowWords = kKsT * 3 * kCt;               // ksk words per coefficient i: 15168
+constexpr int kKsSmemBytes = 2 * kKsRowWords * 4 + kKsCt * N * 2 + 2 * 8;
+
+struct Regions {
+  uint32_t* base[4];  // kRegIn0, kRegIn1, kRegMid, kRegOut; rows of kCt words
+};
+
+struct BrArgs {
+  const BrJob* jobs;
+  uint32_t njobs;
+  int steps;          // CMux steps to run (n normally; fewer for the step-level parity tests)
+  Regions reg;
+  uint32_t* nlwe;     // [rows][kNlwe] output of extract (unless raw_acc)
+  uint32_t* raw_acc;  // debug: [njobs][2][N] accumulators instead of extracting
+  const uint32_t* bsk;  // NTT-domain bsk, layout [i][chunk][t][kChunkWords]
+  const uint2* tw_fwd;  // [N] (w, floor(w 2^32 / p))
+  const uint2* tw_inv;
+};
+
+struct KsArgs {
+  const KsJob* jobs;
+  uint32_t njobs;
+  Regions reg;
+  const uint32_t* nlwe;  // [rows][kNlwe]
+  const uint32_t* ksk;   // [N][8][3][kCt]
+  int parts;             // coefficient-range splits (gridDim.y)
+};
+
+void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd, uint32_t c_mont,
+                        cudaStream_t st);
+void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
+cudaError_t launch_blind_rotate(const BrArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_keyswitch(const KsArgs& a, cudaStream_t st);
+cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st);
+cudaError_t launch_copy_rows(const uint32_t* slots, uint32_t count, Regions reg, uint32_t* out, cudaStream_t st);
+int br_grid(uint32_t njobs, int sm_count);
+
+}  // namespace vlp

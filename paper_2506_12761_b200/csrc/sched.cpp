@@ -1,0 +1,261 @@
+// sched.cpp -- the gate-level scheduler: compiles VeLoPIR's circuits for a shard of
+// records into a list of levels; each level is one batched blind-rotate launch plus one batched
+// key-switch launch over every independent gate of that level across all records.
+//
+// Circuits, written from the paper's listings:
+//   HomCompLE / HomCompL  alg:HomCompLE, alg:HomCompL; R11 UNSIGNED selects ct2[l-1]
+//   HomEQ / HomEqOPT      alg:HomEQ, alg:HomEquiOPT, R14
+//   IntV                  alg:InterValid, R12 CLOSED_UPPER, R13 (d = 2 rectangle)
+//   CoV / IdM             alg:BB2
+//   mask                  alg:HomBitwiseAND, R16
+//   aggregation           alg:HomSum or the pairwise tree, R15, R19
+// Level assignment is ASAP on the gate DAG.  A MUX (R10) is two blind rotations, each depending on
+// the selector and ONE data input, plus one key switch: each half is scheduled as soon as its own inputs
+// exist (the data-independent half of every comparator-ladder MUX is hoisted), the key switch when both
+// halves are done.  Ciphertexts do not depend on the schedule: every gate is a pure function of its
+// inputs and the evaluation key.
+#include <algorithm>
+#include <cstring>
+
+#include "vlp_internal.h"
+
+namespace vlp {
+namespace {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+struct LinForm {
+  uint32_t k0;
+  int8_t ax, ay;
+};
+// S2 / R10 linear forms: c = (0, k0) + ax*x + ay*y.
+LinForm form(int op) {
+  switch (op) {
+    case VLP_AND: return {0xE0000000u, 1, 1};
+    case VLP_NAND: return {0x20000000u, -1, -1};
+    case VLP_OR: return {0x20000000u, 1, 1};
+    case VLP_XOR: return {0x40000000u, 2, 2};
+    default: return {0xC0000000u, -2, -2};  // XNOR
+  }
+}
+
+struct Node {
+  uint8_t kind;  // 0 leaf, 1 gate, 2 mux
+  uint8_t op;
+  uint32_t in[3];
+  uint32_t level;      // level at which the output exists (0 for leaves)
+  uint32_t h1, h2;     // MUX half levels
+  uint32_t slot;       // leaf: fixed slot id; gate: assigned at finalize
+};
+
+class Builder {
+ public:
+  std::vector<Node> nodes;
+  uint32_t leaf(uint32_t slot_id) {
+    nodes.push_back(Node{0, 0, {kNone, kNone, kNone}, 0, 0, 0, slot_id});
+    return static_cast<uint32_t>(nodes.size() - 1);
+  }
+  uint32_t konst(int bit) {  // trivial (0, +-1/8): rows 0 / 1 of the intermediate region (R21)
+    uint32_t& c = bit ? one_ : zero_;
+    if (c == kNone) c = leaf(slot(kRegMid, bit ? 1 : 0));
+    return c;
+  }
+  uint32_t gate(int op, uint32_t x, uint32_t y) {
+    const uint32_t l = std::max(nodes[x].level, nodes[y].level) + 1;
+    nodes.push_back(Node{1, static_cast<uint8_t>(op), {x, y, kNone}, l, 0, 0, kNone});
+    return static_cast<uint32_t>(nodes.size() - 1);
+  }
+  // MUX(c, a, b) = c ? a : b (R10)
+  uint32_t mux(uint32_t c, uint32_t a, uint32_t b) {
+    const uint32_t h1 = std::max(nodes[c].level, nodes[a].level) + 1;
+    const uint32_t h2 = std::max(nodes[c].level, nodes[b].level) + 1;
+    nodes.push_back(Node{2, VLP_MUX, {c, a, b}, std::max(h1, h2), h1, h2, kNone});
+    return static_cast<uint32_t>(nodes.size() - 1);
+  }
+  uint32_t AND(uint32_t x, uint32_t y) { return gate(VLP_AND, x, y); }
+  uint32_t OR(uint32_t x, uint32_t y) { return gate(VLP_OR, x, y); }
+  uint32_t XOR(uint32_t x, uint32_t y) { return gate(VLP_XOR, x, y); }
+  uint32_t XNOR(uint32_t x, uint32_t y) { return gate(VLP_XNOR, x, y); }
+
+  // Assign slots (outputs listed in `outs` go to the out region, in order) and emit the levels.
+  void finalize(const std::vector<uint32_t>& outs, Schedule* s) {
+    std::vector<uint32_t> out_index(nodes.size(), kNone);
+    for (size_t j = 0; j < outs.size(); j++)
+      if (nodes[outs[j]].kind != 0) out_index[outs[j]] = static_cast<uint32_t>(j);
+    uint32_t mid = 2, nl = 0, maxl = 0;
+    for (size_t i = 0; i < nodes.size(); i++) {
+      Node& nd = nodes[i];
+      if (nd.kind == 0) continue;
+      nd.slot = out_index[i] != kNone ? slot(kRegOut, out_index[i]) : slot(kRegMid, mid++);
+      maxl = std::max(maxl, nd.level);
+    }
+    s->levels.assign(maxl, Level{});
+    for (auto& nd : nodes) {
+      if (nd.kind == 1) {
+        const LinForm f = form(nd.op);
+        const uint32_t row = nl++;
+        s->levels[nd.level - 1].br.push_back(BrJob{nodes[nd.in[0]].slot, nodes[nd.in[1]].slot, f.k0, f.ax, f.ay, 0, row});
+        s->levels[nd.level - 1].ks.push_back(KsJob{row, kNone, 0u, nd.slot});
+        s->gates++;
+        s->br++;
+        s->ks++;
+      } else if (nd.kind == 2) {
+        const uint32_t r1 = nl++, r2 = nl++;
+        const uint32_t c = nodes[nd.in[0]].slot, a = nodes[nd.in[1]].slot, b = nodes[nd.in[2]].slot;
+        // BR_N((0,-1/8) + c + a) and BR_N((0,-1/8) - c + b); KS((0,1/8) + u1 + u2)
+        s->levels[nd.h1 - 1].br.push_back(BrJob{c, a, 0xE0000000u, 1, 1, 0, r1});
+        s->levels[nd.h2 - 1].br.push_back(BrJob{c, b, 0xE0000000u, -1, 1, 0, r2});
+        s->levels[nd.level - 1].ks.push_back(KsJob{r1, r2, kMu, nd.slot});
+        s->gates++;
+        s->br += 2;
+        s->ks++;
+      }
+    }
+    s->mid_rows = mid;
+    s->nlwe_rows = nl;
+    s->out_cts = outs.size();
+    for (uint32_t o : outs) s->out_slots.push_back(nodes[o].slot);
+  }
+
+ private:
+  uint32_t zero_ = kNone, one_ = kNone;
+};
+
+using Word = std::vector<uint32_t>;  // bit ciphertexts, LSB first (R20)
+
+// alg:HomCompLE / alg:HomCompL: ladder init trivial Enc(1) / Enc(0).
+uint32_t comp(Builder& B, const Word& c1, const Word& c2, int l, bool le, bool uns) {
+  const uint32_t t0 = B.XOR(c1[l - 1], c2[l - 1]);
+  uint32_t t2 = B.konst(le ? 1 : 0);
+  for (int i = 0; i <= l - 2; i++) {
+    const uint32_t t1 = B.XNOR(c1[i], c2[i]);
+    t2 = B.mux(t1, t2, c2[i]);
+  }
+  return B.mux(t0, uns ? c2[l - 1] : c1[l - 1], t2);
+}
+
+// alg:HomEQ and alg:HomEquiOPT.
+uint32_t eq(Builder& B, const Word& c1, const Word& c2, int l, bool tree) {
+  if (!tree) {
+    uint32_t r = B.konst(1);
+    for (int i = 0; i < l; i++) r = B.AND(r, B.XNOR(c1[i], c2[i]));
+    return r;
+  }
+  std::vector<uint32_t> t(l);
+  for (int i = 0; i < l; i++) t[i] = B.XNOR(c1[i], c2[i]);
+  for (int k = 1; k < l; k *= 2)
+    for (int i = 0; i < l; i += 2 * k)
+      if (i + k < l) t[i] = B.AND(t[i], t[i + k]);
+  return t[0];
+}
+
+uint32_t validate(Builder& B, const vlp_meta& m, const std::vector<Word>& q, const std::vector<Word>& rec) {
+  const int l = static_cast<int>(m.l_I);
+  const bool uns = m.flags & VLP_F_UNSIGNED, closed = m.flags & VLP_F_CLOSED_UPPER, tree = m.flags & VLP_F_EQ_TREE;
+  if (m.mode == VLP_MODE_INTV) {  // alg:InterValid, operand order of P:342-346
+    const uint32_t v_xl = comp(B, rec[0], q[0], l, true, uns);
+    const uint32_t v_xr = comp(B, q[0], rec[1], l, closed, uns);
+    if (m.d == 1) return B.AND(v_xl, v_xr);
+    const uint32_t v_yl = comp(B, rec[2], q[1], l, true, uns);
+    const uint32_t v_yr = comp(B, q[1], rec[3], l, closed, uns);
+    const uint32_t v_x = B.AND(v_xl, v_xr);
+    const uint32_t v_y = B.AND(v_yl, v_yr);
+    return B.AND(v_x, v_y);
+  }
+  if (m.mode == VLP_MODE_COV) {  // alg:BB2
+    const uint32_t v_x = eq(B, q[0], rec[0], l, tree);
+    const uint32_t v_y = eq(B, q[1], rec[1], l, tree);
+    return B.AND(v_x, v_y);
+  }
+  return eq(B, q[0], rec[0], l, tree);  // IdM
+}
+
+// HomSum tree (R15) or serial alg:HomSum; XOR or OR (R19).  Returns the root word.
+Word aggregate(Builder& B, std::vector<Word> S, size_t l_S, uint32_t flags) {
+  const int op = (flags & VLP_F_OR_REDUCE) ? VLP_OR : VLP_XOR;
+  const size_t M = S.size();
+  if (flags & VLP_F_SUM_TREE) {
+    for (size_t k = 1; k < M; k *= 2)
+      for (size_t i = 0; i < M; i += 2 * k)
+        if (i + k < M)
+          for (size_t j = 0; j < l_S; j++) S[i][j] = B.gate(op, S[i][j], S[i + k][j]);
+    return S[0];
+  }
+  Word R(l_S);
+  for (size_t j = 0; j < l_S; j++) R[j] = B.konst(0);
+  for (size_t i = 0; i < M; i++)
+    for (size_t j = 0; j < l_S; j++) R[j] = B.gate(op, R[j], S[i][j]);
+  return R;
+}
+
+}  // namespace
+
+int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s) {
+  if (int rc = check_meta(&m)) return rc;
+  if (count == 0 || first + count > m.M) return fail(VLP_EINVAL, "bad record range");
+  Builder B;
+  const size_t l = m.l_I, W = record_words(m), QW = query_words(m), per = W * l + m.l_S;
+  std::vector<Word> q(QW, Word(l));
+  for (size_t w = 0; w < QW; w++)
+    for (size_t j = 0; j < l; j++) q[w][j] = B.leaf(slot(kRegIn0, static_cast<uint32_t>(w * l + j)));
+  std::vector<Word> masked(count);
+  std::vector<uint32_t> vs(count);
+  for (size_t r = 0; r < count; r++) {  // alg:VeLoPIR record loop
+    const uint32_t base = static_cast<uint32_t>(r * per);
+    std::vector<Word> rec(W, Word(l));
+    for (size_t k = 0; k < W; k++)
+      for (size_t j = 0; j < l; j++) rec[k][j] = B.leaf(slot(kRegIn1, base + static_cast<uint32_t>(k * l + j)));
+    const uint32_t v = validate(B, m, q, rec);
+    vs[r] = v;
+    masked[r].resize(m.l_S);
+    for (size_t j = 0; j < m.l_S; j++)  // alg:HomBitwiseAND with the record's own v (R16)
+      masked[r][j] = B.AND(v, B.leaf(slot(kRegIn1, base + static_cast<uint32_t>(W * l + j))));
+  }
+  const Word root = aggregate(B, masked, m.l_S, m.flags);
+  B.finalize(root, s);
+  s->in0_cts = QW * l;
+  s->in1_cts = count * per;
+  s->l_S = m.l_S;
+  for (size_t r = 0; r < count; r++) {
+    s->v_rows.push_back(B.nodes[vs[r]].slot);
+    for (size_t j = 0; j < m.l_S; j++) s->mask_rows.push_back(B.nodes[masked[r][j]].slot);
+  }
+  return VLP_OK;
+}
+
+int compile_gates(int op, size_t count, Schedule* s) {
+  if (op < VLP_AND || op > VLP_MUX) return fail(VLP_EINVAL, "bad gate op");
+  if (count == 0 || count >= (1u << 27)) return fail(VLP_EINVAL, "bad gate count");
+  Builder B;
+  std::vector<uint32_t> outs(count);
+  for (size_t i = 0; i < count; i++) {
+    const uint32_t a = B.leaf(slot(kRegIn0, static_cast<uint32_t>(i)));
+    const uint32_t b = B.leaf(slot(kRegIn1, static_cast<uint32_t>(i)));
+    if (op == VLP_MUX)
+      outs[i] = B.mux(a, b, B.leaf(slot(kRegIn1, static_cast<uint32_t>(count + i))));
+    else
+      outs[i] = B.gate(op, a, b);
+  }
+  B.finalize(outs, s);
+  s->in0_cts = count;
+  s->in1_cts = op == VLP_MUX ? 2 * count : count;
+  return VLP_OK;
+}
+
+int compile_combine(const vlp_meta& m, uint32_t G, Schedule* s) {
+  if (int rc = check_meta(&m)) return rc;
+  if (G < 1 || (G & (G - 1))) return fail(VLP_EINVAL, "G must be a power of two");
+  Builder B;
+  std::vector<Word> S(G, Word(m.l_S));
+  for (uint32_t g = 0; g < G; g++)
+    for (size_t j = 0; j < m.l_S; j++) S[g][j] = B.leaf(slot(kRegIn0, static_cast<uint32_t>(g * m.l_S + j)));
+  vlp_meta mm = m;
+  mm.flags |= VLP_F_SUM_TREE;  // shard roots combine with the same pairing (R15)
+  const Word root = aggregate(B, S, m.l_S, mm.flags);
+  B.finalize(root, s);
+  s->in0_cts = static_cast<uint64_t>(G) * m.l_S;
+  s->l_S = m.l_S;
+  return VLP_OK;
+}
+
+}  // namespace vlp

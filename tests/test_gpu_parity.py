@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bit-exact everywhere (all arithmetic is integer: torus32 and the NTT primes).  Sizes span several CTAs
+(4 bootstraps each) with ragged tails; full-size configs are checked on sampled outputs the oracle
+recomputes one by one plus properties that hold at any size (decrypted predicate, all-trivial closed
+form P11)."""
+import os
+import random
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from oracle import circuits as OC  # noqa: E402
+from oracle import protocol as OP  # noqa: E402
+from paper_2506_12761_b200 import _lib as L  # noqa: E402
+from paper_2506_12761_b200 import api as A  # noqa: E402
+from synth import make_workload, nand_inputs  # noqa: E402
+
+POOL = ThreadPoolExecutor(max_workers=max(4, os.cpu_count() or 4))
+SEED = 123
+
+
+@pytest.fixture(scope="module")
+def gkeys():
+    return A.Keys(SEED)
+
+
+@pytest.fixture(scope="module")
+def server(gkeys):
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return A.Server(gkeys, 0)
+
+
+def rand_tlwe(rng, count):
+    return rng.integers(0, 2 ** 32, (count, 632), dtype=np.uint64).astype(np.uint32)
+
+
+def test_blind_rotate_steps_bit_exact(server, okeys):
+    """K2 after 1, 2 and 7 CMux steps (raw TRLWE accumulator) == oracle BlindRotate, 9 inputs (3 CTAs,
+    ragged), uniformly random masks (every abar_i != 0 path) plus one trivial input."""
+    rng = np.random.default_rng(1)
+    cts = rand_tlwe(rng, 9)
+    cts[:, 631] = 0
+    cts[4, :630] = 0
+    dev = A.to_device(cts)
+    for steps in (1, 2, 7):
+        got = A.to_host(server.debug_blind_rotate(dev, steps))
+        want = list(POOL.map(lambda c: okeys.blind_rotate(c[:631], steps), cts))
+        for i in range(len(cts)):
+            assert np.array_equal(got[i], want[i]), (steps, i, np.flatnonzero(got[i] != want[i])[:8])
+
+
+def test_blind_rotate_full_bit_exact(server, okeys):
+    """All 630 steps on 5 fresh encryptions (a ragged group of 4 + 1)."""
+    cts = server.keys.encrypt_bits([1, 0, 1, 1, 0], 91)
+    got = A.to_host(server.debug_blind_rotate(A.to_device(cts), 630))
+    want = list(POOL.map(lambda c: okeys.blind_rotate(c[:631], 630), cts))
+    for i in range(5):
+        assert np.array_equal(got[i], want[i]), i
+
+
+@pytest.mark.parametrize("count", [1, 17, 70])
+def test_keyswitch_bit_exact(server, okeys, count):
+    """K3 on random N-LWE rows: 1 (16 coefficient splits), 17 (2 tiles, ragged), 70 (5 tiles)."""
+    rng = np.random.default_rng(count)
+    nl = rng.integers(0, 2 ** 32, (count, 1028), dtype=np.uint64).astype(np.uint32)
+    nl[:, 1025:] = 0
+    got = A.to_host(server.debug_keyswitch(A.to_device(nl)))
+    want = list(POOL.map(lambda r: okeys.keyswitch(r[:1025]), nl))
+    for i in range(count):
+        assert np.array_equal(got[i, :631], want[i]), i
+        assert got[i, 631] == 0
+
+
+def _gate_program(server, op, a, b, c=None):
+    count = a.shape[0]
+    prog = A.Program.gates(server, op, count)
+    in1 = b if c is None else np.concatenate([b, c])
+    out = torch.zeros((count, 632), dtype=torch.int32, device="cuda:0")
+    prog.eval(A.to_device(a), A.to_device(in1), out)
+    torch.cuda.synchronize()
+    return A.to_host(out)
+
+
+@pytest.mark.parametrize("op", [L.AND, L.NAND, L.OR, L.XOR, L.XNOR, L.MUX])
+def test_gate_batches_bit_exact(server, okeys, op):
+    """Every gate type on 13 fresh input pairs (4 CTAs, ragged): ciphertexts byte-equal to the oracle's
+    gates, decrypting to the truth table (R10)."""
+    count = 13
+    rng = np.random.default_rng(op)
+    bits = rng.integers(0, 2, (3, count), dtype=np.uint8)
+    k = server.keys
+    a = k.encrypt_bits(bits[0], 500 + op, 0)
+    b = k.encrypt_bits(bits[1], 600 + op, 0)
+    c = k.encrypt_bits(bits[2], 700 + op, 0) if op == L.MUX else None
+    got = _gate_program(server, op, a, b, c)
+    if op == L.MUX:
+        want = list(POOL.map(lambda i: okeys.mux(a[i, :631], b[i, :631], c[i, :631]), range(count)))
+        truth = np.where(bits[0] == 1, bits[1], bits[2])
+    else:
+        want = list(POOL.map(lambda i: okeys.gate(op, a[i, :631], b[i, :631]), range(count)))
+        f = {L.AND: lambda x, y: x & y, L.NAND: lambda x, y: 1 - (x & y), L.OR: lambda x, y: x | y,
+             L.XOR: lambda x, y: x ^ y, L.XNOR: lambda x, y: 1 - (x ^ y)}[op]
+        truth = f(bits[0], bits[1])
+    for i in range(count):
+        assert np.array_equal(got[i, :631], want[i]), i
+    assert np.array_equal(k.decrypt_bits(got), truth)
+
+
+def test_nand_batch_sampled(server, okeys):
+    """Config 5 shape at 2^12 + 37 gates (ragged): every output decrypts to NAND; 24 sampled outputs are
+    recomputed by the oracle and byte-equal."""
+    count = 4096 + 37
+    a_bits, b_bits = nand_inputs(count, 77)
+    k = server.keys
+    a = k.encrypt_bits(a_bits, 2005, 0)
+    b = k.encrypt_bits(b_bits, 2005, count)
+    got = _gate_program(server, L.NAND, a, b)
+    assert np.array_equal(k.decrypt_bits(got), 1 - (a_bits & b_bits))
+    idx = sorted(random.Random(5).sample(range(count), 23)) + [count - 1]
+    want = list(POOL.map(lambda i: okeys.gate(O.NAND, a[i, :631], b[i, :631]), idx))
+    for i, w in zip(idx, want):
+        assert np.array_equal(got[i, :631], w), i
+
+
+def _run_config(server, wl, query_seed=7, pk_seed=None):
+    k = server.keys
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    q = k.encrypt_query(m, wl.query, query_seed)
+    db = k.encrypt_db(m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1 if pk_seed is None else pk_seed)
+    prog = A.Program.velopir(server, m)
+    out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    prog.eval(A.to_device(q), A.to_device(db), out)
+    torch.cuda.synchronize()
+    return prog, q, db, A.to_host(out)
+
+
+def test_config1_full_parity(server):
+    """Config 1 (IntV 1D tiny): the final aggregate, every record's validation bit and masked payload are
+    byte-equal to the oracle's alg:VeLoPIR, and decrypt to the plain predicate."""
+    wl = make_workload(1, key_seed=SEED)
+    okeys = O.OracleKeys(SEED)
+    prog, q, db, out = _run_config(server, wl)
+    per = A.record_cts(A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags))
+    # oracle from the same inputs it generates itself (same seeds; byte-equality of the inputs is pinned
+    # by test_library_host.py)
+    oq = OP.encrypt_query(okeys, wl.query, wl.l_I, 7)
+    recs, pays = [], []
+    for i in range(wl.M):
+        r, p = OP.server_enc_record(okeys, wl.key_seed + 1, i, [int(v) for v in wl.records[i]], int(wl.payloads[i]),
+                                    wl.l_I, wl.l_S)
+        recs.append(r)
+        pays.append(p)
+        assert np.array_equal(db[i * per:(i + 1) * per, :631], np.array([c for w in r for c in w] + p))
+    R, vs, masked = OC.velopir(OC.TfheBackend(okeys), wl.mode, oq, recs, pays, wl.l_I, wl.d, wl.l_S, wl.flags)
+    mid = A.to_host(prog.intermediate())
+    for i in range(wl.M):
+        assert np.array_equal(mid[prog.node_row(0, i), :631], vs[i]), ("v", i)
+        for j in range(wl.l_S):
+            assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[i][j]), ("mask", i, j)
+    for j in range(wl.l_S):
+        assert np.array_equal(out[j, :631], R[j]), ("R", j)
+    want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+    assert server.keys.decrypt_value(out) == want
+
+
+def _trivial_db(wl, per):
+    """All-trivial inputs (P11): (0, Ecd(bit)) for every record bit."""
+    W = wl.records.shape[1]
+    db = np.zeros((wl.M * per, 632), np.uint32)
+    for i in range(wl.M):
+        bits = [(int(wl.records[i, k]) >> j) & 1 for k in range(W) for j in range(wl.l_I)]
+        bits += [(int(wl.payloads[i]) >> j) & 1 for j in range(wl.l_S)]
+        db[i * per:(i + 1) * per, 630] = np.where(np.array(bits) == 1, 0x20000000, 0xE0000000)
+    return db
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_all_trivial_closed_form_full_size(server, cfg):
+    """P11 at full size: with trivial (noiseless, zero-mask) inputs every bootstrap reduces to the P3
+    closed form and every key switch to the identity, so the aggregate must be exactly (0, Ecd(bit)) of
+    the plain result, byte for byte (exercises the scheduler, linear forms, MUX combine, tree, layout)."""
+    wl = make_workload(cfg, key_seed=SEED)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    per = A.record_cts(m)
+    db = _trivial_db(wl, per)
+    q = np.zeros((len(wl.query) * wl.l_I, 632), np.uint32)
+    for w, v in enumerate(wl.query):
+        for j in range(wl.l_I):
+            q[w * wl.l_I + j, 630] = 0x20000000 if (v >> j) & 1 else 0xE0000000
+    prog = A.Program.velopir(server, m)
+    out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    prog.eval(A.to_device(q), A.to_device(db), out)
+    torch.cuda.synchronize()
+    out = A.to_host(out)
+    want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+    assert not out[:, :630].any()
+    assert [int(x) for x in out[:, 630]] == [0x20000000 if (want >> j) & 1 else 0xE0000000 for j in range(wl.l_S)]
+
+
+def test_config2_full_size_sampled(server):
+    """Config 2 at full size (1024 records, 132,080 BR): decrypted result == plain predicate; two sampled
+    records' validation bits and masked payloads are recomputed by the oracle (from the same seeded
+    inputs) and byte-equal."""
+    wl = make_workload(2, key_seed=SEED)
+    prog, q, db, out = _run_config(server, wl)
+    want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+    assert server.keys.decrypt_value(out) == want
+    okeys = O.OracleKeys(SEED)
+    oq = OP.encrypt_query(okeys, wl.query, wl.l_I, 7)
+    sample = [3, wl.M - 1]
+    mid = A.to_host(prog.intermediate())
+
+    def one(i):
+        r, p = OP.server_enc_record(okeys, wl.key_seed + 1, i, [int(v) for v in wl.records[i]], int(wl.payloads[i]),
+                                    wl.l_I, wl.l_S)
+        return OC.record_outputs(OC.TfheBackend(okeys), wl.mode, oq, r, p, wl.l_I, wl.d, wl.flags)
+
+    for i, (v, masked) in zip(sample, POOL.map(one, sample)):
+        assert np.array_equal(mid[prog.node_row(0, i), :631], v)
+        for j in range(wl.l_S):
+            assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j])

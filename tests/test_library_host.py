@@ -1,0 +1,143 @@
+"""CPU tests of the C-ABI library (no GPU needed): it loads and exports every symbol include/vlp.h declares;
+its host-side KeyGen / encryption / PubKeyGen / ServerEnc bytes equal the oracle's (P10, R3); the level
+scheduler's gate counts and depths equal the closed forms of SURVEY 8(d) / Appendix A."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle import protocol as OP
+from paper_2506_12761_b200 import _lib as L
+from paper_2506_12761_b200 import api as A
+from synth import make_workload
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    with open(os.path.join(ROOT, "include", "vlp.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"\b(vlp_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(L.SIGNATURES), declared ^ set(L.SIGNATURES)
+    lib = L.lib()
+    for name in declared:
+        assert getattr(lib, name) is not None
+    p = L.VlpParams()
+    assert L.lib().vlp_params_tfhe128(ctypes.byref(p)) == 0
+    assert (p.n, p.N, p.k, p.bg_bits, p.ell, p.ks_base_bits, p.ks_t) == (630, 1024, 1, 7, 3, 2, 8)
+    assert (p.sigma_lwe, p.sigma_bk, p.sigma_ks) == (2.0 ** -15, 2.0 ** -25, 2.0 ** -15)
+
+
+@pytest.fixture(scope="module")
+def lkeys():
+    return A.Keys(123)
+
+
+def test_keygen_bytes_equal_oracle(lkeys, okeys):
+    """P10: the library's keys are byte-identical to the oracle's for the same seed (independent code)."""
+    s1, z1, b1, k1 = lkeys.export()
+    s2, z2, b2, k2 = okeys.export()
+    assert np.array_equal(s1, s2) and np.array_equal(z1, z2)
+    assert np.array_equal(b1, b2)
+    assert np.array_equal(k1, k2)
+
+
+def test_encryptions_equal_oracle(lkeys, okeys):
+    bits = np.array([1, 0, 1, 1, 0], np.uint8)
+    got = lkeys.encrypt_bits(bits, 77, obj0=10)
+    for i, b in enumerate(bits):
+        want = okeys.encrypt(int(b), 77, 10 + i)
+        assert np.array_equal(got[i, :631], want) and got[i, 631] == 0
+    m = A.meta(L.MODE_INTV, 4, 8, 8, 2)
+    q = lkeys.encrypt_query(m, [200, 13], 9)
+    oq = OP.encrypt_query(okeys, [200, 13], 8, 9)
+    assert np.array_equal(q[:, :631], np.array([c for w in oq for c in w]))
+    assert list(lkeys.decrypt_bits(q)) == OP.bits_of(200, 8) + OP.bits_of(13, 8)
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4])
+def test_server_enc_equals_oracle(lkeys, okeys, cfg):
+    """alg:PubKeyGen + alg:ServerEnc bytes (two records) equal the oracle's protocol module."""
+    wl = make_workload(cfg, M=2)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    db = lkeys.encrypt_db(m, wl.records, wl.payloads, pk_seed=555)
+    per = A.record_cts(m)
+    W = wl.records.shape[1]
+    assert per == W * wl.l_I + wl.l_S
+    for i in range(wl.M):
+        rec, pay = OP.server_enc_record(okeys, 555, i, [int(v) for v in wl.records[i]], int(wl.payloads[i]),
+                                        wl.l_I, wl.l_S)
+        want = [c for word in rec for c in word] + pay
+        assert np.array_equal(db[i * per:(i + 1) * per, :631], np.array(want))
+
+
+def test_pk_single_use(lkeys):
+    m = A.meta(L.MODE_IDM, 2, 4, 2, 1)
+    pk = ctypes.c_void_p()
+    L.check(L.lib().vlp_pubkeygen(lkeys.sk, ctypes.byref(m), 1, 0, 2, ctypes.byref(pk)))
+    w = np.array([3, 5], np.uint64)
+    p = np.array([1, 2], np.uint64)
+    out = np.zeros((2 * 6, 632), np.uint32)
+    assert L.lib().vlp_server_encrypt_db(pk, A._u64p(w), A._u64p(p), A._u32p(out)) == 0
+    assert L.lib().vlp_server_encrypt_db(pk, A._u64p(w), A._u64p(p), A._u32p(out)) == L.VLP_EPKUSED
+    L.lib().vlp_free_pk(pk)
+
+
+def test_error_codes(lkeys):
+    bad = A.meta(L.MODE_INTV, 4, 1, 8, 1)
+    out = np.zeros((8, 632), np.uint32)
+    v = np.array([1], np.uint64)
+    assert L.lib().vlp_encrypt_query(lkeys.sk, ctypes.byref(bad), A._u64p(v), 0, A._u32p(out)) == L.VLP_EWIDTH
+    m = A.meta(L.MODE_INTV, 4, 8, 8, 1)
+    v = np.array([256], np.uint64)
+    assert L.lib().vlp_encrypt_query(lkeys.sk, ctypes.byref(m), A._u64p(v), 0, A._u32p(out)) == L.VLP_ERANGE
+    assert L.lib().vlp_last_error()
+
+
+def _info(m, first=0, count=None):
+    h = ctypes.c_void_p()
+    L.check(L.lib().vlp_program_create(None, ctypes.byref(m), first, m.M if count is None else count, ctypes.byref(h)))
+    info = L.VlpProgramInfo()
+    L.check(L.lib().vlp_program_get_info(h, ctypes.byref(info)))
+    L.lib().vlp_free_program(h)
+    return info
+
+
+@pytest.mark.parametrize("cfg,br,ks,levels", [(1, 252, 188, 13), (2, 132080, 99312, 29), (3, 1060832, 798688, 32),
+                                              (4, 6750176, 6750176, 23)])
+def test_schedule_closed_forms(cfg, br, ks, levels):
+    """Gate model of Appendix A (comparator 3l BR / 2l KS, EQ tree 2l-1, mask l_S, tree (M-1) l_S) and the
+    hoisted depths 13 / 29 / 32 / 23 of SURVEY 8(d)."""
+    wl = make_workload(cfg, M=None) if cfg != 4 else None
+    c = {1: (0, 4, 8, 8, 1), 2: (0, 1024, 16, 16, 1), 3: (0, 4096, 16, 32, 2), 4: (2, 65536, 20, 32, 1)}[cfg]
+    info = _info(A.meta(*c))
+    assert (info.br, info.ks, info.levels) == (br, ks, levels)
+
+
+def test_schedule_level_widths_config2():
+    """SURVEY 8(d) config 2 widths: L1 32,768; L2 34,816; L3-L17 2,048; L18 1,024; L19 16,384; tree 8,192 -> 16."""
+    h = ctypes.c_void_p()
+    m = A.meta(0, 1024, 16, 16, 1)
+    L.check(L.lib().vlp_program_create(None, ctypes.byref(m), 0, 1024, ctypes.byref(h)))
+    info = L.VlpProgramInfo()
+    L.check(L.lib().vlp_program_get_info(h, ctypes.byref(info)))
+    assert info.max_level_br == 34816
+    L.lib().vlp_free_program(h)
+
+
+def test_shard_schedules_sum_to_whole():
+    """Contiguous power-of-two shards + combine (R15) need exactly the single-shot gate count."""
+    m = A.meta(0, 1024, 16, 16, 1)
+    whole = _info(m)
+    G = 8
+    shards = [_info(m, g * 128, 128) for g in range(G)]
+    h = ctypes.c_void_p()
+    L.check(L.lib().vlp_program_create_combine(None, ctypes.byref(m), G, ctypes.byref(h)))
+    ci = L.VlpProgramInfo()
+    L.check(L.lib().vlp_program_get_info(h, ctypes.byref(ci)))
+    L.lib().vlp_free_program(h)
+    assert sum(s.br for s in shards) + ci.br == whole.br
+    assert ci.br == (G - 1) * 16 and ci.levels == 3
