@@ -166,6 +166,13 @@ int vlp_program_intermediate_offset(const vlp_program* prog, uint64_t* byte_offs
 int vlp_program_eval(vlp_program* prog, void* scratch_dev, size_t scratch_bytes, const uint32_t* in0_dev,
                      const uint32_t* in1_dev, uint32_t* out_dev, uint64_t stream);
 
+/* Per-kernel timing: when enabled, vlp_program_eval records CUDA events on its stream around every
+ * blind-rotate launch and every key-switch launch (init + switch); vlp_program_profile_read waits for
+ * them and returns the accumulated milliseconds and launch counts (reset != 0 clears the totals). */
+int vlp_program_profile(vlp_program* prog, int enable);
+int vlp_program_profile_read(vlp_program* prog, double* br_ms, double* ks_ms, uint64_t* br_launches,
+                             uint64_t* ks_launches, int reset);
+
 /* Debug / parity entry points (device, asynchronous): blind rotation of `count` TLWE inputs
  * (in_dev [count][632], used as is: no gate linear form) for the first `steps` CMux steps, writing the
  * raw TRLWE accumulators acc_dev [count][2][1024]; and the key switch of N-LWE rows

@@ -66,6 +66,9 @@ SIGNATURES = {
     "vlp_program_node_row": (_i, [_vp, _i, _sz, ctypes.c_uint32, _u64p]),
     "vlp_program_intermediate_offset": (_i, [_vp, _u64p]),
     "vlp_program_eval": (_i, [_vp, _vp, _sz, _vp, _vp, _vp, _u64]),
+    "vlp_program_profile": (_i, [_vp, _i]),
+    "vlp_program_profile_read": (_i, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                      _u64p, _u64p, _i]),
     "vlp_debug_scratch_bytes": (_sz, [_sz]),
     "vlp_debug_blind_rotate": (_i, [_vp, _vp, _sz, _i, _vp, _vp, _u64]),
     "vlp_debug_keyswitch": (_i, [_vp, _vp, _sz, _vp, _vp, _u64]),

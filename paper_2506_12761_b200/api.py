@@ -187,6 +187,17 @@ class Program:
         check(lib().vlp_program_eval(self.h, ctypes.c_void_p(self.scratch.data_ptr()), self.scratch.numel(),
                                      p(in0), p(in1), p(out), _stream_handle(stream)))
 
+    def profile(self, enable: bool = True):
+        check(lib().vlp_program_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self, reset: bool = True):
+        """(br_ms, ks_ms, br_launches, ks_launches) accumulated since the last reset."""
+        br, ks = ctypes.c_double(), ctypes.c_double()
+        nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().vlp_program_profile_read(self.h, ctypes.byref(br), ctypes.byref(ks), ctypes.byref(nb),
+                                             ctypes.byref(nk), 1 if reset else 0))
+        return br.value, ks.value, nb.value, nk.value
+
     def node_row(self, kind: int, record: int, bit: int = 0) -> int:
         r = ctypes.c_uint64()
         check(lib().vlp_program_node_row(self.h, kind, record, bit, ctypes.byref(r)))

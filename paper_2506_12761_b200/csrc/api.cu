@@ -27,6 +27,29 @@ struct vlp_program {
   std::vector<uint32_t> copy_slots;        // outputs that are not written in place
   void* bound = nullptr;
   uint32_t launches = 0;
+  // optional per-kernel timing with CUDA events recorded on the launch stream (vlp_program_profile)
+  bool profile = false;
+  struct Ev { cudaEvent_t a, b; int kind; };
+  std::vector<Ev> pending, pool;
+  double br_ms = 0, ks_ms = 0;
+  uint64_t br_launches = 0, ks_launches = 0;
+  ~vlp_program() {
+    for (auto& e : pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    for (auto& e : pool) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+  }
+  Ev* begin(int kind, cudaStream_t st) {
+    if (!profile) return nullptr;
+    Ev e;
+    if (!pool.empty()) { e = pool.back(); pool.pop_back(); }
+    else { cudaEventCreate(&e.a); cudaEventCreate(&e.b); }
+    e.kind = kind;
+    cudaEventRecord(e.a, st);
+    pending.push_back(e);
+    return &pending.back();
+  }
+  void end(int kind, cudaStream_t st) {
+    if (profile) cudaEventRecord(pending.back().b, st);
+  }
 };
 
 namespace vlp {
@@ -272,19 +295,56 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
     ba.bsk = s->bsk_ntt;
     ba.tw_fwd = s->tw_fwd;
     ba.tw_inv = s->tw_inv;
-    if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
+    if (ba.njobs) {
+      p->begin(0, st);
+      if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
+      p->end(0, st);
+    }
     KsArgs ka{};
     ka.jobs = reinterpret_cast<const KsJob*>(sc + p->off_ks) + p->ks_first[L];
     ka.njobs = static_cast<uint32_t>(lv.ks.size());
     ka.reg = reg;
     ka.nlwe = nlwe;
     ka.ksk = s->ksk;
-    if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
+    if (ka.njobs) {
+      p->begin(1, st);
+      if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
+      p->end(1, st);
+    }
   }
   if (!p->copy_slots.empty() &&
       (e = launch_copy_rows(reinterpret_cast<const uint32_t*>(sc + p->off_outslots),
                             static_cast<uint32_t>(p->copy_slots.size()), reg, out, st)))
     return cuda_fail(e, "copy out");
+  return VLP_OK;
+}
+
+int vlp_program_profile(vlp_program* p, int enable) {
+  if (!p) return fail(VLP_EINVAL, "null argument");
+  p->profile = enable != 0;
+  return VLP_OK;
+}
+
+int vlp_program_profile_read(vlp_program* p, double* br_ms, double* ks_ms, uint64_t* br_launches,
+                             uint64_t* ks_launches, int reset) {
+  if (!p) return fail(VLP_EINVAL, "null argument");
+  for (auto& ev : p->pending) {
+    float ms = 0;
+    if (cudaError_t e = cudaEventSynchronize(ev.b)) return cuda_fail(e, "profile event");
+    cudaEventElapsedTime(&ms, ev.a, ev.b);
+    (ev.kind == 0 ? p->br_ms : p->ks_ms) += ms;
+    (ev.kind == 0 ? p->br_launches : p->ks_launches) += 1;
+    p->pool.push_back(ev);
+  }
+  p->pending.clear();
+  if (br_ms) *br_ms = p->br_ms;
+  if (ks_ms) *ks_ms = p->ks_ms;
+  if (br_launches) *br_launches = p->br_launches;
+  if (ks_launches) *ks_launches = p->ks_launches;
+  if (reset) {
+    p->br_ms = p->ks_ms = 0;
+    p->br_launches = p->ks_launches = 0;
+  }
   return VLP_OK;
 }
 
