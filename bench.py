@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""bench.py -- VeLoPIR query throughput on B200 (gate bootstraps/s and records/s per query).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A step is one VeLoPIR query over BASELINE.json config 2 (IntV 1D, 1024 records, l_I = l_S = 16; 132,080
+blind rotations, 99,312 key switches, 29 levels) with the encrypted DB and the query already resident in
+HBM.  With N > 1 (torchrun) the records are sharded contiguously (M/N each, R15): the query is broadcast
+(NCCL), every rank evaluates its shard down to its root, the roots are gathered to rank 0 (NCCL) and rank 0
+runs the top log2 N tree levels: strong scaling of one query.  `e2e` repeats the step through the public API
+with the query copied from pinned host memory and the result copied back every step.  `--impl reference`
+times the CPU oracle (the only reference this paper-only task has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import make_workload, nand_inputs  # noqa: E402
+from synth.workloads import expected_result  # noqa: E402
+
+METRIC = "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
+UNIT = "gate bootstraps/s"
+CONFIG_BR = {1: 252, 2: 132080, 3: 1060832, 4: 6750176}
+
+
+def ops_per_br():
+    """Integer lane-operations of one blind rotation in the implemented algorithm:
+    per CMux step 12 NTTs x 5120 butterflies x 7 ops + 1024 positions x 72 MAC ops + 2048 x 15 digit ops
+    + 2048 x 19 lift/recombine ops."""
+    per_step = 12 * 5120 * 7 + 1024 * 72 + 2048 * 15 + 2048 * 19
+    return 630 * per_step
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def int_peak():
+    """Issue-limited integer peak: 148 SMs x 4 SMSPs x 32 lanes x 1 instr/cycle x max SM clock.
+    If profiles/int_peak.json holds a measured IMAD/IADD3 mix rate, that is used instead."""
+    p = os.path.join(ROOT, "profiles", "int_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d["gops"], "measured " + d.get("how", "")
+    mhz = load_peaks().get("sm_max_mhz", 1965.0)
+    return 148 * 128 * mhz * 1e6 / 1e9, "derived: 148 SM x 128 lanes x %.0f MHz" % mhz
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.path = os.path.join("/tmp", f"vlp_clocks_{os.getpid()}.csv")
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_baseline_oracle(seconds_target=5.0, nand_gates=None):
+    """The oracle as it stands, on this host's cores (threads over independent gates), on a bounded
+    sample: NAND gates on fresh encryptions (one BR + one KS each)."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    cores = os.cpu_count() or 1
+    k = O.OracleKeys(1005)
+    t0 = time.time()
+    k.gate(O.NAND, k.encrypt(1, 1, 0), k.encrypt(0, 1, 1))
+    one = time.time() - t0
+    count = nand_gates or cores * max(1, int(round(seconds_target / max(one, 1e-3))))
+    a_bits, b_bits = nand_inputs(count, 3005)
+    xs = [k.encrypt(int(b), 3005, i) for i, b in enumerate(a_bits)]
+    ys = [k.encrypt(int(b), 3005, count + i) for i, b in enumerate(b_bits)]
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        t0 = time.time()
+        list(pool.map(lambda i: k.gate(O.NAND, xs[i], ys[i]), range(count)))
+        dt = time.time() - t0
+    return {"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{count} NAND gate bootstraps (BR+extract+KS) on fresh encryptions, {cores} threads, "
+                      f"{dt:.1f} s wall"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    wl_br = CONFIG_BR[args.config]
+    wl = make_workload(args.config) if args.config != 4 else None
+    per_step = []
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline_oracle(nand_gates=cores * 2)
+        if s >= args.warmup:
+            per_step.append(cb["value"])
+    v = statistics.median(per_step)
+    M = wl.M if wl else 65536
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "records_per_s": v / (wl_br / M),
+            "config": {"workload": f"cfg{args.config}", "note": "each step: 2 x cores NAND bootstraps on the CPU oracle; "
+                       "BR/s of the same gate bootstrap as the GPU path; records/s extrapolated by the config's BR count"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} steps x {2 * cores} NAND gate bootstraps"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2506_12761_b200 import _lib as L
+    from paper_2506_12761_b200 import api as A
+
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+    stream = torch.cuda.current_stream()
+
+    wl = make_workload(args.config)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    if wl.M % world or (wl.M // world) & (wl.M // world - 1):
+        raise SystemExit("records must split into power-of-two shards")
+    shard = wl.M // world
+    first = rank * shard
+    t_setup = time.time()
+    keys = A.Keys(wl.key_seed)                 # client (every rank regenerates the same keys from the seed)
+    srv = A.Server(keys, local)
+    per = A.record_cts(m)
+    db = A.to_device(keys.encrypt_db(m, wl.records[first:first + shard], wl.payloads[first:first + shard],
+                                     pk_seed=wl.key_seed + 1, first=first, count=shard), local)
+    q_host = keys.encrypt_query(m, wl.query, 7)
+    q = A.to_device(q_host, local)
+    prog = A.Program.velopir(srv, m, first, shard)
+    comb = A.Program.combine(srv, m, world) if (world > 1 and rank == 0) else None
+    part = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
+    gathered = torch.zeros((world, wl.l_S, 632), dtype=torch.int32, device=dev) if world > 1 else None
+    out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    setup_s = time.time() - t_setup
+
+    def step(qdev):
+        if world > 1:
+            dist.broadcast(qdev, src=0)
+        prog.eval(qdev, db, part if world > 1 else out, stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, part)  # shard roots -> every rank (rank 0 combines)
+            if rank == 0:
+                comb.eval(gathered.view(world * wl.l_S, 632), None, out, stream)
+
+    for _ in range(args.warmup):
+        step(q)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # correctness of the measured computation
+    want = expected_result(wl)
+    if rank == 0:
+        got = keys.decrypt_value(A.to_host(out))
+        assert got == want, f"wrong result {got} != {want}"
+
+    # ---- timed region: K steps, L2 flushed between steps (untimed), per-step CUDA events
+    sampler = ClockSampler(local) if rank == 0 else None
+    prog.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall0 = time.time()
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        step(q)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.time() - wall0
+    clocks = sampler.stop() if sampler else None
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    br_ms, ks_ms, br_n, ks_n = prog.profile_read(reset=True)
+    prog.profile(False)
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    br_per_query = CONFIG_BR[args.config]
+    value = br_per_query / (ms_per_step / 1e3)
+    records_per_s = wl.M / (ms_per_step / 1e3)
+
+    # ---- e2e: query H2D from pinned host memory + eval + result D2H, every step (public API)
+    e2e = None
+    if not args.no_e2e:
+        q_pin = torch.from_numpy(q_host.view(np.int32)).pin_memory()
+        out_pin = torch.empty((wl.l_S, 632), dtype=torch.int32).pin_memory()
+        qd = torch.empty_like(q)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(args.steps):
+            if rank == 0:
+                qd.copy_(q_pin, non_blocking=True)
+            step(qd)
+            if rank == 0:
+                out_pin.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms = float(et.item()) / args.steps
+        if rank == 0:
+            assert keys.decrypt_value(out_pin.numpy().view(np.uint32)) == want
+        e2e = {"value": br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": wl.M / (e2e_ms / 1e3),
+               "h2d_bytes_per_step": int(q_host.nbytes), "d2h_bytes_per_step": int(wl.l_S * 632 * 4)}
+
+    if rank == 0:
+        peak, peak_how = int_peak()
+        br_launch_ms = br_ms / max(1, br_n)
+        # achieved over the dominant kernel: algorithmic integer ops of all BRs / total BR kernel time
+        br_in_shard = prog.info.br
+        achieved = ops_per_br() * br_in_shard * args.steps / (br_ms / 1e3) / 1e9 if br_ms > 0 else None
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline_oracle()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "records_per_s": records_per_s, "ks_per_s": 99312 / (ms_per_step / 1e3) if args.config == 2 else None,
+            "config": {"workload": f"cfg{args.config}_{wl.name}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S,
+                       "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels,
+                       "parallelism": f"records sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "flushed between steps (256 MiB write, untimed)",
+                       "params": "TFHE n=630 N=1024 Bg=2^7 l=3 ks 2^2x8 (tab:tfhe_params)"},
+            "roofline": {"bound": "alu", "kernel": "vlp_blind_rotate_kernel", "achieved": achieved,
+                         "peak": peak, "unit": "Gop/s (int32 lane ops)", "frac": (achieved / peak) if achieved else None,
+                         "peak_source": peak_how, "ops_per_br": ops_per_br(),
+                         "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
+                         "br_share_of_step": br_ms / args.steps / ms_per_step,
+                         "br_launch_avg_ms": br_launch_ms, "traffic": None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": prog.info.kernel_launches * args.steps + (comb.info.kernel_launches * args.steps if comb else 0),
+            "setup_s": setup_s, "wall_s_timed": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -132,3 +132,21 @@ def nand_inputs(count: int, data_seed: int = 2005):
     a = rng.integers(0, 2, size=count, dtype=np.uint8)
     b = rng.integers(0, 2, size=count, dtype=np.uint8)
     return a, b
+
+
+def expected_result(wl: Workload) -> int:
+    """The plaintext answer the query must decrypt to (thm:VeLoPIR; R12/R13/R19): XOR (OR with
+    F_OR_REDUCE) of the payloads of the records whose plaintext bounds match the query; 0 if none.
+    Ground truth of the drawn inputs (used by bench.py's sanity check), not the homomorphic method."""
+    r = 0
+    for rec, pay in zip(wl.records.tolist(), wl.payloads.tolist()):
+        if wl.mode == MODE_INTV:
+            ok = all(rec[2 * a] <= wl.query[a] and (wl.query[a] <= rec[2 * a + 1] if wl.flags & F_CLOSED_UPPER
+                                                    else wl.query[a] < rec[2 * a + 1]) for a in range(wl.d))
+        elif wl.mode == MODE_COV:
+            ok = all(wl.query[a] == rec[a] for a in range(wl.d))
+        else:
+            ok = wl.query[0] == rec[0]
+        if ok:
+            r = (r | int(pay)) if wl.flags & F_OR_REDUCE else (r ^ int(pay))
+    return r
