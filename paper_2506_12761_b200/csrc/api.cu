@@ -14,8 +14,9 @@ struct vlp_server {
   uint8_t* evk_dev = nullptr;
   uint32_t* bsk_ntt = nullptr;
   uint32_t* ksk = nullptr;
-  uint2* tw_fwd = nullptr;
-  uint2* tw_inv = nullptr;
+  uint2* tw_fwd = nullptr;   // natural order (bsk conversion)
+  uint2* twl_fwd = nullptr;  // thread-layout tables of the blind-rotate kernel
+  uint2* twl_inv = nullptr;
 };
 
 struct vlp_program {
@@ -58,8 +59,9 @@ namespace {
 constexpr size_t kBskNttBytes = kBskNttWords * 4;
 constexpr size_t kKskBytes = static_cast<size_t>(N) * kKsT * 3 * kCt * 4;
 constexpr size_t kTwBytes = static_cast<size_t>(N) * sizeof(uint2);
+constexpr size_t kTwlBytes = static_cast<size_t>(kTwSlots) * kBT * sizeof(uint2);
 constexpr size_t kRawBskBytes = static_cast<size_t>(n) * kRows * 2 * N * 4;
-constexpr size_t kEvkBytes = kBskNttBytes + kKskBytes + 2 * kTwBytes + kRawBskBytes;
+constexpr size_t kEvkBytes = kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -103,6 +105,29 @@ void make_twiddles(std::vector<uint2>& fwd, std::vector<uint2>& inv) {
     fwd[k] = make_uint2(static_cast<uint32_t>(w), static_cast<uint32_t>((w << 32) / kP));
     inv[k] = make_uint2(static_cast<uint32_t>(wi), static_cast<uint32_t>((wi << 32) / kP));
   }
+}
+
+// Thread-layout twiddle tables of the blind-rotate kernel: slot q (stage 3..9 lane-varying twiddles) x
+// thread t; k(stage, t, qq) is the twiddle index the butterflies of thread t use (kernels.cu layouts).
+void make_layout_twiddles(const std::vector<uint2>& nat, std::vector<uint2>& lay) {
+  lay.resize(static_cast<size_t>(kTwSlots) * kBT);
+  const int st[kTwSlots] = {3, 4, 4, 5, 5, 5, 5, 6, 7, 7, 8, 8, 8, 8, 9, 9, 9, 9};
+  const int qq[kTwSlots] = {0, 0, 1, 0, 1, 2, 3, 0, 0, 1, 0, 1, 2, 3, 0, 1, 2, 3};
+  for (int q = 0; q < kTwSlots; q++)
+    for (uint32_t t = 0; t < static_cast<uint32_t>(kBT); t++) {
+      const uint32_t th = t >> 4, tc = t >> 1;
+      uint32_t k = 0;
+      switch (st[q]) {
+        case 3: k = 8 + th; break;
+        case 4: k = 16 + 2 * th + qq[q]; break;
+        case 5: k = 32 + 4 * th + qq[q]; break;
+        case 6: k = 64 + tc; break;
+        case 7: k = 128 + 2 * tc + qq[q]; break;
+        case 8: k = 256 + 4 * tc + qq[q]; break;
+        default: k = 512 + 8 * tc + ((t & 1) ? 4 + qq[q] : qq[q]); break;
+      }
+      lay[static_cast<size_t>(q) * kBT + t] = nat[k];
+    }
 }
 
 Regions regions(const vlp_program* p, void* scratch, const uint32_t* in0, const uint32_t* in1, uint32_t* out) {
@@ -165,16 +190,20 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   srv->bsk_ntt = reinterpret_cast<uint32_t*>(base);
   srv->ksk = reinterpret_cast<uint32_t*>(base + kBskNttBytes);
   srv->tw_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes);
-  srv->tw_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes);
-  uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + 2 * kTwBytes);
+  srv->twl_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes);
+  srv->twl_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes + kTwlBytes);
+  uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes);
 
-  std::vector<uint2> fwd, inv;
+  std::vector<uint2> fwd, inv, lf, li;
   make_twiddles(fwd, inv);
+  make_layout_twiddles(fwd, lf);
+  make_layout_twiddles(inv, li);
   set_const_twiddles(fwd.data(), inv.data());
   cudaError_t e;
   if ((e = cudaMemsetAsync(srv->bsk_ntt, 0, kBskNttBytes, st))) return cuda_fail(e, "memset");
   if ((e = cudaMemcpyAsync(srv->tw_fwd, fwd.data(), kTwBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "tw");
-  if ((e = cudaMemcpyAsync(srv->tw_inv, inv.data(), kTwBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "tw");
+  if ((e = cudaMemcpyAsync(srv->twl_fwd, lf.data(), kTwlBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "twl");
+  if ((e = cudaMemcpyAsync(srv->twl_inv, li.data(), kTwlBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "twl");
   if ((e = cudaMemcpyAsync(srv->ksk, evk->ksk.data(), kKskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "ksk");
   if ((e = cudaMemcpyAsync(raw, evk->bsk.data(), kRawBskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "bsk");
   // Montgomery factor with N^-1 folded in: c = N^-1 * 2^32 mod p
@@ -293,8 +322,8 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
     ba.nlwe = nlwe;
     ba.raw_acc = nullptr;
     ba.bsk = s->bsk_ntt;
-    ba.tw_fwd = s->tw_fwd;
-    ba.tw_inv = s->tw_inv;
+    ba.twl_fwd = s->twl_fwd;
+    ba.twl_inv = s->twl_inv;
     if (ba.njobs) {
       p->begin(0, st);
       if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
@@ -368,8 +397,8 @@ int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, 
   ba.reg.base[kRegIn0] = const_cast<uint32_t*>(in_dev);
   ba.raw_acc = acc_dev;
   ba.bsk = s->bsk_ntt;
-  ba.tw_fwd = s->tw_fwd;
-  ba.tw_inv = s->tw_inv;
+  ba.twl_fwd = s->twl_fwd;
+  ba.twl_inv = s->twl_inv;
   if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
   return VLP_OK;

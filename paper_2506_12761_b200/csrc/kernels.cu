@@ -12,12 +12,7 @@
 // (values in [0, 4p)) with Shoup twiddles.  Inverse: Gentleman-Sande, bit-reversed -> natural, values in
 // [0, 2p); N^-1 and the Montgomery factor are folded into the stored key.
 //
-// Thread layout of one bootstrap (64 threads, 16 coefficients per thread per polynomial):
-//   layout A (stages 0-3):  j = t + 64 r                        (twiddles uniform per r)
-//   layout B (stages 4-7):  j = (t>>2)<<6 | r<<2 | (t&3)
-//   layout C (stages 8-9):  j = t<<4 | r                        (bit-reversed NTT positions 16t..16t+15)
-// Layout changes go through shared memory with an XOR swizzle that is bank-conflict free for all three
-// layouts (tools/emulate_br_ntt.py checks it).
+// Thread layout of one bootstrap: see "layouts / swizzle" below (128 threads x 8 coefficients).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,7 +33,7 @@ constexpr uint32_t inv_mod_2_32(uint32_t p) {
 constexpr uint32_t PINV_NEG = 0u - inv_mod_2_32(P);  // -p^-1 mod 2^32 (Montgomery REDC)
 static_assert(static_cast<uint32_t>(P * inv_mod_2_32(P)) == 1u, "inverse");
 
-__constant__ uint2 c_tw[2][16];  // uniform twiddles (k < 16) of the forward / inverse transforms
+__constant__ uint2 c_tw[2][8];  // uniform twiddles (k < 8, stages 0-2) of the forward / inverse transforms
 
 // ------------------------------------------------------------------------------ modular helpers
 __device__ __forceinline__ uint32_t umin(uint32_t a, uint32_t b) { return a < b ? a : b; }
@@ -106,125 +101,141 @@ __device__ __forceinline__ uint32_t* slot_wptr(const Regions& reg, uint32_t id) 
 __device__ __forceinline__ const uint32_t* slot_ptr(const Regions& reg, uint32_t id) { return slot_wptr(reg, id); }
 
 // ------------------------------------------------------------------------------ layouts / swizzle
-// phys(j) = j ^ h(j), h = j8 | j5<<1 | j6<<2 | j7<<3 | j8<<4; written as base(t) ^ c(r) per layout.
+// One bootstrap = 128 threads x 8 registers per polynomial (t in [0,128), r in [0,8)):
+//   layout A (stages 0-2, uniform twiddles):  j = t | r<<7
+//   layout B (stages 3-5):                     j = (t>>4)<<7 | r<<4 | (t&15)
+//   layout C (stages 6-8):                     j = (t>>1)<<4 | r<<1 | (t&1)
+//   stage 9 pairs lanes t, t^1: a lane-pair register exchange makes them in-register butterflies on
+//   (reg[i], reg[4+i]); afterwards slot s of lane t holds NTT position posF(t, s) (tools/emulate_br_v2.py).
+// Shared-memory exchanges use phys(j) = j ^ (j5<<1 ^ j6<<2 ^ j7<<3 ^ j7<<4), conflict-free for A, B and C,
+// written as base(t) ^ c(r).
 __device__ __forceinline__ uint32_t bit(uint32_t x, int b) { return (x >> b) & 1u; }
-__device__ __forceinline__ uint32_t baseA(uint32_t t) { return t ^ (bit(t, 5) << 1); }
-__host__ __device__ constexpr uint32_t cA(int r) {
-  return (static_cast<uint32_t>(r) << 6) ^ (((r >> 2) & 1) * 17u) ^ ((r & 1) << 2) ^ (((r >> 1) & 1) << 3);
-}
+__device__ __forceinline__ uint32_t baseA(uint32_t t) { return t ^ (bit(t, 5) << 1) ^ (bit(t, 6) << 2); }
+__host__ __device__ constexpr uint32_t cA(int r) { return (static_cast<uint32_t>(r) << 7) ^ ((r & 1) * 24u); }
 __device__ __forceinline__ uint32_t baseB(uint32_t t) {
-  const uint32_t j = ((t >> 2) << 6) | (t & 3u);
-  return j ^ (bit(t, 4) * 17u) ^ (bit(t, 2) << 2) ^ (bit(t, 3) << 3);
+  return ((((t >> 4) << 7) | (t & 15u)) ^ (bit(t, 4) * 24u));
 }
 __host__ __device__ constexpr uint32_t cB(int r) {
-  return (static_cast<uint32_t>(r) << 2) ^ (((r >> 3) & 1) << 1);
+  return (static_cast<uint32_t>(r) << 4) ^ (((r >> 1) & 1) << 1) ^ (((r >> 2) & 1) << 2);
 }
 __device__ __forceinline__ uint32_t baseC(uint32_t t) {
-  return (t << 4) ^ (bit(t, 4) * 17u) ^ (bit(t, 1) << 1) ^ (bit(t, 2) << 2) ^ (bit(t, 3) << 3);
+  return ((((t >> 1) << 4) | (t & 1u)) ^ (bit(t, 2) << 1) ^ (bit(t, 3) << 2) ^ (bit(t, 4) * 24u));
 }
-__host__ __device__ constexpr uint32_t cC(int r) { return static_cast<uint32_t>(r); }
+__host__ __device__ constexpr uint32_t cC(int r) { return static_cast<uint32_t>(r) << 1; }
 
-typedef uint32_t Poly[6][16];
+typedef uint32_t Poly3[3][8];
 
-// Uniform stages 0-3 (layout A): pair (r, r | rb), rb = 8 >> s; twiddle k = 2^s + (r >> (4 - s)).
+// Stages 0-2 (layout A): pair (r, r | rb), rb = 4 >> s; twiddle k = 2^s + (r >> (3 - s)), uniform.
 template <int S, bool INV>
-__device__ __forceinline__ void stage_uniform(Poly& d) {
-  constexpr int rb = 8 >> S;
+__device__ __forceinline__ void stage_A(Poly3& d) {
+  constexpr int rb = 4 >> S;
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
+  for (int r = 0; r < 8; r++) {
     if (r & rb) continue;
-    const uint2 w = c_tw[INV][(1 << S) + (r >> (4 - S))];
+    const uint2 w = c_tw[INV][(1 << S) + (r >> (3 - S))];
 #pragma unroll
-    for (int p = 0; p < 6; p++) {
-      if (INV)
-        gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
-      else
-        ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+    for (int p = 0; p < 3; p++) {
+      if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
     }
   }
 }
 
-// Lane-varying stages 4-7 (layout B): rb = 8 >> (S-4); block index j >> (10 - S).
+// Lane-varying stages 3-8: layout B (S = 3..5) or C (S = 6..8); rb = 4 >> (S % 3); twiddle slot
+// q = r >> (3 - S % 3) at table row kSlotBase[S] + q, column t.
 template <int S, bool INV>
-__device__ __forceinline__ void stage_B(Poly& d, uint32_t t, const uint2* __restrict__ tw) {
-  constexpr int rb = 8 >> (S - 4);
-  const uint32_t thi = t >> 2;
+__device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl) {
+  constexpr int rb = 4 >> (S % 3);
+  constexpr int base = S == 3 ? 0 : S == 4 ? 1 : S == 5 ? 3 : S == 6 ? 7 : S == 7 ? 8 : 10;
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
+  for (int r = 0; r < 8; r++) {
     if (r & rb) continue;
-    // j = thi<<6 | r<<2 | tlo ; j >> (10 - S) = thi << (S - 4) | r >> (8 - S)
-    const uint32_t k = (1u << S) + (thi << (S - 4)) + (static_cast<uint32_t>(r) >> (8 - S));
-    const uint2 w = __ldg(tw + k);
+    const uint2 w = __ldg(twl + (base + (r >> (3 - S % 3))) * kBT);
 #pragma unroll
-    for (int p = 0; p < 6; p++) {
-      if (INV)
-        gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
-      else
-        ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+    for (int p = 0; p < 3; p++) {
+      if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
     }
   }
 }
 
-// Lane-varying stages 8-9 (layout C): rb = 2 (S = 8) / 1 (S = 9); j = t<<4 | r.
-template <int S, bool INV>
-__device__ __forceinline__ void stage_C(Poly& d, uint32_t t, const uint2* __restrict__ tw) {
-  constexpr int rb = S == 8 ? 2 : 1;
+// Stage 9 forward: lane-pair exchange (lower lane keeps pairs r = 0..3, upper lane r = 4..7), then
+// butterflies on (d[i], d[4+i]) with twiddle slots 14..17.
+__device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __restrict__ twl) {
+  const bool lo = (t & 1u) == 0;
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
-    if (r & rb) continue;
-    const uint32_t k = (1u << S) + (t << (S - 6)) + (static_cast<uint32_t>(r) >> (10 - S));
-    const uint2 w = __ldg(tw + k);
+  for (int i = 0; i < 4; i++) {
+    const uint2 w = __ldg(twl + (14 + i) * kBT);
 #pragma unroll
-    for (int p = 0; p < 6; p++) {
-      if (INV)
-        gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
-      else
-        ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+    for (int p = 0; p < 3; p++) {
+      const uint32_t send = lo ? d[p][4 + i] : d[p][i];
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
+      uint32_t x = lo ? d[p][i] : recv;
+      uint32_t y = lo ? recv : d[p][4 + i];
+      ct_bfly(x, y, w.x, w.y);
+      d[p][i] = x;
+      d[p][4 + i] = y;
     }
   }
 }
 
-// Layout change through shared memory, 3 polynomials per round (xb holds 3 x 1024 words).
+// Stage 9 inverse: butterflies on (d[i], d[4+i]), then the reverse lane-pair exchange (back to layout C).
+__device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __restrict__ twl) {
+  const bool lo = (t & 1u) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const uint2 w = __ldg(twl + (14 + i) * kBT);
+#pragma unroll
+    for (int p = 0; p < 3; p++) {
+      gs_bfly(d[p][i], d[p][4 + i], w.x, w.y);
+      const uint32_t send = lo ? d[p][4 + i] : d[p][i];
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
+      d[p][i] = lo ? d[p][i] : recv;
+      d[p][4 + i] = lo ? recv : d[p][4 + i];
+    }
+  }
+}
+
+// Layout change of 3 polynomials through shared memory (xb: 3 x 1024 words of this bootstrap).
 template <int FROM, int TO>
-__device__ __forceinline__ void exchange(Poly& d, uint32_t* xb, uint32_t t) {
+__device__ __forceinline__ void exchange(Poly3& d, uint32_t* xb, uint32_t t) {
   const uint32_t bs = FROM == 0 ? baseA(t) : (FROM == 1 ? baseB(t) : baseC(t));
   const uint32_t bd = TO == 0 ? baseA(t) : (TO == 1 ? baseB(t) : baseC(t));
+  __syncthreads();
 #pragma unroll
-  for (int half = 0; half < 2; half++) {
-    __syncthreads();
+  for (int q = 0; q < 3; q++)
 #pragma unroll
-    for (int q = 0; q < 3; q++)
+    for (int r = 0; r < 8; r++) xb[q * N + (bs ^ (FROM == 0 ? cA(r) : (FROM == 1 ? cB(r) : cC(r))))] = d[q][r];
+  __syncthreads();
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
-        const uint32_t c = FROM == 0 ? cA(r) : (FROM == 1 ? cB(r) : cC(r));
-        xb[q * N + (bs ^ c)] = d[half * 3 + q][r];
-      }
-    __syncthreads();
+  for (int q = 0; q < 3; q++)
 #pragma unroll
-    for (int q = 0; q < 3; q++)
-#pragma unroll
-      for (int r = 0; r < 16; r++) {
-        const uint32_t c = TO == 0 ? cA(r) : (TO == 1 ? cB(r) : cC(r));
-        d[half * 3 + q][r] = xb[q * N + (bd ^ c)];
-      }
-  }
+    for (int r = 0; r < 8; r++) d[q][r] = xb[q * N + (bd ^ (TO == 0 ? cA(r) : (TO == 1 ? cB(r) : cC(r))))];
 }
 
 }  // namespace
 
 // ================================================================================ K2 blind rotation
+// Per CMux step and bootstrap: two forward rounds (component u of D = X^abar acc - acc: its 3 gadget digit
+// polynomials -> forward NTT -> Montgomery MAC into the 6 output accumulators, bsk chunks streamed by TMA
+// into a smem ring shared by the CTA's 4 bootstraps), then two inverse rounds (output component u: its 3
+// key limbs -> inverse NTT -> centered lift -> recombine mod 2^32 -> acc_u += ...).  The round loops are
+// not unrolled: each round body is ~25 KB of SASS (the instruction cache, not the ALUs, limited the fully
+// unrolled form; profiles/).
 __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const BrArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* ring = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* acc_all = ring + kSlots * 64 * kChunkWords;
+  uint32_t* acc_all = ring + kSlots * kBT * kChunkWords;
   uint32_t* xb_all = acc_all + kBrBoot * 2 * N;
   uint16_t* abar_all = reinterpret_cast<uint16_t*>(xb_all + kBrBoot * 3 * N);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(abar_all + kBrBoot * 640);
 
-  const uint32_t tid = threadIdx.x, g = tid >> 6, t = tid & 63;
+  const uint32_t tid = threadIdx.x, g = tid / kBT, t = tid % kBT;
   uint32_t* acc = acc_all + g * 2 * N;
   uint32_t* xb = xb_all + g * 3 * N;
   uint16_t* abar = abar_all + g * 640;
+  const uint2* twf = a.twl_fwd + t;
+  const uint2* twi = a.twl_inv + t;
 
   const uint32_t ngroups = (a.njobs + kBrBoot - 1) / kBrBoot;
   if (blockIdx.x >= ngroups) return;
@@ -236,11 +247,11 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
     fence_mbar_init();
   }
   __syncthreads();
-  // chunk sequence n -> (step (n / 8) % steps, chunk n % 8) of the bsk; slot n % kSlots
+  // chunk sequence n -> (step (n / 8) % steps, chunk n % 8) of the bsk; ring slot n % kSlots
   auto issue = [&](uint64_t nseq) {
     const uint32_t step = static_cast<uint32_t>((nseq / kChunks) % a.steps), c = nseq % kChunks;
     const uint32_t s = nseq % kSlots;
-    bulk_load(ring + s * 64 * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * 64 * kChunkWords,
+    bulk_load(ring + s * kBT * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * kBT * kChunkWords,
               kChunkBytes, &mbar[s]);
   };
   if (tid == 0)
@@ -255,20 +266,20 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
       const BrJob job = a.jobs[jb];
       const uint32_t* x = slot_ptr(a.reg, job.x);
       const uint32_t* y = slot_ptr(a.reg, job.y);
-      for (uint32_t w = t; w <= static_cast<uint32_t>(n); w += 64) {
+      for (uint32_t w = t; w <= static_cast<uint32_t>(n); w += kBT) {
         uint32_t c = static_cast<uint32_t>(static_cast<int32_t>(job.ax)) * x[w];
         if (job.ay) c += static_cast<uint32_t>(static_cast<int32_t>(job.ay)) * y[w];
         if (w == static_cast<uint32_t>(n)) c += job.k0;
         abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
       }
     } else {
-      for (uint32_t w = t; w <= static_cast<uint32_t>(n); w += 64) abar[w] = 0;
+      for (uint32_t w = t; w <= static_cast<uint32_t>(n); w += kBT) abar[w] = 0;
     }
     __syncthreads();
     // ---- S4 accumulator init: (0, X^{-bbar} testv), testv = 1/8 everywhere (R8)
     {
       const uint32_t bbar = abar[n];
-      for (uint32_t k = t; k < static_cast<uint32_t>(N); k += 64) {
+      for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT) {
         acc[k] = 0;
         acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu);
       }
@@ -276,108 +287,114 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
     __syncthreads();
 
     // ---- S5: CMux steps
+    uint32_t mac[6][8];  // output o = (component u_out, limb) at this thread's 8 NTT positions
+#pragma unroll
+    for (int o = 0; o < 6; o++)
+#pragma unroll
+      for (int s = 0; s < 8; s++) mac[o][s] = 0;
     for (int i = 0; i < a.steps; i++) {
       const uint32_t ab = abar[i];
-      Poly d;
-      // X^{abar} acc - acc, gadget digits (R5, offset 0x81020400), digit + p - 64 in [p-64, p+64)
+#pragma unroll 1
+      for (int u = 0; u < 2; u++) {
+        Poly3 d;
+        // X^abar acc_u - acc_u (layout A: j = t + 128 r), gadget digits (R5, offset 0x81020400),
+        // digit + p - 64 in [p-64, p+64)
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
-        const uint32_t j = t + 64u * r;
-        const uint32_t kk = (j - ab) & (2 * N - 1);
-        const uint32_t src = kk & (N - 1);
-        const bool neg = kk >= static_cast<uint32_t>(N);
-#pragma unroll
-        for (int u = 0; u < 2; u++) {
-          uint32_t v = acc[u * N + src];
-          v = neg ? 0u - v : v;
+        for (int r = 0; r < 8; r++) {
+          const uint32_t j = t + 128u * r;
+          const uint32_t kk = (j - ab) & (2 * N - 1);
+          uint32_t v = acc[u * N + (kk & (N - 1))];
+          v = kk >= static_cast<uint32_t>(N) ? 0u - v : v;
           const uint32_t w = v - acc[u * N + j] + 0x81020400u;
-          d[u * 3 + 0][r] = ((w >> 25) & 127u) + (P - 64u);
-          d[u * 3 + 1][r] = ((w >> 18) & 127u) + (P - 64u);
-          d[u * 3 + 2][r] = ((w >> 11) & 127u) + (P - 64u);
+          d[0][r] = ((w >> 25) & 127u) + (P - 64u);
+          d[1][r] = ((w >> 18) & 127u) + (P - 64u);
+          d[2][r] = ((w >> 11) & 127u) + (P - 64u);
         }
-      }
-      // forward NTT of the 6 digit polynomials
-      stage_uniform<0, false>(d);
-      stage_uniform<1, false>(d);
-      stage_uniform<2, false>(d);
-      stage_uniform<3, false>(d);
-      exchange<0, 1>(d, xb, t);
-      stage_B<4, false>(d, t, a.tw_fwd);
-      stage_B<5, false>(d, t, a.tw_fwd);
-      stage_B<6, false>(d, t, a.tw_fwd);
-      stage_B<7, false>(d, t, a.tw_fwd);
-      exchange<1, 2>(d, xb, t);
-      stage_C<8, false>(d, t, a.tw_fwd);
-      stage_C<9, false>(d, t, a.tw_fwd);
-
-      // pointwise MAC with bsk_i (streamed chunk by chunk through the smem ring, shared by the CTA)
+        stage_A<0, false>(d);
+        stage_A<1, false>(d);
+        stage_A<2, false>(d);
+        exchange<0, 1>(d, xb, t);
+        stage_BC<3, false>(d, twf);
+        stage_BC<4, false>(d, twf);
+        stage_BC<5, false>(d, twf);
+        exchange<1, 2>(d, xb, t);
+        stage_BC<6, false>(d, twf);
+        stage_BC<7, false>(d, twf);
+        stage_BC<8, false>(d, twf);
+        stage9_fwd(d, t, twf);
+        // MAC: mac[o][s] (+)= sum_j Dhat_{3u+j}[s] * B[3u+j][o][s] (Montgomery; key holds N^-1 * 2^32)
 #pragma unroll
-      for (int c = 0; c < kChunks; c++) {
-        const uint32_t s = nseq % kSlots;
-        mbar_wait(&mbar[s], static_cast<uint32_t>((nseq / kSlots) & 1));
-        const uint32_t* rec = ring + s * 64 * kChunkWords + t * kChunkWords;
+        for (int pp = 0; pp < 4; pp++) {
+          const uint32_t sl = nseq % kSlots;
+          mbar_wait(&mbar[sl], static_cast<uint32_t>((nseq / kSlots) & 1));
+          const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
+          uint32_t x[2][3];
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int r = 2 * c + e;
-          uint32_t x[6];
+          for (int e = 0; e < 2; e++)
 #pragma unroll
-          for (int q = 0; q < 6; q++) x[q] = umin(d[q][r], d[q][r] - P2);  // [0, 2p)
-          uint32_t kv[36];
-#pragma unroll
-          for (int v = 0; v < 9; v++) {
-            const uint4 b4 = reinterpret_cast<const uint4*>(rec + e * 36)[v];
-            kv[4 * v + 0] = b4.x;
-            kv[4 * v + 1] = b4.y;
-            kv[4 * v + 2] = b4.z;
-            kv[4 * v + 3] = b4.w;
-          }
+            for (int j = 0; j < 3; j++) {
+              uint32_t v = d[j][2 * pp + e];
+              v = umin(v, v - P2);
+              x[e][j] = umin(v, v - P);  // [0, p)
+            }
 #pragma unroll
           for (int o = 0; o < 6; o++) {
-            uint64_t T = 0;
+            const uint2 k01 = reinterpret_cast<const uint2*>(rec + o * 6)[0];
+            const uint2 k23 = reinterpret_cast<const uint2*>(rec + o * 6)[1];
+            const uint2 k45 = reinterpret_cast<const uint2*>(rec + o * 6)[2];
+            const uint32_t kv[2][3] = {{k01.x, k01.y, k23.x}, {k23.y, k45.x, k45.y}};
 #pragma unroll
-            for (int q = 0; q < 6; q++) T += static_cast<uint64_t>(x[q]) * kv[o * 6 + q];
-            const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
-            const uint32_t y = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);  // < 4p
-            d[o][r] = umin(y, y - P2);
+            for (int e = 0; e < 2; e++) {
+              const int s = 2 * pp + e;
+              uint64_t T = u ? (static_cast<uint64_t>(mac[o][s]) << 32) : 0ull;
+#pragma unroll
+              for (int j = 0; j < 3; j++) T += static_cast<uint64_t>(x[e][j]) * kv[e][j];
+              const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
+              mac[o][s] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);  // < 3.5p
+            }
           }
+          __syncthreads();  // every thread is done with ring slot sl
+          if (tid == 0 && nseq + kSlots < total_chunks) {
+            fence_proxy_async();
+            issue(nseq + kSlots);
+          }
+          nseq++;
         }
-        __syncthreads();  // every thread is done with slot s
-        if (tid == 0 && nseq + kSlots < total_chunks) {
-          fence_proxy_async();
-          issue(nseq + kSlots);
-        }
-        nseq++;
       }
-
-      // inverse NTT of the 6 (component, limb) products
-      stage_C<9, true>(d, t, a.tw_inv);
-      stage_C<8, true>(d, t, a.tw_inv);
-      exchange<2, 1>(d, xb, t);
-      stage_B<7, true>(d, t, a.tw_inv);
-      stage_B<6, true>(d, t, a.tw_inv);
-      stage_B<5, true>(d, t, a.tw_inv);
-      stage_B<4, true>(d, t, a.tw_inv);
-      exchange<1, 0>(d, xb, t);
-      stage_uniform<3, true>(d);
-      stage_uniform<2, true>(d);
-      stage_uniform<1, true>(d);
-      stage_uniform<0, true>(d);
-
-      // centered lift of the three limbs, recombine mod 2^32, acc += (layout A: j = t + 64 r)
+#pragma unroll 1
+      for (int u = 0; u < 2; u++) {
+        Poly3 d;
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
-        const uint32_t j = t + 64u * r;
+        for (int l = 0; l < 3; l++)
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+          for (int s = 0; s < 8; s++) {
+            const uint32_t v = u ? mac[3 + l][s] : mac[l][s];
+            d[l][s] = umin(v, v - P2);  // [0, 2p)
+          }
+        stage9_inv(d, t, twi);
+        stage_BC<8, true>(d, twi);
+        stage_BC<7, true>(d, twi);
+        stage_BC<6, true>(d, twi);
+        exchange<2, 1>(d, xb, t);
+        stage_BC<5, true>(d, twi);
+        stage_BC<4, true>(d, twi);
+        stage_BC<3, true>(d, twi);
+        exchange<1, 0>(d, xb, t);
+        stage_A<2, true>(d);
+        stage_A<1, true>(d);
+        stage_A<0, true>(d);
+        // centered lift of the three limbs, recombine mod 2^32, acc_u += (layout A: j = t + 128 r)
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
           uint32_t sum = 0;
 #pragma unroll
           for (int l = 0; l < 3; l++) {
-            uint32_t v = d[u * 3 + l][r];
-            v = umin(v, v - P);                       // [0, p)
-            const uint32_t sv = v > (P >> 1) ? v - P : v;  // centered, as a 2's complement u32
+            uint32_t v = d[l][r];
+            v = umin(v, v - P);                            // [0, p)
+            const uint32_t sv = v > (P >> 1) ? v - P : v;  // centered, two's complement
             sum += sv << (11 * l);
           }
-          acc[u * N + j] += sum;
+          acc[u * N + t + 128u * r] += sum;
         }
       }
       __syncthreads();
@@ -387,10 +404,10 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
     if (active) {
       if (a.raw_acc) {
         uint32_t* o = a.raw_acc + static_cast<size_t>(jb) * 2 * N;
-        for (uint32_t k = t; k < 2u * N; k += 64) o[k] = acc[k];
+        for (uint32_t k = t; k < 2u * N; k += kBT) o[k] = acc[k];
       } else {
         uint32_t* o = a.nlwe + static_cast<size_t>(a.jobs[jb].out) * kNlwe;
-        for (uint32_t k = t; k < static_cast<uint32_t>(N); k += 64) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+        for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
         if (t == 0) o[N] = acc[N];
       }
     }
@@ -510,15 +527,16 @@ __global__ void vlp_ks_init_kernel(const KsArgs a) {
 }
 
 // ================================================================================ K4 bsk conversion
-// One CTA per (i, row r, component u): split the 1024 torus32 coefficients into 3 signed limbs, forward
-// NTT each limb polynomial mod p (plain, fully reduced), multiply by N^-1 * 2^32 mod p, scatter into
-// the chunked layout [i][chunk][t][e*36 + (u*3 + limb)*6 + r] with position 16t + 2*chunk + e.
+// One CTA per (i, key row q, component u): split the 1024 torus32 coefficients into 3 signed limbs, forward
+// NTT each limb polynomial mod p (plain, fully reduced; natural twiddle table), multiply by
+// N^-1 * 2^32 mod p, and scatter NTT position k to the lane/slot that holds it after the forward
+// transform (inverse of posF): chunk (q / 3) * 4 + slot / 2, word o*6 + (slot & 1)*3 + q % 3, o = u*3 + limb.
 __global__ void __launch_bounds__(512) vlp_bsk_convert_kernel(const uint32_t* __restrict__ raw,
                                                               uint32_t* __restrict__ out,
                                                               const uint2* __restrict__ tw, uint32_t c_mont) {
   __shared__ uint32_t poly[3][N];
-  const uint32_t bid = blockIdx.x;  // (i*6 + r)*2 + u
-  const uint32_t u = bid & 1, r = (bid >> 1) % kRows, i = (bid >> 1) / kRows;
+  const uint32_t bid = blockIdx.x;  // (i*6 + q)*2 + u
+  const uint32_t u = bid & 1, q = (bid >> 1) % kRows, i = (bid >> 1) / kRows;
   const uint32_t* src = raw + static_cast<size_t>(bid) * N;
   for (uint32_t k = threadIdx.x; k < static_cast<uint32_t>(N); k += blockDim.x) {
     const int64_t b = static_cast<int64_t>(src[k]);
@@ -534,8 +552,8 @@ __global__ void __launch_bounds__(512) vlp_bsk_convert_kernel(const uint32_t* __
   __syncthreads();
   for (int s = 0; s < 10; s++) {
     const uint32_t half = 512u >> s;
-    const uint32_t q = threadIdx.x;  // butterfly 0..511
-    const uint32_t blk = q / half, j = 2 * blk * half + (q % half);
+    const uint32_t bf = threadIdx.x;  // butterfly 0..511
+    const uint32_t blk = bf / half, j = 2 * blk * half + (bf % half);
     const uint32_t w = tw[(1u << s) + blk].x;
 #pragma unroll
     for (int l = 0; l < 3; l++) {
@@ -547,12 +565,15 @@ __global__ void __launch_bounds__(512) vlp_bsk_convert_kernel(const uint32_t* __
     __syncthreads();
   }
   for (uint32_t k = threadIdx.x; k < static_cast<uint32_t>(N); k += blockDim.x) {
-    const uint32_t t = k >> 4, pos = k & 15, c = pos >> 1, e = pos & 1;
-    uint32_t* dst = out + ((static_cast<size_t>(i) * kChunks + c) * 64 + t) * kChunkWords + e * 36;
+    const uint32_t b0 = k & 1, r = (k >> 1) & 7;
+    const uint32_t t = ((k >> 4) << 1) | (r >= 4 ? 1u : 0u);
+    const uint32_t slot = (b0 ? 4 : 0) + (r & 3);
+    const uint32_t chunk = (q / 3) * 4 + slot / 2;
+    uint32_t* dst = out + ((static_cast<size_t>(i) * kChunks + chunk) * kBT + t) * kChunkWords;
 #pragma unroll
     for (int l = 0; l < 3; l++) {
       const uint32_t o = u * 3 + l;
-      dst[o * 6 + r] = static_cast<uint32_t>(static_cast<uint64_t>(poly[l][k]) * c_mont % P);
+      dst[o * 6 + (slot & 1) * 3 + q % 3] = static_cast<uint32_t>(static_cast<uint64_t>(poly[l][k]) * c_mont % P);
     }
   }
 }
@@ -573,8 +594,8 @@ __global__ void vlp_copy_rows_kernel(const uint32_t* __restrict__ slots, Regions
 
 // ================================================================================ launchers
 void set_const_twiddles(const uint2* fwd16, const uint2* inv16) {
-  uint2 h[2][16];
-  for (int k = 0; k < 16; k++) {
+  uint2 h[2][8];
+  for (int k = 0; k < 8; k++) {
     h[0][k] = fwd16[k];
     h[1][k] = inv16[k];
   }

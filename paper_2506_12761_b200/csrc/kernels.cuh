@@ -9,14 +9,17 @@
 
 namespace vlp {
 
-// ---- blind rotation (K2): 4 bootstraps per CTA in lock-step, 64 threads each
+// ---- blind rotation (K2): 4 bootstraps per CTA in lock-step, 128 threads each, 8 coefficients per
+// thread per polynomial
+constexpr int kBT = 128;                            // threads per bootstrap
 constexpr int kBrBoot = 4;                          // bootstraps per CTA
-constexpr int kBrThreads = 64 * kBrBoot;            // 256
-constexpr int kChunks = 8;                          // bsk chunks per CMux step
-constexpr int kChunkWords = 76;                     // words per thread per chunk (72 used + pad)
-constexpr int kChunkBytes = 64 * kChunkWords * 4;   // 19456
+constexpr int kBrThreads = kBT * kBrBoot;           // 512
+constexpr int kChunks = 8;                          // bsk chunks per CMux step: round u (2) x slot pair (4)
+constexpr int kChunkWords = 36;                     // words per thread per chunk: [o 6][e 2][j 3]
+constexpr int kChunkBytes = kBT * kChunkWords * 4;  // 18432
 constexpr int kSlots = 6;                           // smem ring of bsk chunks
-constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * 64 * kChunkWords;  // 24,514,560
+constexpr int kTwSlots = 18;                        // lane-varying twiddle slots (stages 3..9)
+constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 23,224,320
 constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
                              kBrBoot * 640 * 2 + kSlots * 8;
 
@@ -38,8 +41,8 @@ struct BrArgs {
   uint32_t* nlwe;     // [rows][kNlwe] output of extract (unless raw_acc)
   uint32_t* raw_acc;  // debug: [njobs][2][N] accumulators instead of extracting
   const uint32_t* bsk;  // NTT-domain bsk, layout [i][chunk][t][kChunkWords]
-  const uint2* tw_fwd;  // [N] (w, floor(w 2^32 / p))
-  const uint2* tw_inv;
+  const uint2* twl_fwd;  // [kTwSlots][kBT] (w, floor(w 2^32 / p)) in thread order
+  const uint2* twl_inv;
 };
 
 struct KsArgs {
