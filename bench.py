@@ -182,12 +182,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(dev))
     stream = torch.cuda.current_stream()
 
+    from paper_2506_12761_b200.dist import shard_range, sharded_step
     wl = make_workload(args.config)
     m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
-    if wl.M % world or (wl.M // world) & (wl.M // world - 1):
-        raise SystemExit("records must split into power-of-two shards")
-    shard = wl.M // world
-    first = rank * shard
+    first, shard = shard_range(wl.M, world, rank)
     t_setup = time.time()
     keys = A.Keys(wl.key_seed)                 # client (every rank regenerates the same keys from the seed)
     srv = A.Server(keys, local)
@@ -199,19 +197,21 @@ def main():
     prog = A.Program.velopir(srv, m, first, shard)
     comb = A.Program.combine(srv, m, world) if (world > 1 and rank == 0) else None
     part = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
-    gathered = torch.zeros((world, wl.l_S, 632), dtype=torch.int32, device=dev) if world > 1 else None
+    gathered = torch.zeros((world * wl.l_S, 632), dtype=torch.int32, device=dev) if world > 1 else None
     out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     setup_s = time.time() - t_setup
 
-    def step(qdev):
-        if world > 1:
-            dist.broadcast(qdev, src=0)
+    def eval_shard(qdev):
         prog.eval(qdev, db, part if world > 1 else out, stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, part)  # shard roots -> every rank (rank 0 combines)
-            if rank == 0:
-                comb.eval(gathered.view(world * wl.l_S, 632), None, out, stream)
+        return part if world > 1 else out
+
+    def combine(roots):
+        comb.eval(roots, None, out, stream)
+        return out
+
+    def step(qdev):  # broadcast query -> shard eval -> gather shard roots -> top tree levels on rank 0
+        sharded_step(qdev, eval_shard, combine, world, rank, gathered)
 
     for _ in range(args.warmup):
         step(q)

@@ -93,6 +93,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Per-bootstrap named barrier (ids 1..4; 128 threads): the 4 bootstraps of a CTA only meet at the bsk ring.
+__device__ __forceinline__ void bar_boot(uint32_t g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kBT) : "memory");
+}
+
 __device__ __forceinline__ uint32_t* slot_wptr(const Regions& reg, uint32_t id) {
   const uint32_t r = id >> 28;  // select without dynamic indexing (keeps the params out of local memory)
   uint32_t* b = r == 0 ? reg.base[0] : (r == 1 ? reg.base[1] : (r == 2 ? reg.base[2] : reg.base[3]));
@@ -198,15 +203,15 @@ __device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __
 
 // Layout change of 3 polynomials through shared memory (xb: 3 x 1024 words of this bootstrap).
 template <int FROM, int TO>
-__device__ __forceinline__ void exchange(Poly3& d, uint32_t* xb, uint32_t t) {
+__device__ __forceinline__ void exchange(Poly3& d, uint32_t* xb, uint32_t t, uint32_t g) {
   const uint32_t bs = FROM == 0 ? baseA(t) : (FROM == 1 ? baseB(t) : baseC(t));
   const uint32_t bd = TO == 0 ? baseA(t) : (TO == 1 ? baseB(t) : baseC(t));
-  __syncthreads();
+  bar_boot(g);
 #pragma unroll
   for (int q = 0; q < 3; q++)
 #pragma unroll
     for (int r = 0; r < 8; r++) xb[q * N + (bs ^ (FROM == 0 ? cA(r) : (FROM == 1 ? cB(r) : cC(r))))] = d[q][r];
-  __syncthreads();
+  bar_boot(g);
 #pragma unroll
   for (int q = 0; q < 3; q++)
 #pragma unroll
@@ -229,6 +234,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
   uint32_t* xb_all = acc_all + kBrBoot * 2 * N;
   uint16_t* abar_all = reinterpret_cast<uint16_t*>(xb_all + kBrBoot * 3 * N);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(abar_all + kBrBoot * 640);
+  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kSlots);  // per-slot release counters (warps)
 
   const uint32_t tid = threadIdx.x, g = tid / kBT, t = tid % kBT;
   uint32_t* acc = acc_all + g * 2 * N;
@@ -243,7 +249,10 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
   const uint64_t total_chunks = static_cast<uint64_t>(my_groups) * a.steps * kChunks;
 
   if (tid == 0) {
-    for (int s = 0; s < kSlots; s++) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < kSlots; s++) {
+      mbar_init(&mbar[s], 1);
+      rel[s] = 0;
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -313,11 +322,11 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
         stage_A<0, false>(d);
         stage_A<1, false>(d);
         stage_A<2, false>(d);
-        exchange<0, 1>(d, xb, t);
+        exchange<0, 1>(d, xb, t, g);
         stage_BC<3, false>(d, twf);
         stage_BC<4, false>(d, twf);
         stage_BC<5, false>(d, twf);
-        exchange<1, 2>(d, xb, t);
+        exchange<1, 2>(d, xb, t, g);
         stage_BC<6, false>(d, twf);
         stage_BC<7, false>(d, twf);
         stage_BC<8, false>(d, twf);
@@ -353,10 +362,18 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
               mac[o][s] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);  // < 3.5p
             }
           }
-          __syncthreads();  // every thread is done with ring slot sl
-          if (tid == 0 && nseq + kSlots < total_chunks) {
-            fence_proxy_async();
-            issue(nseq + kSlots);
+          // release slot sl: the last of the CTA's 16 warps to finish with it refills it (no CTA barrier,
+          // so the 4 bootstraps may drift apart by up to the ring depth)
+          __syncwarp();
+          if ((tid & 31) == 0) {
+            __threadfence_block();
+            if (atomicAdd(&rel[sl], 1u) == kBrThreads / 32 - 1) {
+              atomicExch(&rel[sl], 0u);
+              if (nseq + kSlots < total_chunks) {
+                fence_proxy_async();
+                issue(nseq + kSlots);
+              }
+            }
           }
           nseq++;
         }
@@ -375,11 +392,11 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
         stage_BC<8, true>(d, twi);
         stage_BC<7, true>(d, twi);
         stage_BC<6, true>(d, twi);
-        exchange<2, 1>(d, xb, t);
+        exchange<2, 1>(d, xb, t, g);
         stage_BC<5, true>(d, twi);
         stage_BC<4, true>(d, twi);
         stage_BC<3, true>(d, twi);
-        exchange<1, 0>(d, xb, t);
+        exchange<1, 0>(d, xb, t, g);
         stage_A<2, true>(d);
         stage_A<1, true>(d);
         stage_A<0, true>(d);
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
           acc[u * N + t + 128u * r] += sum;
         }
       }
-      __syncthreads();
+      bar_boot(g);
     }
 
     // ---- S6 SampleExtract: a'_0 = a_0, a'_k = -a_{N-k}, b' = b_0

@@ -21,7 +21,7 @@ constexpr int kSlots = 6;                           // smem ring of bsk chunks
 constexpr int kTwSlots = 18;                        // lane-varying twiddle slots (stages 3..9)
 constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 23,224,320
 constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
-                             kBrBoot * 640 * 2 + kSlots * 8;
+                             kBrBoot * 640 * 2 + kSlots * 8 + kSlots * 4;
 
 // ---- key switch (K3)
 constexpr int kKsCt = 16;                                 // ciphertexts per CTA
