@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
       const uint32_t ab = abar[i];
 #pragma unroll 1
       for (int u = 0; u < 2; u++) {
+        const uint32_t umask = u ? 0xFFFFFFFFu : 0u;
         Poly3 d;
         // X^abar acc_u - acc_u (layout A: j = t + 128 r), gadget digits (R5, offset 0x81020400),
         // digit + p - 64 in [p-64, p+64)
@@ -355,7 +356,8 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
 #pragma unroll
             for (int e = 0; e < 2; e++) {
               const int s = 2 * pp + e;
-              uint64_t T = u ? (static_cast<uint64_t>(mac[o][s]) << 32) : 0ull;
+              // round 1 folds the round-0 value into the high word: REDC(acc*2^32 + X) = acc + REDC(X)
+              uint64_t T = static_cast<uint64_t>(mac[o][s] & umask) << 32;
 #pragma unroll
               for (int j = 0; j < 3; j++) T += static_cast<uint64_t>(x[e][j]) * kv[e][j];
               const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;

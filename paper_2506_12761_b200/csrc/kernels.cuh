@@ -17,7 +17,7 @@ constexpr int kBrThreads = kBT * kBrBoot;           // 512
 constexpr int kChunks = 8;                          // bsk chunks per CMux step: round u (2) x slot pair (4)
 constexpr int kChunkWords = 36;                     // words per thread per chunk: [o 6][e 2][j 3]
 constexpr int kChunkBytes = kBT * kChunkWords * 4;  // 18432
-constexpr int kSlots = 6;                           // smem ring of bsk chunks
+constexpr int kSlots = 7;                           // smem ring of bsk chunks
 constexpr int kTwSlots = 18;                        // lane-varying twiddle slots (stages 3..9)
 constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 23,224,320
 constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
