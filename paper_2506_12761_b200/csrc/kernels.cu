@@ -435,31 +435,20 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
 }
 
 // ================================================================================ K3 key switch
-// CTA: kKsCt ciphertexts x all 632 columns (160 threads x 4 columns), coefficients [i0, i1).
-// The ksk block of one coefficient i (8 x 3 rows, 60,672 B) is streamed into shared memory by TMA
-// (double-buffered) and used by all kKsCt ciphertexts.
+// CTA: kKsCt ciphertexts x all 632 columns (160 threads x 4 columns), coefficients [i0, i1) (a.parts
+// splits of [0, N) across blockIdx.y, reduced atomically).  For every (i, j) each ciphertext's digit selects
+// one of the three ksk rows; the thread reads its 16-byte column quad of that row straight from L2 through
+// L1 (a warp reads 512 contiguous bytes; the CTA's ciphertexts share the three rows in L1).  Only the
+// rounded masks live in shared memory (32 KB), so several CTAs fit per SM.
 __global__ void __launch_bounds__(kKsThreads) vlp_keyswitch_kernel(const KsArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* kbuf = reinterpret_cast<uint32_t*>(smem);  // [2][kKsRowWords]
-  uint16_t* abar = reinterpret_cast<uint16_t*>(kbuf + 2 * kKsRowWords);  // [kKsCt][N]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(abar + kKsCt * N);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(smem);  // [kKsCt][N]
 
   const uint32_t tid = threadIdx.x;
   const uint32_t c0 = blockIdx.x * kKsCt;
   const uint32_t nct = min(static_cast<uint32_t>(kKsCt), a.njobs - c0);
   const int i0 = static_cast<int>(blockIdx.y) * N / a.parts, i1 = static_cast<int>(blockIdx.y + 1) * N / a.parts;
 
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    bulk_load(kbuf, a.ksk + static_cast<size_t>(i0) * kKsRowWords, kKsRowWords * 4, &mbar[0]);
-    if (i0 + 1 < i1)
-      bulk_load(kbuf + kKsRowWords, a.ksk + static_cast<size_t>(i0 + 1) * kKsRowWords, kKsRowWords * 4, &mbar[1]);
-  }
   // S7 MUX combine + rounding to 16 bits (R6)
   for (uint32_t idx = tid; idx < nct * (i1 - i0); idx += blockDim.x) {
     const uint32_t c = idx / (i1 - i0), i = i0 + idx % (i1 - i0);
@@ -476,20 +465,20 @@ __global__ void __launch_bounds__(kKsThreads) vlp_keyswitch_kernel(const KsArgs 
 #pragma unroll
   for (int c = 0; c < kKsCt; c++) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0;
 
-  for (int i = i0; i < i1; i++) {
-    const int buf = (i - i0) & 1;
-    mbar_wait(&mbar[buf], static_cast<uint32_t>(((i - i0) >> 1) & 1));
-    const uint32_t* kb = kbuf + buf * kKsRowWords;
-    if (live) {
+  if (live) {
+    const uint32_t* kq = a.ksk + col;
+    for (int i = i0; i < i1; i++) {
+      uint32_t ab[kKsCt];
 #pragma unroll
-      for (int c = 0; c < kKsCt; c++) {
-        if (c >= static_cast<int>(nct)) break;
-        const uint32_t ab = abar[c * N + i];
+      for (int c = 0; c < kKsCt; c++) ab[c] = c < static_cast<int>(nct) ? abar[c * N + i] : 0u;
+      const uint32_t* ki = kq + static_cast<size_t>(i) * kKsRowWords;
 #pragma unroll
-        for (int j = 0; j < kKsT; j++) {
-          const uint32_t dg = (ab >> (14 - 2 * j)) & 3u;
+      for (int j = 0; j < kKsT; j++) {
+#pragma unroll
+        for (int c = 0; c < kKsCt; c++) {
+          const uint32_t dg = (ab[c] >> (14 - 2 * j)) & 3u;
           if (dg) {
-            const uint4 row = *reinterpret_cast<const uint4*>(kb + (j * 3 + (dg - 1)) * kCt + col);
+            const uint4 row = __ldg(reinterpret_cast<const uint4*>(ki + (j * 3 + (dg - 1)) * kCt));
             acc[c][0] += row.x;
             acc[c][1] += row.y;
             acc[c][2] += row.z;
@@ -497,12 +486,6 @@ __global__ void __launch_bounds__(kKsThreads) vlp_keyswitch_kernel(const KsArgs 
           }
         }
       }
-    }
-    __syncthreads();
-    if (tid == 0 && i + 2 < i1) {
-      fence_proxy_async();
-      bulk_load(kbuf + buf * kKsRowWords, a.ksk + static_cast<size_t>(i + 2) * kKsRowWords, kKsRowWords * 4,
-                &mbar[buf]);
     }
   }
   if (!live) return;
@@ -655,7 +638,7 @@ cudaError_t launch_keyswitch(const KsArgs& a0, cudaStream_t st) {
   KsArgs a = a0;
   const uint32_t tiles = (a.njobs + kKsCt - 1) / kKsCt;
   int parts = 1;
-  while (parts < 16 && tiles * parts * 2 <= 2 * 148) parts *= 2;  // fill the chip on narrow levels
+  while (parts < 16 && tiles * parts < 4 * 148) parts *= 2;  // fill the chip on narrow levels
   a.parts = parts;
   if (parts > 1) vlp_ks_init_kernel<<<a.njobs, 128, 0, st>>>(a);
   vlp_keyswitch_kernel<<<dim3(tiles, parts), kKsThreads, kKsSmemBytes, st>>>(a);

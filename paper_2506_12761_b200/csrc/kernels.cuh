@@ -27,7 +27,7 @@ constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoo
 constexpr int kKsCt = 16;                                 // ciphertexts per CTA
 constexpr int kKsThreads = 160;                           // 158 column quads (632 words)
 constexpr int kKsRowWords = kKsT * 3 * kCt;               // ksk words per coefficient i: 15168
-constexpr int kKsSmemBytes = 2 * kKsRowWords * 4 + kKsCt * N * 2 + 2 * 8;
+constexpr int kKsSmemBytes = kKsCt * N * 2;
 
 struct Regions {
   uint32_t* base[4];  // kRegIn0, kRegIn1, kRegMid, kRegOut; rows of kCt words
