@@ -152,12 +152,69 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_nand(args, rank, world, local, dev, stream, A, L, dist):
+    """Config 5: a batch of independent NAND bootstraps (BR + extract + KS) on fresh encryptions of uniform
+    bits, split evenly over the ranks (no collective on the data path: weak sharding of one batch)."""
+    import torch
+    total = args.nand
+    per = total // world
+    a_bits, b_bits = nand_inputs(total, 2005)
+    keys = A.Keys(1005)
+    srv = A.Server(keys, local)
+    lo = rank * per
+    a = A.to_device(keys.encrypt_bits(a_bits[lo:lo + per], 2005, lo), local)
+    b = A.to_device(keys.encrypt_bits(b_bits[lo:lo + per], 2005, total + lo), local)
+    prog = A.Program.gates(srv, L.NAND, per)
+    out = torch.zeros((per, 632), dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        prog.eval(a, b, out, stream)
+    torch.cuda.synchronize()
+    ok = bool(np.array_equal(keys.decrypt_bits(A.to_host(out)), 1 - (a_bits[lo:lo + per] & b_bits[lo:lo + per])))
+    assert ok, "NAND outputs decrypt wrong"
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(local) if rank == 0 else None
+    prog.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        prog.eval(a, b, out, stream)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    br_ms, ks_ms, br_n, _ = prog.profile_read(reset=True)
+    tot = torch.tensor([sum(a0.elapsed_time(b0) for a0, b0 in ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / args.steps
+    if rank == 0:
+        peak, how = int_peak()
+        achieved = ops_per_br() * per * args.steps / (br_ms / 1e3) / 1e9
+        print(json.dumps({
+            "metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"cfg5_nand_{total}", "gates": total, "l2": "flushed between steps (untimed)"},
+            "roofline": {"bound": "alu", "kernel": "vlp_blind_rotate_kernel", "achieved": achieved, "peak": peak,
+                         "unit": "Gop/s (int32 lane ops)", "frac": achieved / peak, "peak_source": how,
+                         "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
+                         "traffic": None},
+            "cpu_baseline": None, "e2e": None, "clocks": clocks,
+            "gpu_launches": prog.info.kernel_launches * args.steps}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--nand", type=int, default=1 << 17, help="config 5: NAND gates per step (split over ranks)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -183,6 +240,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     from paper_2506_12761_b200.dist import shard_range, sharded_step
+    if args.config == 5:
+        return run_nand(args, rank, world, local, dev, stream, A, L, dist)
     wl = make_workload(args.config)
     m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
     first, shard = shard_range(wl.M, world, rank)

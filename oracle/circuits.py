@@ -228,8 +228,13 @@ def velopir(B, mode, q, records, payloads, l, d, l_S, flags, threads=None):
 
 
 # ------------------------------------------------------------------------------- plain predicate (8(c))
-def plain_match(mode, qvals, rec_words, d, flags):
-    """The plaintext predicate of thm:bb1 / thm:bb2 / IdM, unsigned values (R11-R13)."""
+def plain_match(mode, qvals, rec_words, d, flags, l=None):
+    """The plaintext predicate of thm:bb1 / thm:bb2 / IdM (R11-R13).  Values are l-bit words; without
+    F_UNSIGNED (and with l given) they are compared as two's complement, as the paper's comparators do."""
+    if mode == MODE_INTV and l is not None and not flags & F_UNSIGNED:
+        sg = lambda v: int(v) - (1 << l) if (int(v) >> (l - 1)) & 1 else int(v)  # noqa: E731
+        qvals = [sg(v) for v in qvals]
+        rec_words = [sg(v) for v in rec_words]
     if mode == MODE_INTV:
         ok = True
         for a in range(d):
@@ -241,10 +246,10 @@ def plain_match(mode, qvals, rec_words, d, flags):
     return qvals[0] == rec_words[0]
 
 
-def plain_result(mode, qvals, records, payloads, d, flags):
+def plain_result(mode, qvals, records, payloads, d, flags, l=None):
     """R = XOR (OR with F_OR_REDUCE) of the payloads of all matching records; 0 if none (R19)."""
     r = 0
     for rec, pay in zip(records, payloads):
-        if plain_match(mode, qvals, rec, d, flags):
+        if plain_match(mode, qvals, rec, d, flags, l):
             r = (r | int(pay)) if flags & F_OR_REDUCE else (r ^ int(pay))
     return r

@@ -225,3 +225,55 @@ def test_config2_full_size_sampled(server):
         assert np.array_equal(mid[prog.node_row(0, i), :631], v)
         for j in range(wl.l_S):
             assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j])
+
+
+def _full_parity_small(server, mode, d, l_I, l_S, flags, records, payloads, query, okeys_seed=SEED):
+    """Full byte parity of a small instance (every record's v and masked payload, and R) vs the oracle."""
+    m = A.meta(mode, len(records), l_I, l_S, d, flags)
+    k = server.keys
+    okeys = O.OracleKeys(okeys_seed)
+    q = k.encrypt_query(m, query, 7)
+    db = k.encrypt_db(m, np.array(records, np.uint64), np.array(payloads, np.uint64), pk_seed=99)
+    prog = A.Program.velopir(server, m)
+    out = torch.zeros((l_S, 632), dtype=torch.int32, device="cuda:0")
+    prog.eval(A.to_device(q), A.to_device(db), out)
+    torch.cuda.synchronize()
+    out = A.to_host(out)
+    oq = OP.encrypt_query(okeys, query, l_I, 7)
+    recs, pays = [], []
+    for i in range(len(records)):
+        r, p = OP.server_enc_record(okeys, 99, i, list(records[i]), payloads[i], l_I, l_S)
+        recs.append(r)
+        pays.append(p)
+    R, vs, masked = OC.velopir(OC.TfheBackend(okeys), mode, oq, recs, pays, l_I, d, l_S, flags)
+    mid = A.to_host(prog.intermediate())
+    for i in range(len(records)):
+        if len(records) > 1 or not (flags & OC.F_SUM_TREE):
+            assert np.array_equal(mid[prog.node_row(0, i), :631], vs[i]), ("v", i)
+    for j in range(l_S):
+        assert np.array_equal(out[j, :631], R[j]), ("R", j)
+    want = OC.plain_result(mode, query, records, payloads, d, flags, l_I)
+    assert k.decrypt_value(out) == want
+    return want
+
+
+def test_paper_cov_mode_full_parity(server):
+    """Paper CoV (alg:BB2: HomEQ(x, loc_x) AND HomEQ(y, loc_y)), EQ tree, d = 2, l = 4, 3 records (not a
+    power of two), one exact match."""
+    recs = [(3, 9), (5, 12), (3, 12)]
+    want = _full_parity_small(server, OC.MODE_COV, 2, 4, 3, OC.CONFIG_FLAGS, recs, [5, 2, 6], [5, 12])
+    assert want == 2
+
+
+def test_paper_literal_intv_serial_full_parity(server):
+    """Paper-literal IntV: signed comparators (final MUX on ct1[l-1]), half-open upper bound via
+    HomCompL, serial HomEQ flag irrelevant, serial HomSum from trivial Enc(0)."""
+    recs = [(-3 & 15, 2), (1, 7), (-8 & 15, -1 & 15)]
+    flags = 0
+    _full_parity_small(server, OC.MODE_INTV, 1, 4, 2, flags, recs, [1, 2, 3], [1])
+
+
+def test_idm_serial_eq_or_reduce_full_parity(server):
+    """IdM with the serial alg:HomEQ and the OR reduction flag (R19), 4 records."""
+    flags = OC.F_SUM_TREE | OC.F_OR_REDUCE
+    _full_parity_small(server, OC.MODE_IDM, 1, 5, 2, flags, [(7,), (19,), (7,), (30,)], [1, 2, 2, 3], [7])

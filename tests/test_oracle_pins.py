@@ -306,7 +306,7 @@ def test_velopir_plain_configs():
                 pc = [[B.const(b) for b in P.bits_of(v, 5)] for v in pays]
                 R, _, _ = C.velopir(B, mode, qc, rc, pc, l, d, 5, flags, threads=1)
                 got = sum(int(b[0]) << j for j, b in enumerate(R))
-                assert got == C.plain_result(mode, q, recs, pays, d, flags), (mode, d, flags, M)
+                assert got == C.plain_result(mode, q, recs, pays, d, flags, l), (mode, d, flags, M)
 
 
 # ----------------------------------------------------------------------------------- P8 on TFHE
