@@ -43,16 +43,20 @@ __device__ __forceinline__ uint32_t shoup(uint32_t y, uint32_t w, uint32_t ws) {
   const uint32_t q = __umulhi(y, ws);
   return y * w - q * P;
 }
+// a + b as a three-input add with a runtime zero (BrArgs::zero, always 0): an IADD3 on the ALU pipe, which
+// keeps ptxas from turning the add into IMAD.IADD on the heavy FMA pipe -- the binding unit of the blind
+// rotation.
+__device__ __forceinline__ uint32_t add_alu(uint32_t a, uint32_t b, uint32_t zero) { return a + b + zero; }
 // Forward CT butterfly, inputs / outputs in [0, 4p).
-__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws) {
+__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, uint32_t z = 0) {
   const uint32_t xr = umin(x, x - P2);
   const uint32_t t = shoup(y, w, ws);
-  x = xr + t;
+  x = add_alu(xr, t, z);
   y = xr - t + P2;
 }
 // Inverse GS butterfly, inputs / outputs in [0, 2p).
-__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws) {
-  uint32_t s = x + y;
+__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, uint32_t z = 0) {
+  uint32_t s = add_alu(x, y, z);
   s = umin(s, s - P2);
   const uint32_t d = x - y + P2;
   x = s;
@@ -132,7 +136,7 @@ typedef uint32_t Poly3[3][8];
 
 // Stages 0-2 (layout A): pair (r, r | rb), rb = 4 >> s; twiddle k = 2^s + (r >> (3 - s)), uniform.
 template <int S, bool INV>
-__device__ __forceinline__ void stage_A(Poly3& d) {
+__device__ __forceinline__ void stage_A(Poly3& d, uint32_t z) {
   constexpr int rb = 4 >> S;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
@@ -140,8 +144,8 @@ __device__ __forceinline__ void stage_A(Poly3& d) {
     const uint2 w = c_tw[INV][(1 << S) + (r >> (3 - S))];
 #pragma unroll
     for (int p = 0; p < 3; p++) {
-      if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
-      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+      if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
+      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
     }
   }
 }
@@ -149,7 +153,7 @@ __device__ __forceinline__ void stage_A(Poly3& d) {
 // Lane-varying stages 3-8: layout B (S = 3..5) or C (S = 6..8); rb = 4 >> (S % 3); twiddle slot
 // q = r >> (3 - S % 3) at table row kSlotBase[S] + q, column t.
 template <int S, bool INV>
-__device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl) {
+__device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl, uint32_t z) {
   constexpr int rb = 4 >> (S % 3);
   constexpr int base = S == 3 ? 0 : S == 4 ? 1 : S == 5 ? 3 : S == 6 ? 7 : S == 7 ? 8 : 10;
 #pragma unroll
@@ -158,15 +162,15 @@ __device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl
     const uint2 w = __ldg(twl + (base + (r >> (3 - S % 3))) * kBT);
 #pragma unroll
     for (int p = 0; p < 3; p++) {
-      if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y);
-      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y);
+      if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
+      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
     }
   }
 }
 
 // Stage 9 forward: lane-pair exchange (lower lane keeps pairs r = 0..3, upper lane r = 4..7), then
 // butterflies on (d[i], d[4+i]) with twiddle slots 14..17.
-__device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __restrict__ twl) {
+__device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __restrict__ twl, uint32_t z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
@@ -177,7 +181,7 @@ __device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __
       const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
       uint32_t x = lo ? d[p][i] : recv;
       uint32_t y = lo ? recv : d[p][4 + i];
-      ct_bfly(x, y, w.x, w.y);
+      ct_bfly(x, y, w.x, w.y, z);
       d[p][i] = x;
       d[p][4 + i] = y;
     }
@@ -185,14 +189,14 @@ __device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __
 }
 
 // Stage 9 inverse: butterflies on (d[i], d[4+i]), then the reverse lane-pair exchange (back to layout C).
-__device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __restrict__ twl) {
+__device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __restrict__ twl, uint32_t z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const uint2 w = __ldg(twl + (14 + i) * kBT);
 #pragma unroll
     for (int p = 0; p < 3; p++) {
-      gs_bfly(d[p][i], d[p][4 + i], w.x, w.y);
+      gs_bfly(d[p][i], d[p][4 + i], w.x, w.y, z);
       const uint32_t send = lo ? d[p][4 + i] : d[p][i];
       const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
       d[p][i] = lo ? d[p][i] : recv;
@@ -242,6 +246,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
   uint16_t* abar = abar_all + g * 640;
   const uint2* twf = a.twl_fwd + t;
   const uint2* twi = a.twl_inv + t;
+  const uint32_t zr = a.zero;
 
   const uint32_t ngroups = (a.njobs + kBrBoot - 1) / kBrBoot;
   if (blockIdx.x >= ngroups) return;
@@ -320,18 +325,18 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
           d[1][r] = ((w >> 18) & 127u) + (P - 64u);
           d[2][r] = ((w >> 11) & 127u) + (P - 64u);
         }
-        stage_A<0, false>(d);
-        stage_A<1, false>(d);
-        stage_A<2, false>(d);
+        stage_A<0, false>(d, zr);
+        stage_A<1, false>(d, zr);
+        stage_A<2, false>(d, zr);
         exchange<0, 1>(d, xb, t, g);
-        stage_BC<3, false>(d, twf);
-        stage_BC<4, false>(d, twf);
-        stage_BC<5, false>(d, twf);
+        stage_BC<3, false>(d, twf, zr);
+        stage_BC<4, false>(d, twf, zr);
+        stage_BC<5, false>(d, twf, zr);
         exchange<1, 2>(d, xb, t, g);
-        stage_BC<6, false>(d, twf);
-        stage_BC<7, false>(d, twf);
-        stage_BC<8, false>(d, twf);
-        stage9_fwd(d, t, twf);
+        stage_BC<6, false>(d, twf, zr);
+        stage_BC<7, false>(d, twf, zr);
+        stage_BC<8, false>(d, twf, zr);
+        stage9_fwd(d, t, twf, zr);
         // MAC: mac[o][s] (+)= sum_j Dhat_{3u+j}[s] * B[3u+j][o][s] (Montgomery; key holds N^-1 * 2^32)
 #pragma unroll
         for (int pp = 0; pp < 4; pp++) {
@@ -356,12 +361,12 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
 #pragma unroll
             for (int e = 0; e < 2; e++) {
               const int s = 2 * pp + e;
-              // round 1 folds the round-0 value into the high word: REDC(acc*2^32 + X) = acc + REDC(X)
-              uint64_t T = static_cast<uint64_t>(mac[o][s] & umask) << 32;
-#pragma unroll
-              for (int j = 0; j < 3; j++) T += static_cast<uint64_t>(x[e][j]) * kv[e][j];
+              uint64_t T = static_cast<uint64_t>(x[e][0]) * kv[e][0];
+              T += static_cast<uint64_t>(x[e][1]) * kv[e][1];
+              T += static_cast<uint64_t>(x[e][2]) * kv[e][2];
               const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
-              mac[o][s] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);  // < 3.5p
+              const uint32_t y = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);  // < 1.75p
+              mac[o][s] = y + (mac[o][s] & umask);  // round 0: y; round 1: acc + y < 3.5p
             }
           }
           // release slot sl: the last of the CTA's 16 warps to finish with it refills it (no CTA barrier,
@@ -390,18 +395,18 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
             const uint32_t v = u ? mac[3 + l][s] : mac[l][s];
             d[l][s] = umin(v, v - P2);  // [0, 2p)
           }
-        stage9_inv(d, t, twi);
-        stage_BC<8, true>(d, twi);
-        stage_BC<7, true>(d, twi);
-        stage_BC<6, true>(d, twi);
+        stage9_inv(d, t, twi, zr);
+        stage_BC<8, true>(d, twi, zr);
+        stage_BC<7, true>(d, twi, zr);
+        stage_BC<6, true>(d, twi, zr);
         exchange<2, 1>(d, xb, t, g);
-        stage_BC<5, true>(d, twi);
-        stage_BC<4, true>(d, twi);
-        stage_BC<3, true>(d, twi);
+        stage_BC<5, true>(d, twi, zr);
+        stage_BC<4, true>(d, twi, zr);
+        stage_BC<3, true>(d, twi, zr);
         exchange<1, 0>(d, xb, t, g);
-        stage_A<2, true>(d);
-        stage_A<1, true>(d);
-        stage_A<0, true>(d);
+        stage_A<2, true>(d, zr);
+        stage_A<1, true>(d, zr);
+        stage_A<0, true>(d, zr);
         // centered lift of the three limbs, recombine mod 2^32, acc_u += (layout A: j = t + 128 r)
 #pragma unroll
         for (int r = 0; r < 8; r++) {

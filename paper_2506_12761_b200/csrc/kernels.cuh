@@ -43,6 +43,7 @@ struct BrArgs {
   const uint32_t* bsk;  // NTT-domain bsk, layout [i][chunk][t][kChunkWords]
   const uint2* twl_fwd;  // [kTwSlots][kBT] (w, floor(w 2^32 / p)) in thread order
   const uint2* twl_inv;
+  uint32_t zero;  // always 0 (a runtime zero; see add_alu in kernels.cu)
 };
 
 struct KsArgs {
