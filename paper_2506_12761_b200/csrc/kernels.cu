@@ -302,15 +302,19 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
 
     // ---- S5: CMux steps
     uint32_t mac[6][8];  // output o = (component u_out, limb) at this thread's 8 NTT positions
+    Poly3 d0;            // round 0 (component a) transformed digits
 #pragma unroll
     for (int o = 0; o < 6; o++)
 #pragma unroll
       for (int s = 0; s < 8; s++) mac[o][s] = 0;
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+      for (int s = 0; s < 8; s++) d0[j][s] = 0;
     for (int i = 0; i < a.steps; i++) {
       const uint32_t ab = abar[i];
 #pragma unroll 1
       for (int u = 0; u < 2; u++) {
-        const uint32_t umask = u ? 0xFFFFFFFFu : 0u;
         Poly3 d;
         // X^abar acc_u - acc_u (layout A: j = t + 128 r), gadget digits (R5, offset 0x81020400),
         // digit + p - 64 in [p-64, p+64)
@@ -337,36 +341,43 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
         stage_BC<7, false>(d, twf, zr);
         stage_BC<8, false>(d, twf, zr);
         stage9_fwd(d, t, twf, zr);
-        // MAC: mac[o][s] (+)= sum_j Dhat_{3u+j}[s] * B[3u+j][o][s] (Montgomery; key holds N^-1 * 2^32)
+        if (u == 0) {  // keep component 0's transformed digits for the MAC after round 1
 #pragma unroll
-        for (int pp = 0; pp < 4; pp++) {
+          for (int j = 0; j < 3; j++)
+#pragma unroll
+            for (int r = 0; r < 8; r++) d0[j][r] = d[j][r];
+          continue;
+        }
+        // MAC: mac[o][s] = sum_{q<6} Dhat_q[s] * B[q][o][s] (Montgomery, one REDC per output; the key holds
+        // N^-1 * 2^32).  T < 6p^2 and T + m p < 2^64; output < 2.5p.
+#pragma unroll
+        for (int pp = 0; pp < kChunks; pp++) {
           const uint32_t sl = nseq % kSlots;
           mbar_wait(&mbar[sl], static_cast<uint32_t>((nseq / kSlots) & 1));
           const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
-          uint32_t x[2][3];
 #pragma unroll
-          for (int e = 0; e < 2; e++)
+          for (int e = 0; e < 2; e++) {
+            const int sp = 2 * pp + e;
+            uint32_t x[6];
 #pragma unroll
             for (int j = 0; j < 3; j++) {
-              uint32_t v = d[j][2 * pp + e];
+              uint32_t v = d0[j][sp];
               v = umin(v, v - P2);
-              x[e][j] = umin(v, v - P);  // [0, p)
+              x[j] = umin(v, v - P);  // [0, p)
+              v = d[j][sp];
+              v = umin(v, v - P2);
+              x[3 + j] = umin(v, v - P);
             }
 #pragma unroll
-          for (int o = 0; o < 6; o++) {
-            const uint2 k01 = reinterpret_cast<const uint2*>(rec + o * 6)[0];
-            const uint2 k23 = reinterpret_cast<const uint2*>(rec + o * 6)[1];
-            const uint2 k45 = reinterpret_cast<const uint2*>(rec + o * 6)[2];
-            const uint32_t kv[2][3] = {{k01.x, k01.y, k23.x}, {k23.y, k45.x, k45.y}};
+            for (int o = 0; o < 6; o++) {
+              const uint2* kp = reinterpret_cast<const uint2*>(rec + o * 12 + e * 6);
+              const uint2 k0 = kp[0], k1 = kp[1], k2 = kp[2];
+              const uint32_t kv[6] = {k0.x, k0.y, k1.x, k1.y, k2.x, k2.y};
+              uint64_t T = static_cast<uint64_t>(x[0]) * kv[0];
 #pragma unroll
-            for (int e = 0; e < 2; e++) {
-              const int s = 2 * pp + e;
-              uint64_t T = static_cast<uint64_t>(x[e][0]) * kv[e][0];
-              T += static_cast<uint64_t>(x[e][1]) * kv[e][1];
-              T += static_cast<uint64_t>(x[e][2]) * kv[e][2];
+              for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(x[q]) * kv[q];
               const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
-              const uint32_t y = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);  // < 1.75p
-              mac[o][s] = y + (mac[o][s] & umask);  // round 0: y; round 1: acc + y < 3.5p
+              mac[o][sp] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
             }
           }
           // release slot sl: the last of the CTA's 16 warps to finish with it refills it (no CTA barrier,
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
 #pragma unroll
           for (int s = 0; s < 8; s++) {
             const uint32_t v = u ? mac[3 + l][s] : mac[l][s];
-            d[l][s] = umin(v, v - P2);  // [0, 2p)
+            d[l][s] = umin(v, v - P2);  // [0, 2p) (mac < 2.5p)
           }
         stage9_inv(d, t, twi, zr);
         stage_BC<8, true>(d, twi, zr);
@@ -537,7 +548,7 @@ __global__ void vlp_ks_init_kernel(const KsArgs a) {
 // One CTA per (i, key row q, component u): split the 1024 torus32 coefficients into 3 signed limbs, forward
 // NTT each limb polynomial mod p (plain, fully reduced; natural twiddle table), multiply by
 // N^-1 * 2^32 mod p, and scatter NTT position k to the lane/slot that holds it after the forward
-// transform (inverse of posF): chunk (q / 3) * 4 + slot / 2, word o*6 + (slot & 1)*3 + q % 3, o = u*3 + limb.
+// transform (inverse of posF): chunk slot / 2, word o*12 + (slot & 1)*6 + q, o = u*3 + limb.
 __global__ void __launch_bounds__(512) vlp_bsk_convert_kernel(const uint32_t* __restrict__ raw,
                                                               uint32_t* __restrict__ out,
                                                               const uint2* __restrict__ tw, uint32_t c_mont) {
@@ -575,12 +586,12 @@ __global__ void __launch_bounds__(512) vlp_bsk_convert_kernel(const uint32_t* __
     const uint32_t b0 = k & 1, r = (k >> 1) & 7;
     const uint32_t t = ((k >> 4) << 1) | (r >= 4 ? 1u : 0u);
     const uint32_t slot = (b0 ? 4 : 0) + (r & 3);
-    const uint32_t chunk = (q / 3) * 4 + slot / 2;
+    const uint32_t chunk = slot / 2;
     uint32_t* dst = out + ((static_cast<size_t>(i) * kChunks + chunk) * kBT + t) * kChunkWords;
 #pragma unroll
     for (int l = 0; l < 3; l++) {
       const uint32_t o = u * 3 + l;
-      dst[o * 6 + (slot & 1) * 3 + q % 3] = static_cast<uint32_t>(static_cast<uint64_t>(poly[l][k]) * c_mont % P);
+      dst[o * 12 + (slot & 1) * 6 + q] = static_cast<uint32_t>(static_cast<uint64_t>(poly[l][k]) * c_mont % P);
     }
   }
 }

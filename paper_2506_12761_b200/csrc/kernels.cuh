@@ -14,12 +14,12 @@ namespace vlp {
 constexpr int kBT = 128;                            // threads per bootstrap
 constexpr int kBrBoot = 4;                          // bootstraps per CTA
 constexpr int kBrThreads = kBT * kBrBoot;           // 512
-constexpr int kChunks = 8;                          // bsk chunks per CMux step: round u (2) x slot pair (4)
-constexpr int kChunkWords = 36;                     // words per thread per chunk: [o 6][e 2][j 3]
-constexpr int kChunkBytes = kBT * kChunkWords * 4;  // 18432
-constexpr int kSlots = 7;                           // smem ring of bsk chunks
+constexpr int kChunks = 4;                          // bsk chunks per CMux step: slot pairs (positions)
+constexpr int kChunkWords = 76;                     // words per thread per chunk: [o 6][e 2][q 6] + 4 pad
+constexpr int kChunkBytes = kBT * kChunkWords * 4;  // 38912
+constexpr int kSlots = 3;                           // smem ring of bsk chunks
 constexpr int kTwSlots = 18;                        // lane-varying twiddle slots (stages 3..9)
-constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 23,224,320
+constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 24,514,560
 constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
                              kBrBoot * 640 * 2 + kSlots * 8 + kSlots * 4;
 
