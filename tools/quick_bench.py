@@ -1,5 +1,7 @@
 """Developer tool: time the NAND gate batch (BR + KS kernels) and config 2 on one GPU with CUDA events."""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import time
 
 import numpy as np
