@@ -97,7 +97,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Per-bootstrap named barrier (ids 1..4; 128 threads): the 4 bootstraps of a CTA only meet at the bsk ring.
+// ------------------------------------------------------------------------------ TMEM as spill space
+// tcgen05.ld / tcgen05.st move registers to and from this warp's 32 TMEM lanes (32x32b shape: lane = thread,
+// one 32-bit column per register).  No MMA is issued; TMEM only extends the register file.
+__device__ __forceinline__ void tmem_st2(uint32_t ta, uint32_t a, uint32_t b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t ta, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t ta, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Per-bootstrap named barrier (ids 1..kBrBoot; 128 threads): the 4 bootstraps of a CTA only meet at the bsk ring.
 __device__ __forceinline__ void bar_boot(uint32_t g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kBT) : "memory");
 }
@@ -239,6 +259,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
   uint16_t* abar_all = reinterpret_cast<uint16_t*>(xb_all + kBrBoot * 3 * N);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(abar_all + kBrBoot * 640);
   uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kSlots);  // per-slot release counters (warps)
+  uint32_t* tmem_base_sh = rel + kSlots;
 
   const uint32_t tid = threadIdx.x, g = tid / kBT, t = tid % kBT;
   uint32_t* acc = acc_all + g * 2 * N;
@@ -260,7 +281,18 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
     }
     fence_mbar_init();
   }
+  if (tid < 32) {  // warp 0 allocates the CTA's TMEM (one CTA per SM: smem-bound)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this warp's TMEM: lanes 32 (warp % 4) .. +31, column slot warp / 4
+  const uint32_t warp = tid >> 5;
+  const uint32_t tm = *tmem_base_sh + ((32u * (warp & 3u)) << 16) + (warp >> 2) * kTmemSlotCols;
   // chunk sequence n -> (step (n / 8) % steps, chunk n % 8) of the bsk; ring slot n % kSlots
   auto issue = [&](uint64_t nseq) {
     const uint32_t step = static_cast<uint32_t>((nseq / kChunks) % a.steps), c = nseq % kChunks;
@@ -301,16 +333,6 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
     __syncthreads();
 
     // ---- S5: CMux steps
-    uint32_t mac[6][8];  // output o = (component u_out, limb) at this thread's 8 NTT positions
-    Poly3 d0;            // round 0 (component a) transformed digits
-#pragma unroll
-    for (int o = 0; o < 6; o++)
-#pragma unroll
-      for (int s = 0; s < 8; s++) mac[o][s] = 0;
-#pragma unroll
-    for (int j = 0; j < 3; j++)
-#pragma unroll
-      for (int s = 0; s < 8; s++) d0[j][s] = 0;
     for (int i = 0; i < a.steps; i++) {
       const uint32_t ab = abar[i];
 #pragma unroll 1
@@ -341,13 +363,16 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
         stage_BC<7, false>(d, twf, zr);
         stage_BC<8, false>(d, twf, zr);
         stage9_fwd(d, t, twf, zr);
-        if (u == 0) {  // keep component 0's transformed digits for the MAC after round 1
+        if (u == 0) {  // park component 0's transformed digits in TMEM for the MAC after round 1
 #pragma unroll
-          for (int j = 0; j < 3; j++)
-#pragma unroll
-            for (int r = 0; r < 8; r++) d0[j][r] = d[j][r];
+          for (int j = 0; j < 3; j++) tmem_st8(tm + 64 + 8 * j, d[j]);
           continue;
         }
+        Poly3 d0;
+        tmem_wait_st();
+#pragma unroll
+        for (int j = 0; j < 3; j++) tmem_ld8(tm + 64 + 8 * j, d0[j]);
+        tmem_wait_ld();
         // MAC: mac[o][s] = sum_{q<6} Dhat_q[s] * B[q][o][s] (Montgomery, one REDC per output; the key holds
         // N^-1 * 2^32).  T < 6p^2 and T + m p < 2^64; output < 2.5p.
 #pragma unroll
@@ -355,33 +380,37 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
           const uint32_t sl = nseq % kSlots;
           mbar_wait(&mbar[sl], static_cast<uint32_t>((nseq / kSlots) & 1));
           const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
+          uint32_t x[2][6];  // the 6 transformed digit polynomials at positions 2pp + e, reduced to [0, p)
 #pragma unroll
-          for (int e = 0; e < 2; e++) {
-            const int sp = 2 * pp + e;
-            uint32_t x[6];
+          for (int e = 0; e < 2; e++)
 #pragma unroll
             for (int j = 0; j < 3; j++) {
-              uint32_t v = d0[j][sp];
+              uint32_t v = d0[j][2 * pp + e];
               v = umin(v, v - P2);
-              x[j] = umin(v, v - P);  // [0, p)
-              v = d[j][sp];
+              x[e][j] = umin(v, v - P);
+              v = d[j][2 * pp + e];
               v = umin(v, v - P2);
-              x[3 + j] = umin(v, v - P);
+              x[e][3 + j] = umin(v, v - P);
             }
 #pragma unroll
-            for (int o = 0; o < 6; o++) {
-              const uint2* kp = reinterpret_cast<const uint2*>(rec + o * 12 + e * 6);
-              const uint2 k0 = kp[0], k1 = kp[1], k2 = kp[2];
-              const uint32_t kv[6] = {k0.x, k0.y, k1.x, k1.y, k2.x, k2.y};
-              uint64_t T = static_cast<uint64_t>(x[0]) * kv[0];
+          for (int o = 0; o < 6; o++) {
+            const uint4* kp = reinterpret_cast<const uint4*>(rec + o * 12);  // [e 2][q 6]
+            const uint4 k0 = kp[0], k1 = kp[1], k2 = kp[2];
+            const uint32_t kv[2][6] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y}, {k1.z, k1.w, k2.x, k2.y, k2.z, k2.w}};
+            uint32_t res[2];
 #pragma unroll
-              for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(x[q]) * kv[q];
+            for (int e = 0; e < 2; e++) {
+              uint64_t T = static_cast<uint64_t>(x[e][0]) * kv[e][0];
+#pragma unroll
+              for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(x[e][q]) * kv[e][q];
               const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
-              mac[o][sp] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
+              res[e] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
             }
+            // MAC output o = 3 u_out + limb at positions 2pp, 2pp+1 -> TMEM column 32 u_out + 8 limb + 2pp
+            tmem_st2(tm + 32 * (o / 3) + 8 * (o % 3) + 2 * pp, res[0], res[1]);
           }
-          // release slot sl: the last of the CTA's 16 warps to finish with it refills it (no CTA barrier,
-          // so the 4 bootstraps may drift apart by up to the ring depth)
+          // release slot sl: the last of the CTA's warps to finish with it refills it (no CTA barrier,
+          // so the CTA's bootstraps may drift apart by up to the ring depth)
           __syncwarp();
           if ((tid & 31) == 0) {
             __threadfence_block();
@@ -396,16 +425,17 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
           nseq++;
         }
       }
+      tmem_wait_st();
 #pragma unroll 1
       for (int u = 0; u < 2; u++) {
         Poly3 d;
 #pragma unroll
+        for (int l = 0; l < 3; l++) tmem_ld8(tm + 32 * u + 8 * l, d[l]);
+        tmem_wait_ld();
+#pragma unroll
         for (int l = 0; l < 3; l++)
 #pragma unroll
-          for (int s = 0; s < 8; s++) {
-            const uint32_t v = u ? mac[3 + l][s] : mac[l][s];
-            d[l][s] = umin(v, v - P2);  // [0, 2p) (mac < 2.5p)
-          }
+          for (int s = 0; s < 8; s++) d[l][s] = umin(d[l][s], d[l][s] - P2);  // [0, 2p) (mac < 2.5p)
         stage9_inv(d, t, twi, zr);
         stage_BC<8, true>(d, twi, zr);
         stage_BC<7, true>(d, twi, zr);
@@ -448,6 +478,10 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
     }
     __syncthreads();
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kTmemCols) : "memory");
 }
 
 // ================================================================================ K3 key switch

@@ -9,10 +9,10 @@
 
 namespace vlp {
 
-// ---- blind rotation (K2): 4 bootstraps per CTA in lock-step, 128 threads each, 8 coefficients per
-// thread per polynomial
+// ---- blind rotation (K2): 5 bootstraps per CTA, 128 threads each, 8 coefficients per thread per
+// polynomial
 constexpr int kBT = 128;                            // threads per bootstrap
-constexpr int kBrBoot = 4;                          // bootstraps per CTA
+constexpr int kBrBoot = 5;                          // bootstraps per CTA
 constexpr int kBrThreads = kBT * kBrBoot;           // 512
 constexpr int kChunks = 4;                          // bsk chunks per CMux step: slot pairs (positions)
 constexpr int kChunkWords = 76;                     // words per thread per chunk: [o 6][e 2][q 6] + 4 pad
@@ -21,7 +21,13 @@ constexpr int kSlots = 3;                           // smem ring of bsk chunks
 constexpr int kTwSlots = 18;                        // lane-varying twiddle slots (stages 3..9)
 constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 24,514,560
 constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
-                             kBrBoot * 640 * 2 + kSlots * 8 + kSlots * 4;
+                             kBrBoot * 640 * 2 + kSlots * 8 + kSlots * 4 + 8;
+// TMEM (tcgen05.ld/st, no MMA) as per-thread spill space: per warp slot 96 columns -- MAC outputs of
+// component u at columns 32u + 8l + s, round-0 transformed digits at 64 + 8j + s.
+constexpr int kTmemCols = 512;
+constexpr int kTmemSlotCols = 96;
+static_assert(kBrBoot * kTmemSlotCols <= kTmemCols, "TMEM columns");
+static_assert(kBrSmemBytes <= 232448, "shared memory per CTA");
 
 // ---- key switch (K3)
 constexpr int kKsCt = 16;                                 // ciphertexts per CTA
