@@ -47,18 +47,22 @@ __device__ __forceinline__ uint32_t shoup(uint32_t y, uint32_t w, uint32_t ws) {
 // keeps ptxas from turning the add into IMAD.IADD on the heavy FMA pipe -- the binding unit of the blind
 // rotation.
 __device__ __forceinline__ uint32_t add_alu(uint32_t a, uint32_t b, uint32_t zero) { return a + b + zero; }
+// Runtime constants (BrArgs::zero = 0, BrArgs::p2 = 2p): three-register adds cannot become IMAD.IADD.
+struct Rc {
+  uint32_t z, p2;
+};
 // Forward CT butterfly, inputs / outputs in [0, 4p).
-__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, uint32_t z = 0) {
+__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, Rc z) {
   const uint32_t xr = umin(x, x - P2);
   const uint32_t t = shoup(y, w, ws);
-  x = add_alu(xr, t, z);
-  y = xr - t + P2;
+  x = add_alu(xr, t, z.z);
+  y = xr - t + z.p2;
 }
 // Inverse GS butterfly, inputs / outputs in [0, 2p).
-__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, uint32_t z = 0) {
-  uint32_t s = add_alu(x, y, z);
+__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, Rc z) {
+  uint32_t s = add_alu(x, y, z.z);
   s = umin(s, s - P2);
-  const uint32_t d = x - y + P2;
+  const uint32_t d = x - y + z.p2;
   x = s;
   y = shoup(d, w, ws);
 }
@@ -156,7 +160,7 @@ typedef uint32_t Poly3[3][8];
 
 // Stages 0-2 (layout A): pair (r, r | rb), rb = 4 >> s; twiddle k = 2^s + (r >> (3 - s)), uniform.
 template <int S, bool INV>
-__device__ __forceinline__ void stage_A(Poly3& d, uint32_t z) {
+__device__ __forceinline__ void stage_A(Poly3& d, Rc z) {
   constexpr int rb = 4 >> S;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
@@ -173,7 +177,7 @@ __device__ __forceinline__ void stage_A(Poly3& d, uint32_t z) {
 // Lane-varying stages 3-8: layout B (S = 3..5) or C (S = 6..8); rb = 4 >> (S % 3); twiddle slot
 // q = r >> (3 - S % 3) at table row kSlotBase[S] + q, column t.
 template <int S, bool INV>
-__device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl, uint32_t z) {
+__device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl, Rc z) {
   constexpr int rb = 4 >> (S % 3);
   constexpr int base = S == 3 ? 0 : S == 4 ? 1 : S == 5 ? 3 : S == 6 ? 7 : S == 7 ? 8 : 10;
 #pragma unroll
@@ -190,7 +194,7 @@ __device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl
 
 // Stage 9 forward: lane-pair exchange (lower lane keeps pairs r = 0..3, upper lane r = 4..7), then
 // butterflies on (d[i], d[4+i]) with twiddle slots 14..17.
-__device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __restrict__ twl, uint32_t z) {
+__device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __restrict__ twl, Rc z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
@@ -209,7 +213,7 @@ __device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __
 }
 
 // Stage 9 inverse: butterflies on (d[i], d[4+i]), then the reverse lane-pair exchange (back to layout C).
-__device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __restrict__ twl, uint32_t z) {
+__device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __restrict__ twl, Rc z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
@@ -267,12 +271,12 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
   uint16_t* abar = abar_all + g * 640;
   const uint2* twf = a.twl_fwd + t;
   const uint2* twi = a.twl_inv + t;
-  const uint32_t zr = a.zero;
+  const Rc zr{a.zero, a.p2};
 
   const uint32_t ngroups = (a.njobs + kBrBoot - 1) / kBrBoot;
   if (blockIdx.x >= ngroups) return;
   const uint32_t my_groups = (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const uint64_t total_chunks = static_cast<uint64_t>(my_groups) * a.steps * kChunks;
+  const uint32_t total_chunks = my_groups * static_cast<uint32_t>(a.steps) * kChunks;  // < 2^32 (api.cu limits)
 
   if (tid == 0) {
     for (int s = 0; s < kSlots; s++) {
@@ -294,15 +298,15 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
   const uint32_t warp = tid >> 5;
   const uint32_t tm = *tmem_base_sh + ((32u * (warp & 3u)) << 16) + (warp >> 2) * kTmemSlotCols;
   // chunk sequence n -> (step (n / 8) % steps, chunk n % 8) of the bsk; ring slot n % kSlots
-  auto issue = [&](uint64_t nseq) {
-    const uint32_t step = static_cast<uint32_t>((nseq / kChunks) % a.steps), c = nseq % kChunks;
+  auto issue = [&](uint32_t nseq) {
+    const uint32_t step = (nseq / kChunks) % static_cast<uint32_t>(a.steps), c = nseq % kChunks;
     const uint32_t s = nseq % kSlots;
     bulk_load(ring + s * kBT * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * kBT * kChunkWords,
               kChunkBytes, &mbar[s]);
   };
   if (tid == 0)
-    for (uint64_t q = 0; q < kSlots && q < total_chunks; q++) issue(q);
-  uint64_t nseq = 0;
+    for (uint32_t q = 0; q < kSlots && q < total_chunks; q++) issue(q);
+  uint32_t nseq = 0, sl = 0, ph = 0;  // chunk sequence number, its ring slot (nseq % kSlots) and phase parity
 
   for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const uint32_t jb = grp * kBrBoot + g;
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
           const uint32_t j = t + 128u * r;
           const uint32_t kk = (j - ab) & (2 * N - 1);
           uint32_t v = acc[u * N + (kk & (N - 1))];
-          v = kk >= static_cast<uint32_t>(N) ? 0u - v : v;
+          v = kk >= static_cast<uint32_t>(N) ? zr.z - v : v;
           const uint32_t w = v - acc[u * N + j] + 0x81020400u;
           d[0][r] = ((w >> 25) & 127u) + (P - 64u);
           d[1][r] = ((w >> 18) & 127u) + (P - 64u);
@@ -377,8 +381,7 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
         // N^-1 * 2^32).  T < 6p^2 and T + m p < 2^64; output < 2.5p.
 #pragma unroll
         for (int pp = 0; pp < kChunks; pp++) {
-          const uint32_t sl = nseq % kSlots;
-          mbar_wait(&mbar[sl], static_cast<uint32_t>((nseq / kSlots) & 1));
+          mbar_wait(&mbar[sl], ph);
           const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
           uint32_t x[2][6];  // the 6 transformed digit polynomials at positions 2pp + e, reduced to [0, p)
 #pragma unroll
@@ -423,6 +426,10 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
             }
           }
           nseq++;
+          if (++sl == kSlots) {
+            sl = 0;
+            ph ^= 1u;
+          }
         }
       }
       tmem_wait_st();
@@ -451,15 +458,17 @@ __global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const B
         // centered lift of the three limbs, recombine mod 2^32, acc_u += (layout A: j = t + 128 r)
 #pragma unroll
         for (int r = 0; r < 8; r++) {
-          uint32_t sum = 0;
+          uint32_t sv[3];
 #pragma unroll
           for (int l = 0; l < 3; l++) {
             uint32_t v = d[l][r];
-            v = umin(v, v - P);                            // [0, p)
-            const uint32_t sv = v > (P >> 1) ? v - P : v;  // centered, two's complement
-            sum += sv << (11 * l);
+            v = umin(v, v - P);                    // [0, p)
+            sv[l] = v > (P >> 1) ? v - P : v;      // centered, two's complement
           }
-          acc[u * N + t + 128u * r] += sum;
+          // sv0 + 2^11 sv1 + 2^22 sv2 + acc (funnel shifts and three-input adds stay on the ALU pipe)
+          const uint32_t hi = __funnelshift_l(0u, sv[1], 11) + __funnelshift_l(0u, sv[2], 22) + zr.z;
+          uint32_t& av = acc[u * N + t + 128u * r];
+          av = add_alu(av, sv[0], hi);
         }
       }
       bar_boot(g);
@@ -672,7 +681,14 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int grid, cudaStream_t st) {
     attr = true;
   }
   if (a.njobs == 0) return cudaSuccess;
-  vlp_blind_rotate_kernel<<<grid, kBrThreads, kBrSmemBytes, st>>>(a);
+  // the kernel counts bsk chunks in 32 bits: (groups per CTA) x steps x kChunks must stay below 2^32
+  const uint64_t groups = (a.njobs + kBrBoot - 1) / kBrBoot;
+  if (grid <= 0 || (groups + grid - 1) / grid * static_cast<uint64_t>(a.steps) * kChunks >= (1ull << 32))
+    return cudaErrorInvalidValue;
+  BrArgs b = a;
+  b.zero = 0;
+  b.p2 = P2;
+  vlp_blind_rotate_kernel<<<grid, kBrThreads, kBrSmemBytes, st>>>(b);
   return cudaGetLastError();
 }
 

@@ -50,6 +50,7 @@ struct BrArgs {
   const uint2* twl_fwd;  // [kTwSlots][kBT] (w, floor(w 2^32 / p)) in thread order
   const uint2* twl_inv;
   uint32_t zero;  // always 0 (a runtime zero; see add_alu in kernels.cu)
+  uint32_t p2;    // always 2p, set by launch_blind_rotate (a runtime constant; see ct_bfly in kernels.cu)
 };
 
 struct KsArgs {
