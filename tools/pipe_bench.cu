@@ -9,6 +9,7 @@
 #include <cstdio>
 
 #define CH 8
+__device__ __forceinline__ uint32_t umin_(uint32_t a, uint32_t b) { return a < b ? a : b; }
 
 template <int MODE>
 __global__ void __launch_bounds__(512) kern(uint32_t* out, uint32_t iters, uint32_t seed) {
@@ -60,6 +61,28 @@ __global__ void __launch_bounds__(512) kern(uint32_t* out, uint32_t iters, uint3
         if (MODE == 14) {  // IMAD.WIDE.U32 with 64-bit addend, multiplier refreshed by an IADD3
           a[c] += m;
           asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"(a[c]), "r"(k));
+        }
+        if (MODE == 15) {  // IMAD.WIDE.U32 with a 64-bit register addend, multiplier = low word of the chain
+          asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"((uint32_t)w[c]), "r"(k));
+        }
+        if (MODE == 16) {  // IMAD.WIDE.U32 with RZ addend + LOP3 to refresh the multiplier
+          asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w[c]) : "r"((uint32_t)w[c] ^ (uint32_t)(w[c] >> 32)), "r"(k));
+        }
+        if (MODE == 17) {  // IMAD.WIDE.U32 acc + LOP3 (same ALU op as mode 16, for a fair comparison)
+          asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"((uint32_t)w[c] ^ (uint32_t)(w[c] >> 32)), "r"(k));
+        }
+        if (MODE == 18) a[c] = umin_(a[c], a[c] - m);  // VIADDMNMX
+        if (MODE == 19) {  // VIADDMNMX + IMAD
+          a[c] = umin_(a[c], a[c] - m);
+          asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(*reinterpret_cast<uint32_t*>(&f[c])) : "r"(k), "r"(m));
+        }
+        if (MODE == 20) {  // VIADDMNMX + IADD3
+          a[c] = umin_(a[c], a[c] - m);
+          asm volatile("add.u32 %0, %0, %1;" : "+r"(*reinterpret_cast<uint32_t*>(&f[c])) : "r"(m));
+        }
+        if (MODE == 21) {  // VIADDMNMX + IMAD.HI
+          a[c] = umin_(a[c], a[c] - m);
+          asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(*reinterpret_cast<uint32_t*>(&f[c])) : "r"(k));
         }
         if (MODE == 13) {  // IMAD + FFMA
           asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[c]) : "r"(k), "r"(m));
@@ -113,6 +136,13 @@ int main() {
   run<8>("IMAD+IADD3 (2 instr)", 2, out, mhz);
   run<12>("DFMA+IADD3 (2 instr)", 2, out, mhz);
   run<13>("IMAD+FFMA (2 instr)", 2, out, mhz);
+  run<15>("IMAD.WIDE.U32 acc64 chain", 1, out, mhz);
+  run<16>("IMAD.WIDE.U32 RZ-addend + LOP3 (2 instr)", 2, out, mhz);
+  run<17>("IMAD.WIDE.U32 acc64 + LOP3 (2 instr)", 2, out, mhz);
+  run<18>("VIADDMNMX", 1, out, mhz);
+  run<19>("VIADDMNMX+IMAD (2 instr)", 2, out, mhz);
+  run<20>("VIADDMNMX+IADD3 (2 instr)", 2, out, mhz);
+  run<21>("VIADDMNMX+IMAD.HI (2 instr)", 2, out, mhz);
   run<14>("IMAD.WIDE.U32 acc64 + IADD3 (2 instr)", 2, out, mhz);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
