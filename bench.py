@@ -32,6 +32,11 @@ from synth.workloads import expected_result  # noqa: E402
 METRIC = "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
 UNIT = "gate bootstraps/s"
 CONFIG_BR = {1: 252, 2: 132080, 3: 1060832, 4: 6750176}
+# dram__bytes_read.sum + dram__bytes_write.sum of one vlp_blind_rotate_kernel launch from `ncu --set full`
+# (profiles/r1_br_v5_ncu_summary.txt: a one-wave launch of 740 bootstraps, i.e. one bsk pass per CTA; the bsk
+# itself is L2-resident, so DRAM sees about one 92.9 MB bsk read per launch plus the ciphertexts)
+TRAFFIC_BYTES_PER_LAUNCH = (102.109952 + 5.181696) * 1e6
+TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_kernel, 740-bootstrap launch (profiles/r1_br_v5_ncu_summary.txt)"
 
 
 def ops_per_br():
@@ -128,24 +133,37 @@ def cpu_baseline_oracle(seconds_target=5.0, nand_gates=None):
 
 
 def run_reference(args, rank, world):
+    """The base contract's reference arm for this paper-only task: the CPU oracle, as it stands, on the
+    box's host cores; each step a bounded sample (2 x cores NAND gate bootstraps, the same BR + extract + KS
+    the GPU path runs) of the same workload; the metric is the same gate bootstraps/s (records/s is
+    extrapolated with the config's BR count).  Rank 0 only."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    wl_br = CONFIG_BR[args.config]
-    wl = make_workload(args.config) if args.config != 4 else None
-    per_step = []
+    wl_br = CONFIG_BR.get(args.config)
+    wl = make_workload(args.config) if args.config in (1, 2, 3) else None
+    per_step, t_steps = [], []
     for s in range(args.warmup + args.steps):
+        t0 = time.time()
         cb = cpu_baseline_oracle(nand_gates=cores * 2)
         if s >= args.warmup:
             per_step.append(cb["value"])
+            t_steps.append(time.time() - t0)
     v = statistics.median(per_step)
     M = wl.M if wl else 65536
+    if wl is not None:
+        config = {"workload": f"cfg{args.config}_{wl.name}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S, "d": wl.d,
+                  "br_per_query": wl_br, "parallelism": "CPU oracle, rank 0",
+                  "params": "TFHE n=630 N=1024 Bg=2^7 l=3 ks 2^2x8 (tab:tfhe_params)"}
+    else:
+        config = {"workload": f"cfg{args.config}", "parallelism": "CPU oracle, rank 0"}
+    config["sample"] = ("each step: 2 x cores NAND gate bootstraps on the CPU oracle (the same BR + extract + KS "
+                        "as the GPU path); records/s extrapolated with the config's BR count")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "records_per_s": v / (wl_br / M),
-            "config": {"workload": f"cfg{args.config}", "note": "each step: 2 x cores NAND bootstraps on the CPU oracle; "
-                       "BR/s of the same gate bootstrap as the GPU path; records/s extrapolated by the config's BR count"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(t_steps),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "records_per_s": v / (wl_br / M) if wl_br else None,
+            "config": config,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} steps x {2 * cores} NAND gate bootstraps"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -363,7 +381,8 @@ def main():
                          "peak_source": peak_how, "ops_per_br": ops_per_br(),
                          "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
                          "br_share_of_step": br_ms / args.steps / ms_per_step,
-                         "br_launch_avg_ms": br_launch_ms, "traffic": None},
+                         "br_launch_avg_ms": br_launch_ms, "traffic": TRAFFIC_BYTES_PER_LAUNCH,
+                         "traffic_source": TRAFFIC_SOURCE},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
