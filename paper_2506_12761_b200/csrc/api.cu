@@ -160,7 +160,8 @@ int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
   p->launches = 1 + (p->copy_slots.empty() ? 0 : 1);
   for (auto& L : s.levels) {
     const uint32_t tiles = static_cast<uint32_t>((L.ks.size() + kKsCt - 1) / kKsCt);
-    p->launches += (L.br.empty() ? 0 : 1) + (L.ks.empty() ? 0 : (tiles < 4 * 148 ? 2 : 1));
+    p->launches += br_launch_count(static_cast<uint32_t>(L.br.size()), server->sm_count) +
+                   (L.ks.empty() ? 0 : (tiles < 4 * 148 ? 2 : 1));
   }
   return VLP_OK;
 }
@@ -326,7 +327,7 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
     ba.twl_inv = s->twl_inv;
     if (ba.njobs) {
       p->begin(0, st);
-      if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
+      if ((e = launch_blind_rotate(ba, s->sm_count, st))) return cuda_fail(e, "blind rotate");
       p->end(0, st);
     }
     KsArgs ka{};
@@ -399,7 +400,7 @@ int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, 
   ba.bsk = s->bsk_ntt;
   ba.twl_fwd = s->twl_fwd;
   ba.twl_inv = s->twl_inv;
-  if ((e = launch_blind_rotate(ba, br_grid(ba.njobs, s->sm_count), st))) return cuda_fail(e, "blind rotate");
+  if ((e = launch_blind_rotate(ba, s->sm_count, st))) return cuda_fail(e, "blind rotate");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
   return VLP_OK;
 }

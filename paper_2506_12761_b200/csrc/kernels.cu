@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -255,7 +256,9 @@ __device__ __forceinline__ void exchange(Poly3& d, uint32_t* xb, uint32_t t, uin
 // key limbs -> inverse NTT -> centered lift -> recombine mod 2^32 -> acc_u += ...).  The round loops are
 // not unrolled: each round body is ~25 KB of SASS (the instruction cache, not the ALUs, limited the fully
 // unrolled form; profiles/).
-__global__ void __launch_bounds__(kBrThreads, 1) vlp_blind_rotate_kernel(const BrArgs a) {
+template <int B>  // bootstraps per CTA (5 = throughput mode; 1-4 for the narrow tail of a level)
+__global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrArgs a) {
+  constexpr int kBrBoot = B, kBrThreads = B * kBT, kTmemCols = tmem_cols(B);
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* ring = reinterpret_cast<uint32_t*>(smem);
   uint32_t* acc_all = ring + kSlots * kBT * kChunkWords;
@@ -667,29 +670,78 @@ void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd,
   vlp_bsk_convert_kernel<<<n * kRows * 2, 512, 0, st>>>(raw, out, tw_fwd, c_mont);
 }
 
-int br_grid(uint32_t njobs, int sm_count) {
-  const uint32_t groups = (njobs + kBrBoot - 1) / kBrBoot;
-  return static_cast<int>(groups < static_cast<uint32_t>(sm_count) ? groups : sm_count);
-}
-
-cudaError_t launch_blind_rotate(const BrArgs& a, int grid, cudaStream_t st) {
+template <int B>
+static cudaError_t launch_br_b(const BrArgs& a, int sm_count, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(vlp_blind_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kBrSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(vlp_blind_rotate_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         br_smem_bytes(B));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   if (a.njobs == 0) return cudaSuccess;
+  const uint64_t groups = (a.njobs + B - 1) / B;
+  const int grid = static_cast<int>(groups < static_cast<uint64_t>(sm_count) ? groups : sm_count);
   // the kernel counts bsk chunks in 32 bits: (groups per CTA) x steps x kChunks must stay below 2^32
-  const uint64_t groups = (a.njobs + kBrBoot - 1) / kBrBoot;
   if (grid <= 0 || (groups + grid - 1) / grid * static_cast<uint64_t>(a.steps) * kChunks >= (1ull << 32))
     return cudaErrorInvalidValue;
   BrArgs b = a;
   b.zero = 0;
   b.p2 = P2;
-  vlp_blind_rotate_kernel<<<grid, kBrThreads, kBrSmemBytes, st>>>(b);
+  vlp_blind_rotate_kernel<B><<<grid, B * kBT, br_smem_bytes(B), st>>>(b);
   return cudaGetLastError();
+}
+
+static cudaError_t launch_br_width(const BrArgs& a, int B, int sm_count, cudaStream_t st) {
+  switch (B) {
+    case 1: return launch_br_b<1>(a, sm_count, st);
+    case 2: return launch_br_b<2>(a, sm_count, st);
+    case 3: return launch_br_b<3>(a, sm_count, st);
+    case 4: return launch_br_b<4>(a, sm_count, st);
+    default: return launch_br_b<kBrBoot>(a, sm_count, st);
+  }
+}
+
+// One level of blind rotations: whole waves of kBrBoot bootstraps per SM, then the remainder (fewer than
+// kBrBoot x sm_count jobs) as one wave of the smallest CTA size that holds it -- a CTA runs all its
+// bootstrap slots, so a narrow tail on 5-slot CTAs would cost a full-width wave.  VLP_BR_BOOT=b (debug)
+// forces b bootstraps per CTA for the whole level.
+static int forced_boot() {
+  static const int f = [] {
+    const char* e = getenv("VLP_BR_BOOT");
+    return e ? atoi(e) : 0;
+  }();
+  return f;
+}
+
+int br_launch_count(uint32_t njobs, int sm_count) {
+  if (njobs == 0) return 0;
+  if (forced_boot() >= 1 && forced_boot() <= kBrBoot) return 1;
+  const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
+  return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
+}
+
+cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) {
+  if (a.njobs == 0) return cudaSuccess;
+  const int forced = forced_boot();
+  if (forced >= 1 && forced <= kBrBoot) return launch_br_width(a, forced, sm_count, st);
+  const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
+  const uint32_t full = a.njobs / wave * wave, tail = a.njobs - full;
+  cudaError_t e = cudaSuccess;
+  if (full) {
+    BrArgs f = a;
+    f.njobs = full;
+    if ((e = launch_br_width(f, kBrBoot, sm_count, st)) != cudaSuccess) return e;
+  }
+  if (tail) {
+    BrArgs r = a;
+    r.jobs = a.jobs + full;
+    r.njobs = tail;
+    if (r.raw_acc) r.raw_acc = a.raw_acc + static_cast<size_t>(full) * 2 * N;
+    const int b = static_cast<int>((tail + sm_count - 1) / sm_count);
+    e = launch_br_width(r, b, sm_count, st);
+  }
+  return e;
 }
 
 cudaError_t launch_keyswitch(const KsArgs& a0, cudaStream_t st) {

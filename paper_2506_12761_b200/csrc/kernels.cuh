@@ -20,13 +20,17 @@ constexpr int kChunkBytes = kBT * kChunkWords * 4;  // 38912
 constexpr int kSlots = 3;                           // smem ring of bsk chunks
 constexpr int kTwSlots = 18;                        // lane-varying twiddle slots (stages 3..9)
 constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkWords;  // 24,514,560
-constexpr int kBrSmemBytes = kSlots * kChunkBytes + kBrBoot * 2 * N * 4 + kBrBoot * 3 * N * 4 +
-                             kBrBoot * 640 * 2 + kSlots * 8 + kSlots * 4 + 8;
+// shared memory of a blind-rotate CTA with B bootstraps: bsk ring + per bootstrap (accumulator, exchange
+// buffer, mod-switched mask) + mbarriers, release counters, TMEM base
+__host__ __device__ constexpr int br_smem_bytes(int B) {
+  return kSlots * kChunkBytes + B * (2 * N * 4 + 3 * N * 4 + 640 * 2) + kSlots * 8 + kSlots * 4 + 8;
+}
+constexpr int kBrSmemBytes = br_smem_bytes(kBrBoot);
 // TMEM (tcgen05.ld/st, no MMA) as per-thread spill space: per warp slot 96 columns -- MAC outputs of
 // component u at columns 32u + 8l + s, round-0 transformed digits at 64 + 8j + s.
-constexpr int kTmemCols = 512;
 constexpr int kTmemSlotCols = 96;
-static_assert(kBrBoot * kTmemSlotCols <= kTmemCols, "TMEM columns");
+__host__ __device__ constexpr int tmem_cols(int B) { return B * kTmemSlotCols <= 128 ? 128 : (B * kTmemSlotCols <= 256 ? 256 : 512); }
+static_assert(kBrBoot * kTmemSlotCols <= 512, "TMEM columns");
 static_assert(kBrSmemBytes <= 232448, "shared memory per CTA");
 
 // ---- key switch (K3)
@@ -65,10 +69,11 @@ struct KsArgs {
 void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd, uint32_t c_mont,
                         cudaStream_t st);
 void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
-cudaError_t launch_blind_rotate(const BrArgs& a, int grid, cudaStream_t st);
+// one level: whole waves of kBrBoot bootstraps per CTA + a narrower tail wave (1 or 2 kernel launches)
+cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st);
+int br_launch_count(uint32_t njobs, int sm_count);
 cudaError_t launch_keyswitch(const KsArgs& a, cudaStream_t st);
 cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st);
 cudaError_t launch_copy_rows(const uint32_t* slots, uint32_t count, Regions reg, uint32_t* out, cudaStream_t st);
-int br_grid(uint32_t njobs, int sm_count);
 
 }  // namespace vlp
