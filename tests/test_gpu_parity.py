@@ -1,7 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
 
 Bit-exact everywhere (all arithmetic is integer: torus32 and the NTT primes).  Sizes span several CTAs
-(4 bootstraps each) with ragged tails; full-size configs are checked on sampled outputs the oracle
+(5 bootstraps each in whole waves, 1-4 in the narrower tail wave of a level) with ragged tails; full-size configs are checked on sampled outputs the oracle
 recomputes one by one plus properties that hold at any size (decrypted predicate, all-trivial closed
 form P11)."""
 import os
@@ -53,6 +53,23 @@ def test_blind_rotate_steps_bit_exact(server, okeys):
         want = list(POOL.map(lambda c: okeys.blind_rotate(c[:631], steps), cts))
         for i in range(len(cts)):
             assert np.array_equal(got[i], want[i]), (steps, i, np.flatnonzero(got[i] != want[i])[:8])
+
+
+@pytest.mark.parametrize("tail", [1, 150, 300, 600])
+def test_blind_rotate_wave_split_bit_exact(server, okeys, tail):
+    """A level of 5 x 148 + tail blind rotations runs as one whole wave (5 bootstraps per CTA) plus a tail
+    wave of ceil(tail / 148) bootstraps per CTA (kernels.cu launch_blind_rotate): 2 CMux steps, sampled
+    rows on both sides of the split and the ragged end byte-equal to the oracle."""
+    count = 740 + tail
+    rng = np.random.default_rng(tail)
+    cts = rand_tlwe(rng, count)
+    cts[:, 631] = 0
+    got = A.to_host(server.debug_blind_rotate(A.to_device(cts), 2))
+    idx = sorted(set([i for i in (0, 4, 5, 738, 739, 740, 741) if i < count] + [count - 2, count - 1] +
+                     random.Random(tail).sample(range(count), 8)))
+    want = list(POOL.map(lambda i: okeys.blind_rotate(cts[i, :631], 2), idx))
+    for i, w in zip(idx, want):
+        assert np.array_equal(got[i], w), (tail, i)
 
 
 def test_blind_rotate_full_bit_exact(server, okeys):
