@@ -220,17 +220,15 @@ def test_all_trivial_closed_form_full_size(server, cfg):
     assert [int(x) for x in out[:, 630]] == [0x20000000 if (want >> j) & 1 else 0xE0000000 for j in range(wl.l_S)]
 
 
-def test_config2_full_size_sampled(server):
-    """Config 2 at full size (1024 records, 132,080 BR): decrypted result == plain predicate; two sampled
-    records' validation bits and masked payloads are recomputed by the oracle (from the same seeded
-    inputs) and byte-equal."""
-    wl = make_workload(2, key_seed=SEED)
+def _full_size_sampled(server, cfg, sample):
+    """A config at full size: decrypted result == plain predicate; the sampled records' validation bits and
+    masked payloads are recomputed by the oracle (from the same seeded inputs) and byte-equal."""
+    wl = make_workload(cfg, key_seed=SEED)
     prog, q, db, out = _run_config(server, wl)
     want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
     assert server.keys.decrypt_value(out) == want
     okeys = O.OracleKeys(SEED)
     oq = OP.encrypt_query(okeys, wl.query, wl.l_I, 7)
-    sample = [3, wl.M - 1]
     mid = A.to_host(prog.intermediate())
 
     def one(i):
@@ -239,9 +237,29 @@ def test_config2_full_size_sampled(server):
         return OC.record_outputs(OC.TfheBackend(okeys), wl.mode, oq, r, p, wl.l_I, wl.d, wl.flags)
 
     for i, (v, masked) in zip(sample, POOL.map(one, sample)):
-        assert np.array_equal(mid[prog.node_row(0, i), :631], v)
+        assert np.array_equal(mid[prog.node_row(0, i), :631], v), ("v", i)
         for j in range(wl.l_S):
-            assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j])
+            assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j]), ("mask", i, j)
+    return wl, want
+
+
+def test_config2_full_size_sampled(server):
+    """Config 2 at full size (IntV 1D, 1024 records, 132,080 BR): predicate + records 3 and 1023 byte-equal."""
+    _full_size_sampled(server, 2, [3, 1023])
+
+
+def test_config3_full_size_sampled(server):
+    """Config 3 at full size (rectangle containment, 4096 records, 1,060,832 BR): predicate + records 0 and
+    4095 byte-equal."""
+    _full_size_sampled(server, 3, [0, 4095])
+
+
+def test_config4_full_size_sampled(server):
+    """Config 4 at full size (IdM, 65,536 records, 6,750,176 BR on one GPU): predicate + the matching record
+    (if the seed put the query id in the DB) and the last record byte-equal."""
+    wl = make_workload(4, key_seed=SEED)
+    hits = [i for i in range(wl.M) if int(wl.records[i][0]) == int(wl.query[0])]
+    _full_size_sampled(server, 4, (hits[:1] or [1]) + [wl.M - 1])
 
 
 def _full_parity_small(server, mode, d, l_I, l_S, flags, records, payloads, query, okeys_seed=SEED):
