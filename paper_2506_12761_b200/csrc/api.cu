@@ -160,7 +160,7 @@ int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
   p->launches = 1 + (p->copy_slots.empty() ? 0 : 1);
   for (auto& L : s.levels) {
     const uint32_t tiles = static_cast<uint32_t>((L.ks.size() + kKsCt - 1) / kKsCt);
-    p->launches += br_launch_count(static_cast<uint32_t>(L.br.size()), server->sm_count) +
+    p->launches += br_launch_count(static_cast<uint32_t>(L.br.size()), server ? server->sm_count : 148) +
                    (L.ks.empty() ? 0 : (tiles < 4 * 148 ? 2 : 1));
   }
   return VLP_OK;
