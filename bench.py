@@ -331,12 +331,26 @@ def main():
     value = br_per_query / (ms_per_step / 1e3)
     records_per_s = wl.M / (ms_per_step / 1e3)
 
-    # ---- e2e: query H2D from pinned host memory + eval + result D2H, every step (public API)
+    # ---- e2e: query H2D from pinned host memory + server_eval (+ combine) + result D2H, every step, through
+    # the problem-statement calls a user makes (vlp_server_eval / vlp_server_combine)
     e2e = None
     if not args.no_e2e:
         q_pin = torch.from_numpy(q_host.view(np.int32)).pin_memory()
         out_pin = torch.empty((wl.l_S, 632), dtype=torch.int32).pin_memory()
         qd = torch.empty_like(q)
+
+        def eval_api(qdev):
+            srv.eval(m, qdev, db, part if world > 1 else out, first=first, count=shard, stream=stream)
+            return part if world > 1 else out
+
+        def combine_api(roots):
+            srv.combine(m, world, roots, out, stream=stream)
+            return out
+
+        def step(qdev):  # noqa: F811 -- the e2e step goes through the public calls
+            sharded_step(qdev, eval_api, combine_api, world, rank, gathered)
+
+        step(q)  # compile + bind the cached schedules outside the timed region
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

@@ -183,6 +183,39 @@ int vlp_debug_blind_rotate(vlp_server* server, const uint32_t* in_dev, size_t co
 int vlp_debug_keyswitch(vlp_server* server, const uint32_t* nlwe_dev, size_t count, uint32_t* out_dev,
                         void* scratch_dev, uint64_t stream);
 
+/* ---- The problem-statement calls (the north star's keygen / encrypt_query / server_eval /
+ * decrypt_result).  They wrap the program calls above: the schedule for a (meta, first, count) shard, a
+ * gate batch or a combine is compiled on first use and cached in the server (thread-safe); device buffers
+ * stay caller-owned. */
+
+/* Sizes of the caller-owned device buffers for vlp_server_eval on a shard of `count` records:
+ * evaluation key (vlp_server_evk_bytes), encrypted DB rows (count * per_record * 632 * 4) and scratch
+ * (job arrays, intermediates, N-LWE staging).  Host only (compiles the schedule). */
+int vlp_server_workspace_bytes(const vlp_meta* meta, size_t count, size_t* evk_bytes, size_t* db_bytes,
+                               size_t* scratch_bytes);
+/* server_eval (alg:VeLoPIR P:307-329): evaluate the encrypted query (query_dev, vlp_encrypt_query
+ * layout) against records [first, first+count) of the encrypted DB (db_dev, record `first` at row 0),
+ * writing the shard's l_S aggregate ciphertexts to out_dev.  Asynchronous on `stream`. */
+int vlp_server_eval(vlp_server* server, const vlp_meta* meta, size_t first, size_t count,
+                    const uint32_t* query_dev, const uint32_t* db_dev, uint32_t* out_dev, void* scratch_dev,
+                    size_t scratch_bytes, uint64_t stream);
+/* Scratch bytes of vlp_server_combine for G shard roots. */
+int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t* scratch_bytes);
+/* The top log2(G) XOR-tree levels over the G shard roots partials_dev [G][l_S][632] (rank order, G a power
+ * of two): the query's l_S result ciphertexts to out_dev (R15). */
+int vlp_server_combine(vlp_server* server, const vlp_meta* meta, uint32_t G, const uint32_t* partials_dev,
+                       uint32_t* out_dev, void* scratch_dev, size_t scratch_bytes, uint64_t stream);
+/* Scratch bytes of vlp_gate_batch (includes room to stage b and c contiguously for VLP_MUX). */
+int vlp_gate_batch_workspace_bytes(int op, size_t count, size_t* scratch_bytes);
+/* A batch of `count` independent gates (BASELINE config 5): out[i] = op(a[i], b[i]), or for VLP_MUX
+ * out[i] = MUX(a[i], b[i], c[i]) = a ? b : c (R10).  c_dev is ignored unless op == VLP_MUX. */
+int vlp_gate_batch(vlp_server* server, int op, const uint32_t* a_dev, const uint32_t* b_dev,
+                   const uint32_t* c_dev, uint32_t* out_dev, size_t count, void* scratch_dev,
+                   size_t scratch_bytes, uint64_t stream);
+/* decrypt_result: bit j = [int32(phase of ct[j]) > 0] (R18), LSB first (R20); *value_out (may
+ * be NULL) = sum bit_j 2^j for l_S <= 64. */
+int vlp_decrypt_result(const vlp_sk* sk, const uint32_t* ct, uint32_t l_S, uint8_t* bits_out, uint64_t* value_out);
+
 void vlp_free_sk(vlp_sk* sk);
 void vlp_free_evk(vlp_evk* evk);
 void vlp_free_pk(vlp_pk* pk);

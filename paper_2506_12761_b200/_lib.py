@@ -72,6 +72,15 @@ SIGNATURES = {
     "vlp_debug_scratch_bytes": (_sz, [_sz]),
     "vlp_debug_blind_rotate": (_i, [_vp, _vp, _sz, _i, _vp, _vp, _u64]),
     "vlp_debug_keyswitch": (_i, [_vp, _vp, _sz, _vp, _vp, _u64]),
+    "vlp_server_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t),
+                                        ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_server_eval": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _vp, _vp, _vp, _vp, _sz, _u64]),
+    "vlp_server_combine_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), ctypes.c_uint32,
+                                                ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_server_combine": (_i, [_vp, ctypes.POINTER(VlpMeta), ctypes.c_uint32, _vp, _vp, _vp, _sz, _u64]),
+    "vlp_gate_batch_workspace_bytes": (_i, [_i, _sz, ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_gate_batch": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _sz, _vp, _sz, _u64]),
+    "vlp_decrypt_result": (_i, [_vp, _u32p, ctypes.c_uint32, _u8p, _u64p]),
     "vlp_free_sk": (None, [_vp]),
     "vlp_free_evk": (None, [_vp]),
     "vlp_free_pk": (None, [_vp]),

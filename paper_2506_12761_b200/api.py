@@ -78,6 +78,16 @@ class Keys:
         check(lib().vlp_decrypt_bits(self.sk, _u32p(ct), ct.shape[0], out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
         return out
 
+    def decrypt_result(self, ct: np.ndarray, l_S: int | None = None):
+        """decrypt_result: (bits LSB first, value) of the l_S result ciphertexts."""
+        ct = np.ascontiguousarray(ct, dtype=np.uint32)
+        l_S = ct.shape[0] if l_S is None else l_S
+        bits = np.zeros(l_S, np.uint8)
+        v = ctypes.c_uint64()
+        check(lib().vlp_decrypt_result(self.sk, _u32p(ct), l_S, bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                       ctypes.byref(v) if l_S <= 64 else None))
+        return bits, v.value
+
     def decrypt_value(self, ct: np.ndarray) -> int:
         return int(sum(int(b) << j for j, b in enumerate(self.decrypt_bits(ct))))
 
@@ -123,6 +133,54 @@ class Server:
             lib().vlp_free_server(self.h)
         except Exception:
             pass
+
+    # ---- the problem-statement calls (vlp_server_eval / vlp_server_combine / vlp_gate_batch): schedules are
+    # compiled and cached inside the library; the scratch buffers are torch tensors owned here
+    def _scratch(self, key, nbytes):
+        import torch
+        cache = self.__dict__.setdefault("_scratch_cache", {})
+        t = cache.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(256, nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
+            cache[key] = t
+        return t
+
+    def eval(self, m: VlpMeta, query_dev, db_dev, out_dev, first: int = 0, count: int | None = None, stream=None):
+        """server_eval: the shard [first, first+count)'s l_S aggregate ciphertexts into out_dev."""
+        count = m.M - first if count is None else count
+        key = ("eval", bytes(m), first, count)
+        if key not in self.__dict__.setdefault("_ws", {}):
+            sb = ctypes.c_size_t()
+            check(lib().vlp_server_workspace_bytes(ctypes.byref(m), count, None, None, ctypes.byref(sb)))
+            self._ws[key] = sb.value
+        sc = self._scratch(key, self._ws[key])
+        check(lib().vlp_server_eval(self.h, ctypes.byref(m), first, count, ctypes.c_void_p(query_dev.data_ptr()),
+                                    ctypes.c_void_p(db_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
+                                    ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream)))
+
+    def combine(self, m: VlpMeta, G: int, partials_dev, out_dev, stream=None):
+        key = ("combine", bytes(m), G)
+        if key not in self.__dict__.setdefault("_ws", {}):
+            sb = ctypes.c_size_t()
+            check(lib().vlp_server_combine_workspace_bytes(ctypes.byref(m), G, ctypes.byref(sb)))
+            self._ws[key] = sb.value
+        sc = self._scratch(key, self._ws[key])
+        check(lib().vlp_server_combine(self.h, ctypes.byref(m), G, ctypes.c_void_p(partials_dev.data_ptr()),
+                                       ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(sc.data_ptr()),
+                                       sc.numel(), _stream_handle(stream)))
+
+    def gate_batch(self, op: int, a_dev, b_dev, out_dev, c_dev=None, stream=None):
+        """A batch of independent gates (config 5): out = op(a, b), or MUX(a, b, c) = a ? b : c."""
+        count = a_dev.shape[0]
+        key = ("gates", op, count)
+        if key not in self.__dict__.setdefault("_ws", {}):
+            sb = ctypes.c_size_t()
+            check(lib().vlp_gate_batch_workspace_bytes(op, count, ctypes.byref(sb)))
+            self._ws[key] = sb.value
+        sc = self._scratch(key, self._ws[key])
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        check(lib().vlp_gate_batch(self.h, op, p(a_dev), p(b_dev), p(c_dev), p(out_dev), count,
+                                   ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream)))
 
     def debug_blind_rotate(self, in_dev, steps: int, stream=None):
         import torch

@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -17,6 +20,9 @@ struct vlp_server {
   uint2* tw_fwd = nullptr;   // natural order (bsk conversion)
   uint2* twl_fwd = nullptr;  // thread-layout tables of the blind-rotate kernel
   uint2* twl_inv = nullptr;
+  // programs compiled by the problem-statement calls (vlp_server_eval, vlp_server_combine, vlp_gate_batch)
+  std::mutex mu;
+  std::map<std::string, std::unique_ptr<vlp_program>> cache;
 };
 
 struct vlp_program {
@@ -425,6 +431,107 @@ int vlp_debug_keyswitch(vlp_server* s, const uint32_t* nlwe_dev, size_t count, u
   if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
   return VLP_OK;
+}
+
+// ------------------------------------------------------------------------- problem-statement calls
+extern "C++" {
+static std::string meta_key(const char* kind, const vlp_meta& m, size_t a, size_t b) {
+  return std::string(kind) + ":" + std::to_string(m.mode) + "," + std::to_string(m.M) + "," +
+         std::to_string(m.l_I) + "," + std::to_string(m.l_S) + "," + std::to_string(m.d) + "," +
+         std::to_string(m.flags) + "," + std::to_string(a) + "," + std::to_string(b);
+}
+
+template <class Make>
+static int cached_program(vlp_server* s, const std::string& key, Make make, vlp_program** out) {
+  std::lock_guard<std::mutex> lock(s->mu);
+  auto it = s->cache.find(key);
+  if (it == s->cache.end()) {
+    vlp_program* p = nullptr;
+    if (int rc = make(&p)) return rc;
+    it = s->cache.emplace(key, std::unique_ptr<vlp_program>(p)).first;
+  }
+  *out = it->second.get();
+  return VLP_OK;
+}
+static size_t gate_stage_bytes(int op, size_t count) { return op == VLP_MUX ? 2 * count * kCt * 4 : 0; }
+}  // extern "C++"
+
+int vlp_server_workspace_bytes(const vlp_meta* meta, size_t count, size_t* evk_bytes, size_t* db_bytes,
+                               size_t* scratch_bytes) {
+  if (!meta) return fail(VLP_EINVAL, "null argument");
+  size_t per = 0;
+  if (int rc = vlp_db_record_cts(meta, &per)) return rc;
+  vlp_program* p = nullptr;
+  if (int rc = vlp_program_create(nullptr, meta, 0, count, &p)) return rc;
+  if (evk_bytes) *evk_bytes = kEvkBytes;
+  if (db_bytes) *db_bytes = count * per * kCt * 4;
+  if (scratch_bytes) *scratch_bytes = p->bytes;
+  delete p;
+  return VLP_OK;
+}
+
+int vlp_server_eval(vlp_server* s, const vlp_meta* meta, size_t first, size_t count, const uint32_t* query_dev,
+                    const uint32_t* db_dev, uint32_t* out_dev, void* scratch, size_t scratch_bytes,
+                    uint64_t stream) {
+  if (!s || !meta) return fail(VLP_EINVAL, "null argument");
+  vlp_program* p = nullptr;
+  if (int rc = cached_program(s, meta_key("eval", *meta, first, count),
+                              [&](vlp_program** o) { return vlp_program_create(s, meta, first, count, o); }, &p))
+    return rc;
+  return vlp_program_eval(p, scratch, scratch_bytes, query_dev, db_dev, out_dev, stream);
+}
+
+int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t* scratch_bytes) {
+  if (!meta || !scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  vlp_program* p = nullptr;
+  if (int rc = vlp_program_create_combine(nullptr, meta, G, &p)) return rc;
+  *scratch_bytes = p->bytes;
+  delete p;
+  return VLP_OK;
+}
+
+int vlp_server_combine(vlp_server* s, const vlp_meta* meta, uint32_t G, const uint32_t* partials_dev,
+                       uint32_t* out_dev, void* scratch, size_t scratch_bytes, uint64_t stream) {
+  if (!s || !meta) return fail(VLP_EINVAL, "null argument");
+  vlp_program* p = nullptr;
+  if (int rc = cached_program(s, meta_key("combine", *meta, G, 0),
+                              [&](vlp_program** o) { return vlp_program_create_combine(s, meta, G, o); }, &p))
+    return rc;
+  return vlp_program_eval(p, scratch, scratch_bytes, partials_dev, nullptr, out_dev, stream);
+}
+
+int vlp_gate_batch_workspace_bytes(int op, size_t count, size_t* scratch_bytes) {
+  if (!scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  vlp_program* p = nullptr;
+  if (int rc = vlp_program_create_gates(nullptr, op, count, &p)) return rc;
+  *scratch_bytes = align256(p->bytes) + gate_stage_bytes(op, count);
+  delete p;
+  return VLP_OK;
+}
+
+int vlp_gate_batch(vlp_server* s, int op, const uint32_t* a_dev, const uint32_t* b_dev, const uint32_t* c_dev,
+                   uint32_t* out_dev, size_t count, void* scratch, size_t scratch_bytes, uint64_t stream) {
+  if (!s || !scratch || (count && (!a_dev || !b_dev || !out_dev || (op == VLP_MUX && !c_dev))))
+    return fail(VLP_EINVAL, "null argument");
+  if (count == 0) return VLP_OK;
+  vlp_program* p = nullptr;
+  if (int rc = cached_program(s, "gates:" + std::to_string(op) + "," + std::to_string(count),
+                              [&](vlp_program** o) { return vlp_program_create_gates(s, op, count, o); }, &p))
+    return rc;
+  const size_t prog_bytes = align256(p->bytes);
+  if (scratch_bytes < prog_bytes + gate_stage_bytes(op, count)) return fail(VLP_ENOMEM, "scratch too small");
+  const uint32_t* in1 = b_dev;
+  if (op == VLP_MUX) {  // the program reads c right after b: stage both behind the program's scratch
+    uint32_t* st_bc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + prog_bytes);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+    if ((e = cudaMemcpyAsync(st_bc, b_dev, count * kCt * 4, cudaMemcpyDeviceToDevice, st)) ||
+        (e = cudaMemcpyAsync(st_bc + count * kCt, c_dev, count * kCt * 4, cudaMemcpyDeviceToDevice, st)))
+      return cuda_fail(e, "stage mux operands");
+    in1 = st_bc;
+  }
+  return vlp_program_eval(p, scratch, scratch_bytes, a_dev, in1, out_dev, stream);
 }
 
 void vlp_free_server(vlp_server* s) { delete s; }

@@ -202,6 +202,18 @@ int vlp_decrypt_bits(const vlp_sk* sk, const uint32_t* ct, size_t count, uint8_t
   return VLP_OK;
 }
 
+int vlp_decrypt_result(const vlp_sk* sk, const uint32_t* ct, uint32_t l_S, uint8_t* bits, uint64_t* value) {
+  if (!sk || (l_S && (!ct || !bits))) return fail(VLP_EINVAL, "null argument");
+  if (value && l_S > 64) return fail(VLP_EWIDTH, "value_out needs l_S <= 64");
+  if (int rc = vlp_decrypt_bits(sk, ct, l_S, bits)) return rc;
+  if (value) {
+    uint64_t v = 0;
+    for (uint32_t j = 0; j < l_S; j++) v |= static_cast<uint64_t>(bits[j]) << j;
+    *value = v;
+  }
+  return VLP_OK;
+}
+
 int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record) {
   if (int rc = check_meta(meta)) return rc;
   if (!per_record) return fail(VLP_EINVAL, "null output");

@@ -312,3 +312,47 @@ def test_idm_serial_eq_or_reduce_full_parity(server):
     """IdM with the serial alg:HomEQ and the OR reduction flag (R19), 4 records."""
     flags = OC.F_SUM_TREE | OC.F_OR_REDUCE
     _full_parity_small(server, OC.MODE_IDM, 1, 5, 2, flags, [(7,), (19,), (7,), (30,)], [1, 2, 2, 3], [7])
+
+
+def test_problem_statement_calls(server, okeys):
+    """vlp_server_eval / vlp_server_combine / vlp_gate_batch / vlp_decrypt_result: config 1
+    through server_eval equals the program path byte for byte; two shards of 2 records + combine(G=2)
+    equal the single-shot result (R15); a MUX batch with separate b and c buffers equals the oracle."""
+    wl = make_workload(1, key_seed=SEED)
+    k = server.keys
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    q = A.to_device(k.encrypt_query(m, wl.query, 7))
+    db_h = k.encrypt_db(m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1)
+    db = A.to_device(db_h)
+    prog = A.Program.velopir(server, m)
+    ref = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    prog.eval(q, db, ref)
+    out = torch.zeros_like(ref)
+    server.eval(m, q, db, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(A.to_host(out), A.to_host(ref))
+    bits, value = k.decrypt_result(A.to_host(out), wl.l_S)
+    want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+    assert value == want and list(bits) == [(want >> j) & 1 for j in range(wl.l_S)]
+    # two shards of M/2 records, then the top tree level
+    per = A.record_cts(m)
+    half = wl.M // 2
+    roots = torch.zeros((2, wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    for r in range(2):
+        server.eval(m, q, db[r * half * per:(r + 1) * half * per], roots[r], first=r * half, count=half)
+    comb = torch.zeros_like(ref)
+    server.combine(m, 2, roots, comb)
+    torch.cuda.synchronize()
+    assert np.array_equal(A.to_host(comb), A.to_host(ref))
+    # MUX with separate b / c device buffers
+    rng = np.random.default_rng(11)
+    bits3 = rng.integers(0, 2, (3, 9), dtype=np.uint8)
+    a, b, c = (k.encrypt_bits(bits3[i], 800 + i, 0) for i in range(3))
+    o = torch.zeros((9, 632), dtype=torch.int32, device="cuda:0")
+    server.gate_batch(L.MUX, A.to_device(a), A.to_device(b), o, c_dev=A.to_device(c))
+    torch.cuda.synchronize()
+    got = A.to_host(o)
+    want_ct = list(POOL.map(lambda i: okeys.mux(a[i, :631], b[i, :631], c[i, :631]), range(9)))
+    for i in range(9):
+        assert np.array_equal(got[i, :631], want_ct[i]), i
+    assert np.array_equal(k.decrypt_bits(got), np.where(bits3[0] == 1, bits3[1], bits3[2]))
