@@ -243,6 +243,60 @@ def _full_size_sampled(server, cfg, sample):
     return wl, want
 
 
+def _trivial_run(server, mode, d, l_I, l_S, flags, records, payloads, query):
+    """P11 on explicit records: every input trivial (0, Ecd(bit)); returns the l_S output rows."""
+    m = A.meta(mode, len(records), l_I, l_S, d, flags)
+    per = A.record_cts(m)
+    W = len(records[0])
+    db = np.zeros((len(records) * per, 632), np.uint32)
+    for i, (rec, pay) in enumerate(zip(records, payloads)):
+        bits = [(int(rec[k]) >> j) & 1 for k in range(W) for j in range(l_I)] + [(int(pay) >> j) & 1 for j in range(l_S)]
+        db[i * per:(i + 1) * per, 630] = np.where(np.array(bits) == 1, 0x20000000, 0xE0000000)
+    q = np.zeros((len(query) * l_I, 632), np.uint32)
+    for w, v in enumerate(query):
+        for j in range(l_I):
+            q[w * l_I + j, 630] = 0x20000000 if (int(v) >> j) & 1 else 0xE0000000
+    out = torch.zeros((l_S, 632), dtype=torch.int32, device="cuda:0")
+    server.eval(m, A.to_device(q), A.to_device(db), out)
+    torch.cuda.synchronize()
+    return A.to_host(out)
+
+
+@pytest.mark.parametrize("case", ["idm32x64", "rect32x64", "cov32", "intv2x1_single", "idm_or_serial"])
+def test_all_trivial_extreme_widths(server, case):
+    """P11 at the width limits of the ABI (l_I = 32, l_S = 64), a single record (no aggregation tree), the
+    minimum comparator width l_I = 2, non-power-of-two M, and the paper-literal serial/OR variants: the
+    output must be exactly (0, Ecd(bit)) of the plain predicate."""
+    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    full = lambda l: int(rng.integers(0, 2 ** l, dtype=np.uint64))  # noqa: E731
+    if case == "idm32x64":
+        mode, d, l_I, l_S, flags = OC.MODE_IDM, 1, 32, 64, OC.CONFIG_FLAGS
+        q = [full(32)]
+        recs = [(full(32),), (q[0],), (full(32),)]
+    elif case == "rect32x64":
+        mode, d, l_I, l_S, flags = OC.MODE_INTV, 2, 32, 64, OC.CONFIG_FLAGS
+        q = [full(31), full(31)]
+        recs = [(q[0] - 5, q[0] + 9, q[1] - 1, q[1]), (q[0], q[0], q[1] + 1, q[1] + 2), (0, 2 ** 32 - 1, 0, 2 ** 32 - 1),
+                (q[0] + 1, q[0] + 3, 0, 7), (0, q[0], q[1], 2 ** 32 - 1)]
+    elif case == "cov32":
+        mode, d, l_I, l_S, flags = OC.MODE_COV, 2, 32, 40, OC.CONFIG_FLAGS
+        q = [full(32), full(32)]
+        recs = [(q[0], q[1]), (q[0], q[1] ^ 1), (q[0], q[1])]
+    elif case == "intv2x1_single":
+        mode, d, l_I, l_S, flags = OC.MODE_INTV, 1, 2, 1, OC.CONFIG_FLAGS
+        q = [2]
+        recs = [(1, 3)]
+    else:
+        mode, d, l_I, l_S, flags = OC.MODE_IDM, 1, 9, 7, OC.F_OR_REDUCE
+        q = [300]
+        recs = [(300,), (5,), (300,), (511,), (0,), (300,), (299,)]
+    pays = [full(l_S) for _ in recs]
+    out = _trivial_run(server, mode, d, l_I, l_S, flags, recs, pays, q)
+    want = OC.plain_result(mode, q, [list(r) for r in recs], pays, d, flags, l_I)
+    assert not out[:, :630].any()
+    assert [int(x) for x in out[:, 630]] == [0x20000000 if (want >> j) & 1 else 0xE0000000 for j in range(l_S)]
+
+
 def test_config2_full_size_sampled(server):
     """Config 2 at full size (IntV 1D, 1024 records, 132,080 BR): predicate + records 3 and 1023 byte-equal."""
     _full_size_sampled(server, 2, [3, 1023])
@@ -356,3 +410,10 @@ def test_problem_statement_calls(server, okeys):
     for i in range(9):
         assert np.array_equal(got[i, :631], want_ct[i]), i
     assert np.array_equal(k.decrypt_bits(got), np.where(bits3[0] == 1, bits3[1], bits3[2]))
+
+
+def test_single_record_min_width_full_parity(server):
+    """Degenerate instance on real encryptions: one record (no aggregation tree, the masked payload is the
+    result), the minimum comparator width l_I = 2 and a 1-bit payload."""
+    want = _full_parity_small(server, OC.MODE_INTV, 1, 2, 1, OC.CONFIG_FLAGS, [(1, 3)], [1], [2])
+    assert want == 1
