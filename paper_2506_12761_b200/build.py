@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             subprocess.check_call(cmd)
         objs.append(o)
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-pthread"])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-pthread",
+                               "-lcublasLt", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
         os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -1,6 +1,7 @@
 // api.cu -- the device half of the C ABI (include/vlp.h): server creation (evk upload + NTT conversion),
 // program compilation / binding / evaluation (one BR launch + one KS launch per circuit level),
 // and the debug entry points used by the parity tests.
+#include <cublasLt.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -20,6 +21,13 @@ struct vlp_server {
   uint2* tw_fwd = nullptr;   // natural order (bsk conversion)
   uint2* twl_fwd = nullptr;  // thread-layout tables of the blind-rotate kernel
   uint2* twl_inv = nullptr;
+  int8_t* kmat = nullptr;  // ksk as 4 signed byte limbs, [2528][24576] (tensor-core key switch)
+  cublasLtHandle_t lt = nullptr;
+  std::mutex algo_mu;
+  std::map<uint32_t, cublasLtMatmulAlgo_t> algos;  // cuBLASLt algorithm per GEMM row count
+  ~vlp_server() {
+    if (lt) cublasLtDestroy(lt);
+  }
   // programs compiled by the problem-statement calls (vlp_server_eval, vlp_server_combine, vlp_gate_batch)
   std::mutex mu;
   std::map<std::string, std::unique_ptr<vlp_program>> cache;
@@ -30,6 +38,8 @@ struct vlp_program {
   vlp::Schedule sched;
   // scratch layout (byte offsets)
   size_t off_br = 0, off_ks = 0, off_outslots = 0, off_mid = 0, off_nlwe = 0, bytes = 0;
+  size_t off_ks_ws = 0;  // tensor-core key switch staging (ks_stage_bytes)
+  uint32_t ks_chunk = 0;
   std::vector<size_t> br_first, ks_first;  // per level, index of the level's first job
   std::vector<uint32_t> copy_slots;        // outputs that are not written in place
   void* bound = nullptr;
@@ -67,7 +77,7 @@ constexpr size_t kKskBytes = static_cast<size_t>(N) * kKsT * 3 * kCt * 4;
 constexpr size_t kTwBytes = static_cast<size_t>(N) * sizeof(uint2);
 constexpr size_t kTwlBytes = static_cast<size_t>(kTwSlots) * kBT * sizeof(uint2);
 constexpr size_t kRawBskBytes = static_cast<size_t>(n) * kRows * 2 * N * 4;
-constexpr size_t kEvkBytes = kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes;
+constexpr size_t kEvkBytes = kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes + kKmatBytes;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -136,6 +146,74 @@ void make_layout_twiddles(const std::vector<uint2>& nat, std::vector<uint2>& lay
     }
 }
 
+// K3' key switch on the tensor cores, in chunks of at most `chunk` ciphertexts: one-hot digit indicator
+// (our kernel) -> D = ind x kmat^T as a cuBLASLt int8 GEMM with int32 accumulation (a plain library GEMM;
+// exact, |D| < 2^21) -> combine (our kernel).
+int ks_gemm(vlp_server* s, uint32_t rows, const int8_t* ind, int32_t* dmat, void* ws, cudaStream_t st) {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, ld = nullptr;
+  int rc = VLP_OK;
+  const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+  const int32_t one = 1, zero = 0;
+  if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, kKsK, kKsNp, kKsK) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, kKsK, rows, kKsK) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&ld, CUDA_R_32I, kKsNp, rows, kKsNp) != CUBLAS_STATUS_SUCCESS) {
+    rc = fail(VLP_ECUDA, "cuBLASLt descriptor setup failed");
+  }
+  cublasLtMatmulAlgo_t algo{};
+  if (rc == VLP_OK) {
+    std::lock_guard<std::mutex> lock(s->algo_mu);
+    auto it = s->algos.find(rows);
+    if (it == s->algos.end()) {
+      cublasLtMatmulPreference_t pref = nullptr;
+      size_t wsb = kKsWsBytes;
+      cublasLtMatmulHeuristicResult_t h{};
+      int nres = 0;
+      if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS ||
+          cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb)) !=
+              CUBLAS_STATUS_SUCCESS ||
+          cublasLtMatmulAlgoGetHeuristic(s->lt, op, la, lb, ld, ld, pref, 1, &h, &nres) != CUBLAS_STATUS_SUCCESS ||
+          nres == 0)
+        rc = fail(VLP_ECUDA, "no cuBLASLt int8 algorithm for the key-switch GEMM");
+      else
+        it = s->algos.emplace(rows, h.algo).first;
+      if (pref) cublasLtMatmulPreferenceDestroy(pref);
+    }
+    if (rc == VLP_OK) algo = it->second;
+  }
+  if (rc == VLP_OK &&
+      cublasLtMatmul(s->lt, op, &one, s->kmat, la, ind, lb, &zero, dmat, ld, dmat, ld, &algo, ws, kKsWsBytes, st) !=
+          CUBLAS_STATUS_SUCCESS)
+    rc = fail(VLP_ECUDA, "cuBLASLt key-switch GEMM failed");
+  if (ld) cublasLtMatrixLayoutDestroy(ld);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (op) cublasLtMatmulDescDestroy(op);
+  return rc;
+}
+
+int run_keyswitch(vlp_server* s, const KsArgs& ka, uint8_t* stage, uint32_t chunk, cudaStream_t st) {
+  // stage: [cuBLASLt workspace][indicator chunk x 24576][D chunk x 2528 int32]
+  void* ws = stage;
+  int8_t* ind = reinterpret_cast<int8_t*>(stage + align256(kKsWsBytes));
+  int32_t* dmat = reinterpret_cast<int32_t*>(stage + align256(kKsWsBytes) + align256(static_cast<size_t>(chunk) * kKsK));
+  cudaError_t e;
+  for (uint32_t c0 = 0; c0 < ka.njobs; c0 += chunk) {
+    const uint32_t cnt = std::min(chunk, ka.njobs - c0);
+    if ((e = launch_ks_indicator(ka, c0, cnt, ind, st))) return cuda_fail(e, "key-switch indicator");
+    if (int rc = ks_gemm(s, cnt, ind, dmat, ws, st)) return rc;
+    if ((e = launch_ks_combine(ka, c0, cnt, dmat, st))) return cuda_fail(e, "key-switch combine");
+  }
+  return VLP_OK;
+}
+
+size_t ks_stage_bytes(uint32_t chunk) {
+  return align256(kKsWsBytes) + align256(static_cast<size_t>(chunk) * kKsK) + align256(static_cast<size_t>(chunk) * kKsNp * 4);
+}
+
 Regions regions(const vlp_program* p, void* scratch, const uint32_t* in0, const uint32_t* in1, uint32_t* out) {
   Regions r;
   r.base[kRegIn0] = const_cast<uint32_t*>(in0);
@@ -161,13 +239,16 @@ int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
   p->off_outslots = align256(p->off_ks + nks * sizeof(KsJob));
   p->off_mid = align256(p->off_outslots + p->copy_slots.size() * 4 + 4);
   p->off_nlwe = align256(p->off_mid + s.mid_rows * kCt * 4);
-  p->bytes = align256(p->off_nlwe + s.nlwe_rows * kNlwe * 4);
+  size_t max_ks = 0;
+  for (auto& L : s.levels) max_ks = std::max(max_ks, L.ks.size());
+  p->ks_chunk = static_cast<uint32_t>(std::min<size_t>(std::max<size_t>(max_ks, 1), kKsChunk));
+  p->off_ks_ws = align256(p->off_nlwe + s.nlwe_rows * kNlwe * 4);
+  p->bytes = p->off_ks_ws + ks_stage_bytes(p->ks_chunk);
   p->server = server;
   p->launches = 1 + (p->copy_slots.empty() ? 0 : 1);
-  for (auto& L : s.levels) {
-    const uint32_t tiles = static_cast<uint32_t>((L.ks.size() + kKsCt - 1) / kKsCt);
+  for (auto& L : s.levels) {  // our kernels: BR waves + (indicator, combine) per key-switch GEMM chunk
     p->launches += br_launch_count(static_cast<uint32_t>(L.br.size()), server ? server->sm_count : 148) +
-                   (L.ks.empty() ? 0 : (tiles < 4 * 148 ? 2 : 1));
+                   2 * static_cast<uint32_t>((L.ks.size() + p->ks_chunk - 1) / p->ks_chunk);
   }
   return VLP_OK;
 }
@@ -200,6 +281,8 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   srv->twl_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes);
   srv->twl_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes + kTwlBytes);
   uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes);
+  srv->kmat = reinterpret_cast<int8_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes);
+  if (cublasLtCreate(&srv->lt) != CUBLAS_STATUS_SUCCESS) return fail(VLP_ECUDA, "cublasLtCreate failed");
 
   std::vector<uint2> fwd, inv, lf, li;
   make_twiddles(fwd, inv);
@@ -216,6 +299,7 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   // Montgomery factor with N^-1 folded in: c = N^-1 * 2^32 mod p
   const uint32_t c_mont = static_cast<uint32_t>(mulmod(powmod(N, kP - 2), (1ull << 32) % kP));
   launch_bsk_convert(raw, srv->bsk_ntt, srv->tw_fwd, c_mont, st);
+  launch_ksk_to_i8(srv->ksk, srv->kmat, st);
   if ((e = cudaGetLastError())) return cuda_fail(e, "bsk convert launch");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server create");
   *out = srv.release();
@@ -344,7 +428,7 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
     ka.ksk = s->ksk;
     if (ka.njobs) {
       p->begin(1, st);
-      if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
+      if (int rc = run_keyswitch(s, ka, sc + p->off_ks_ws, p->ks_chunk, st)) return rc;
       p->end(1, st);
     }
   }
@@ -384,7 +468,10 @@ int vlp_program_profile_read(vlp_program* p, double* br_ms, double* ks_ms, uint6
   return VLP_OK;
 }
 
-size_t vlp_debug_scratch_bytes(size_t count) { return align256(count * sizeof(BrJob)) + align256(count * sizeof(KsJob)); }
+size_t vlp_debug_scratch_bytes(size_t count) {
+  const uint32_t chunk = static_cast<uint32_t>(std::min<size_t>(std::max<size_t>(count, 1), kKsChunk));
+  return std::max(align256(count * sizeof(BrJob)), align256(count * sizeof(KsJob)) + ks_stage_bytes(chunk));
+}
 
 int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, int steps, uint32_t* acc_dev,
                            void* scratch, uint64_t stream) {
@@ -428,7 +515,9 @@ int vlp_debug_keyswitch(vlp_server* s, const uint32_t* nlwe_dev, size_t count, u
   ka.reg.base[kRegOut] = out_dev;
   ka.nlwe = nlwe_dev;
   ka.ksk = s->ksk;
-  if ((e = launch_keyswitch(ka, st))) return cuda_fail(e, "key switch");
+  const uint32_t chunk = static_cast<uint32_t>(std::min<size_t>(std::max<size_t>(count, 1), kKsChunk));
+  if (int rc = run_keyswitch(s, ka, static_cast<uint8_t*>(scratch) + align256(count * sizeof(KsJob)), chunk, st))
+    return rc;
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
   return VLP_OK;
 }

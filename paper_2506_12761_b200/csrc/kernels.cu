@@ -2,7 +2,8 @@
 //
 //  K2 vlp_blind_rotate_kernel : gate linear form (S2) + mod-switch (S3) + accumulator init (S4) +
 //                               630 CMux steps (S5) with the accumulator on chip + SampleExtract (S6)
-//  K3 vlp_keyswitch_kernel    : MUX combine (S7) + key switch (S8)
+//  K3 vlp_ks_indicator_kernel + cuBLASLt int8 GEMM + vlp_ks_combine_kernel : MUX combine (S7) + key
+//                               switch (S8) as a one-hot-indicator x byte-limb-ksk GEMM on the tensor cores
 //  K4 vlp_bsk_convert_kernel  : bsk -> 3-limb NTT domain (setup)
 //
 // Exact arithmetic: NTT prime p = 0x3fff7801 (p = 1 mod 2048, 4p < 2^32); the
@@ -496,97 +497,66 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kTmemCols) : "memory");
 }
 
-// ================================================================================ K3 key switch
-// CTA: kKsCt ciphertexts x all 632 columns (160 threads x 4 columns), coefficients [i0, i1) (a.parts
-// splits of [0, N) across blockIdx.y, reduced atomically).  For every (i, j) each ciphertext's digit selects
-// one of the three ksk rows; the thread reads its 16-byte column quad of that row straight from L2 through
-// L1 (a warp reads 512 contiguous bytes; the CTA's ciphertexts share the three rows in L1).  Only the
-// rounded masks live in shared memory (32 KB), so several CTAs fit per SM.
-__global__ void __launch_bounds__(kKsThreads) vlp_keyswitch_kernel(const KsArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint16_t* abar = reinterpret_cast<uint16_t*>(smem);  // [kKsCt][N]
-
-  const uint32_t tid = threadIdx.x;
-  const uint32_t c0 = blockIdx.x * kKsCt;
-  const uint32_t nct = min(static_cast<uint32_t>(kKsCt), a.njobs - c0);
-  const int i0 = static_cast<int>(blockIdx.y) * N / a.parts, i1 = static_cast<int>(blockIdx.y + 1) * N / a.parts;
-
-  // S7 MUX combine + rounding to 16 bits (R6)
-  for (uint32_t idx = tid; idx < nct * (i1 - i0); idx += blockDim.x) {
-    const uint32_t c = idx / (i1 - i0), i = i0 + idx % (i1 - i0);
-    const KsJob job = a.jobs[c0 + c];
-    uint32_t v = a.nlwe[static_cast<size_t>(job.n0) * kNlwe + i];
-    if (job.n1 != 0xFFFFFFFFu) v += a.nlwe[static_cast<size_t>(job.n1) * kNlwe + i];
-    abar[c * N + i] = static_cast<uint16_t>((v + (1u << 15)) >> 16);
-  }
-  __syncthreads();
-
-  const uint32_t col = tid * 4;
-  const bool live = col < static_cast<uint32_t>(kCt);
-  uint32_t acc[kKsCt][4];
+// ================================================================================ K3' key switch on tensor cores
+// (a) one-hot digit indicator: CTA per ciphertext; coefficient i -> 24 bytes ind[c][i*24 + j*3 + v-1].
+//     MUX combine (S7) and the 16-bit rounding (R6) in the prologue, as in K3.
+__global__ void __launch_bounds__(256) vlp_ks_indicator_kernel(const KsArgs a, uint32_t c0, int8_t* __restrict__ ind) {
+  const uint32_t c = blockIdx.x;
+  const KsJob job = a.jobs[c0 + c];
+  const uint32_t* x0 = a.nlwe + static_cast<size_t>(job.n0) * kNlwe;
+  const uint32_t* x1 = job.n1 != 0xFFFFFFFFu ? a.nlwe + static_cast<size_t>(job.n1) * kNlwe : nullptr;
+  uint2* row = reinterpret_cast<uint2*>(ind + static_cast<size_t>(c) * kKsK);
+  for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(N); i += blockDim.x) {
+    uint32_t v = x0[i];
+    if (x1) v += x1[i];
+    const uint32_t ab = (v + (1u << 15)) >> 16;  // 16-bit rounded mask (R6)
+    uint64_t w[3] = {0, 0, 0};
 #pragma unroll
-  for (int c = 0; c < kKsCt; c++) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0;
-
-  if (live) {
-    const uint32_t* kq = a.ksk + col;
-    for (int i = i0; i < i1; i++) {
-      uint32_t ab[kKsCt];
-#pragma unroll
-      for (int c = 0; c < kKsCt; c++) ab[c] = c < static_cast<int>(nct) ? abar[c * N + i] : 0u;
-      const uint32_t* ki = kq + static_cast<size_t>(i) * kKsRowWords;
-#pragma unroll
-      for (int j = 0; j < kKsT; j++) {
-#pragma unroll
-        for (int c = 0; c < kKsCt; c++) {
-          const uint32_t dg = (ab[c] >> (14 - 2 * j)) & 3u;
-          if (dg) {
-            const uint4 row = __ldg(reinterpret_cast<const uint4*>(ki + (j * 3 + (dg - 1)) * kCt));
-            acc[c][0] += row.x;
-            acc[c][1] += row.y;
-            acc[c][2] += row.z;
-            acc[c][3] += row.w;
-          }
-        }
+    for (int j = 0; j < kKsT; j++) {
+      const uint32_t dg = (ab >> (14 - 2 * j)) & 3u;  // most significant digit first
+      if (dg) {
+        const int byte = j * 3 + static_cast<int>(dg) - 1;
+        w[byte >> 3] |= 1ull << (8 * (byte & 7));
       }
     }
-  }
-  if (!live) return;
-  // out = (0, b') - sum (S8); with several coefficient parts the partial sums are reduced atomically
-  // into a row pre-set to (0, b') by vlp_ks_init_kernel (u32 adds commute: exact).
 #pragma unroll
-  for (int c = 0; c < kKsCt; c++) {
-    if (c >= static_cast<int>(nct)) break;
-    const KsJob job = a.jobs[c0 + c];
-    uint32_t* o = slot_wptr(a.reg, job.out);
-    if (a.parts == 1) {
-      uint32_t bp = a.nlwe[static_cast<size_t>(job.n0) * kNlwe + N];
-      if (job.n1 != 0xFFFFFFFFu) bp += a.nlwe[static_cast<size_t>(job.n1) * kNlwe + N];
-      bp += job.add;
-      uint4 r;
-      r.x = (col + 0 == static_cast<uint32_t>(n) ? bp : 0u) - acc[c][0];
-      r.y = (col + 1 == static_cast<uint32_t>(n) ? bp : 0u) - acc[c][1];
-      r.z = (col + 2 == static_cast<uint32_t>(n) ? bp : 0u) - acc[c][2];
-      r.w = col + 3 >= static_cast<uint32_t>(n + 1) ? 0u : ((col + 3 == static_cast<uint32_t>(n) ? bp : 0u) - acc[c][3]);
-      *reinterpret_cast<uint4*>(o + col) = r;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; e++)
-        if (col + e <= static_cast<uint32_t>(n) && acc[c][e]) atomicAdd(o + col + e, 0u - acc[c][e]);
-    }
+    for (int q = 0; q < 3; q++) row[i * 3 + q] = make_uint2(static_cast<uint32_t>(w[q]), static_cast<uint32_t>(w[q] >> 32));
   }
 }
 
-__global__ void vlp_ks_init_kernel(const KsArgs a) {
+// (b) combine: out = (0, b' + add) - sum_l D_l << 8l (mod 2^32), pad word 0.  CTA per ciphertext.
+__global__ void __launch_bounds__(256) vlp_ks_combine_kernel(const KsArgs a, uint32_t c0, const int32_t* __restrict__ d) {
   const uint32_t c = blockIdx.x;
-  const KsJob job = a.jobs[c];
+  const KsJob job = a.jobs[c0 + c];
+  const int32_t* dr = d + static_cast<size_t>(c) * kKsNp;
   uint32_t* o = slot_wptr(a.reg, job.out);
-  for (uint32_t k = threadIdx.x; k < static_cast<uint32_t>(kCt); k += blockDim.x) {
+  for (uint32_t col = threadIdx.x; col < static_cast<uint32_t>(kCt); col += blockDim.x) {
     uint32_t v = 0;
-    if (k == static_cast<uint32_t>(n)) {
-      v = a.nlwe[static_cast<size_t>(job.n0) * kNlwe + N] + job.add;
-      if (job.n1 != 0xFFFFFFFFu) v += a.nlwe[static_cast<size_t>(job.n1) * kNlwe + N];
+    if (col <= static_cast<uint32_t>(n)) {
+      const uint32_t s = static_cast<uint32_t>(dr[col]) + (static_cast<uint32_t>(dr[kCt + col]) << 8) +
+                         (static_cast<uint32_t>(dr[2 * kCt + col]) << 16) + (static_cast<uint32_t>(dr[3 * kCt + col]) << 24);
+      uint32_t b = 0;
+      if (col == static_cast<uint32_t>(n)) {
+        b = a.nlwe[static_cast<size_t>(job.n0) * kNlwe + N] + job.add;
+        if (job.n1 != 0xFFFFFFFFu) b += a.nlwe[static_cast<size_t>(job.n1) * kNlwe + N];
+      }
+      v = b - s;
     }
-    o[k] = v;
+    o[col] = v;
+  }
+}
+
+// (c) setup: kmat[l*632 + col][k] = signed byte limb l of ksk row k (k = (i*8 + j)*3 + v-1), column col.
+__global__ void vlp_ksk_to_i8_kernel(const uint32_t* __restrict__ ksk, int8_t* __restrict__ kmat) {
+  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<size_t>(kKsK) * kCt) return;
+  const uint32_t k = static_cast<uint32_t>(idx / kCt), col = static_cast<uint32_t>(idx % kCt);
+  int64_t x = static_cast<int64_t>(ksk[idx]);  // row k, column col of the [K][632] ksk
+#pragma unroll
+  for (int l = 0; l < 4; l++) {
+    const int64_t s = ((x + 128) & 255) - 128;  // balanced limb in [-128, 128)
+    kmat[(static_cast<size_t>(l) * kCt + col) * kKsK + k] = static_cast<int8_t>(s);
+    x = (x - s) >> 8;
   }
 }
 
@@ -744,22 +714,18 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
   return e;
 }
 
-cudaError_t launch_keyswitch(const KsArgs& a0, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(vlp_keyswitch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kKsSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  if (a0.njobs == 0) return cudaSuccess;
-  KsArgs a = a0;
-  const uint32_t tiles = (a.njobs + kKsCt - 1) / kKsCt;
-  int parts = 1;
-  while (parts < 16 && tiles * parts < 4 * 148) parts *= 2;  // fill the chip on narrow levels
-  a.parts = parts;
-  if (parts > 1) vlp_ks_init_kernel<<<a.njobs, 128, 0, st>>>(a);
-  vlp_keyswitch_kernel<<<dim3(tiles, parts), kKsThreads, kKsSmemBytes, st>>>(a);
+void launch_ksk_to_i8(const uint32_t* ksk, int8_t* kmat, cudaStream_t st) {
+  const size_t total = static_cast<size_t>(kKsK) * kCt;
+  vlp_ksk_to_i8_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ksk, kmat);
+}
+
+cudaError_t launch_ks_indicator(const KsArgs& a, uint32_t c0, uint32_t cnt, int8_t* ind, cudaStream_t st) {
+  if (cnt) vlp_ks_indicator_kernel<<<cnt, 256, 0, st>>>(a, c0, ind);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const int32_t* d, cudaStream_t st) {
+  if (cnt) vlp_ks_combine_kernel<<<cnt, 256, 0, st>>>(a, c0, d);
   return cudaGetLastError();
 }
 

@@ -33,11 +33,16 @@ __host__ __device__ constexpr int tmem_cols(int B) { return B * kTmemSlotCols <=
 static_assert(kBrBoot * kTmemSlotCols <= 512, "TMEM columns");
 static_assert(kBrSmemBytes <= 232448, "shared memory per CTA");
 
-// ---- key switch (K3)
-constexpr int kKsCt = 16;                                 // ciphertexts per CTA
-constexpr int kKsThreads = 160;                           // 158 column quads (632 words)
-constexpr int kKsRowWords = kKsT * 3 * kCt;               // ksk words per coefficient i: 15168
-constexpr int kKsSmemBytes = kKsCt * N * 2;
+
+// ---- key switch on the tensor cores (K3'): out = (0, b') - sum_{i,j} ksk[i][j][d_ij] written as a GEMM
+// D[c][l*632 + col] = sum_k ind[c][k] * kmat[l*632 + col][k] with the one-hot digit indicator
+// ind[c][(i*8 + j)*3 + v-1] = [d_ij == v] (int8) and kmat = the ksk split into 4 balanced signed byte limbs
+// (int8, |D| <= 8192 * 128 < 2^31: exact), then out = (0, b') - sum_l D_l 2^(8l) mod 2^32.
+constexpr int kKsK = N * kKsT * 3;               // 24576 GEMM depth
+constexpr int kKsNp = 4 * kCt;                   // 2528 GEMM columns (4 limbs x 632)
+constexpr size_t kKmatBytes = static_cast<size_t>(kKsNp) * kKsK;  // 62,128,128
+constexpr int kKsChunk = 8192;                   // ciphertexts per GEMM
+constexpr size_t kKsWsBytes = 32u << 20;         // cuBLASLt workspace
 
 struct Regions {
   uint32_t* base[4];  // kRegIn0, kRegIn1, kRegMid, kRegOut; rows of kCt words
@@ -62,8 +67,7 @@ struct KsArgs {
   uint32_t njobs;
   Regions reg;
   const uint32_t* nlwe;  // [rows][kNlwe]
-  const uint32_t* ksk;   // [N][8][3][kCt]
-  int parts;             // coefficient-range splits (gridDim.y)
+  const uint32_t* ksk;   // [N][8][3][kCt] (torus32 key-switching key; the GEMM uses its byte limbs)
 };
 
 void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd, uint32_t c_mont,
@@ -72,7 +76,9 @@ void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
 // one level: whole waves of kBrBoot bootstraps per CTA + a narrower tail wave (1 or 2 kernel launches)
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st);
 int br_launch_count(uint32_t njobs, int sm_count);
-cudaError_t launch_keyswitch(const KsArgs& a, cudaStream_t st);
+void launch_ksk_to_i8(const uint32_t* ksk, int8_t* kmat, cudaStream_t st);
+cudaError_t launch_ks_indicator(const KsArgs& a, uint32_t c0, uint32_t cnt, int8_t* ind, cudaStream_t st);
+cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const int32_t* d, cudaStream_t st);
 cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st);
 cudaError_t launch_copy_rows(const uint32_t* slots, uint32_t count, Regions reg, uint32_t* out, cudaStream_t st);
 
