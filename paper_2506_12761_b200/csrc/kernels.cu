@@ -16,6 +16,7 @@
 // Thread layout of one bootstrap: see "layouts / swizzle" below (128 threads x 8 coefficients).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -642,12 +643,16 @@ void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd,
 
 template <int B>
 static cudaError_t launch_br_b(const BrArgs& a, int sm_count, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(vlp_blind_rotate_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         br_smem_bytes(B));
+  // the dynamic shared-memory opt-in is per device: remember it per device ordinal (< 64)
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    e = cudaFuncSetAttribute(vlp_blind_rotate_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, br_smem_bytes(B));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(bit);
   }
   if (a.njobs == 0) return cudaSuccess;
   const uint64_t groups = (a.njobs + B - 1) / B;
