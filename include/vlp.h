@@ -69,7 +69,7 @@ typedef struct {
   double sigma_lwe, sigma_bk, sigma_ks;
 } vlp_params;
 
-/* Session meta: M records, l_I location bits, l_S payload bits, d coordinates. */
+/* Session meta: M records, l_I location bits (2..32), l_S payload bits (1..128), d coordinates. */
 typedef struct {
   uint32_t mode, M, l_I, l_S, d, flags;
 } vlp_meta;
@@ -127,7 +127,8 @@ int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t 
 int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);
 /* alg:ServerEnc for the pk's records: ct = (0, Ecd(bit)) + pk sample.
  * words: [count][W] plaintext bound words (IntV: lo,hi per axis; CoV: loc per axis; IdM: id);
- * payloads: [count] values (< 2^l_S).  out: host [count][per_record][632] in the order word-major
+ * payloads: [count][ceil(l_S / 64)] little-endian 64-bit words (value < 2^l_S; one word for l_S <= 64).
+ * out: host [count][per_record][632] in the order word-major
  * location bits (word k bit j at row k*l_I + j) then payload bits (row W*l_I + j).  Consumes the pk:
  * a second call returns VLP_EPKUSED.  Server side: needs no secret key. */
 int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* out);

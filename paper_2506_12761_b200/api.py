@@ -88,14 +88,19 @@ class Keys:
                                        ctypes.byref(v) if l_S <= 64 else None))
         return bits, v.value
 
-    def decrypt_value(self, ct: np.ndarray) -> int:
+    def decrypt_value(self, ct: np.ndarray) -> int:  # any l_S (Python int)
         return int(sum(int(b) << j for j, b in enumerate(self.decrypt_bits(ct))))
 
     def encrypt_db(self, m: VlpMeta, words, payloads, pk_seed: int, first: int = 0, count: int | None = None):
         """Client PubKeyGen (alg:PubKeyGen) + server ServerEnc (alg:ServerEnc) for records [first, first+count)."""
         words = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
-        payloads = np.ascontiguousarray(np.asarray(payloads, dtype=np.uint64))
         count = len(payloads) if count is None else count
+        pw = (m.l_S + 63) // 64  # payload words per record (l_S up to 128)
+        if pw == 1:
+            payloads = np.ascontiguousarray(np.asarray(payloads, dtype=np.uint64))
+        else:
+            payloads = np.array([[(int(v) >> (64 * w)) & (2 ** 64 - 1) for w in range(pw)] for v in payloads],
+                                dtype=np.uint64)
         pk = ctypes.c_void_p()
         check(lib().vlp_pubkeygen(self.sk, ctypes.byref(m), pk_seed, first, count, ctypes.byref(pk)))
         try:

@@ -77,8 +77,8 @@ static void parallel_for(size_t count, F&& fn) {
 int check_meta(const vlp_meta* m) {
   if (!m) return fail(VLP_EINVAL, "meta is NULL");
   if (m->mode > VLP_MODE_IDM) return fail(VLP_EMODE, "unknown mode");
-  if (m->l_I < 2 || m->l_I > 32 || m->l_S < 1 || m->l_S > 64)
-    return fail(VLP_EWIDTH, "l_I must be in [2, 32] and l_S in [1, 64]");
+  if (m->l_I < 2 || m->l_I > 32 || m->l_S < 1 || m->l_S > 128)
+    return fail(VLP_EWIDTH, "l_I must be in [2, 32] and l_S in [1, 128]");
   if (m->mode == VLP_MODE_IDM ? m->d != 1 : (m->d < 1 || m->d > 2)) return fail(VLP_EMODE, "bad d for mode");
   if (m->M < 1) return fail(VLP_EINVAL, "M must be >= 1");
   return VLP_OK;
@@ -262,18 +262,21 @@ int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* pay
   if (pk->used) return fail(VLP_EPKUSED, "public-key samples already used (single-use, alg:PubKeyGen)");
   const vlp_meta& m = pk->meta;
   const size_t W = record_words(m), lI = m.l_I, lS = m.l_S, per = W * lI + lS;
+  const size_t PW = (lS + 63) / 64, top = lS - 64 * (PW - 1);  // payload words per record, bits in the last
   for (size_t r = 0; r < pk->count; r++) {
     for (size_t k = 0; k < W; k++)
       if (lI < 64 && words[r * W + k] >> lI) return fail(VLP_ERANGE, "record word >= 2^l_I");
-    if (lS < 64 && payloads[r] >> lS) return fail(VLP_ERANGE, "payload >= 2^l_S");
+    if (top < 64 && payloads[r * PW + PW - 1] >> top) return fail(VLP_ERANGE, "payload >= 2^l_S");
   }
   parallel_for(pk->count * per, [&](size_t idx) {
     const size_t rec = idx / per, row = idx % per;
     uint32_t bit;
-    if (row < W * lI)
+    if (row < W * lI) {
       bit = static_cast<uint32_t>((words[rec * W + row / lI] >> (row % lI)) & 1);
-    else
-      bit = static_cast<uint32_t>((payloads[rec] >> (row - W * lI)) & 1);
+    } else {
+      const size_t j = row - W * lI;
+      bit = static_cast<uint32_t>((payloads[rec * PW + j / 64] >> (j % 64)) & 1);
+    }
     const uint32_t* s = pk->samples.data() + idx * kCt;
     uint32_t* d = out + idx * kCt;
     std::memcpy(d, s, kCt * 4);

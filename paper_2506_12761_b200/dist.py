@@ -12,6 +12,8 @@ from __future__ import annotations
 
 def shard_range(M: int, world: int, rank: int):
     """(first, count) of rank's contiguous shard; M/world must be a power of two (R15)."""
+    if world == 1:
+        return 0, M  # a single shard needs no tree boundary alignment
     if world < 1 or M % world:
         raise ValueError("M must be divisible by the number of ranks")
     count = M // world

@@ -6,6 +6,13 @@ Configs (BASELINE.json):
   3 rectangle      l_I=16, M=4096,   l_S=32  d=2, sides round(2^u), u ~ U[6,12] per axis; K forced hits
   4 IdM            l_I=20, M=65536,  l_S=32  distinct U[0,2^20) ids; query id present or absent by seed
   5 NAND sweep     2^10 / 2^14 / 2^17 / 2^20 pairs of U{0,1} bits
+Synthetic stand-ins with the SHAPES of the paper's four datasets.  No
+dataset record is reproduced: regions are disjoint random boxes in a 16 x 16 grid of the 2^16 x 2^16
+plane, points / ids are distinct uniform draws, payloads uniform; the query hits one record or none by seed.
+  6 covid-kor shape  IntV d=2 (rectangles)  M=9,   l_I=16, l_S=9
+  7 covid-usa shape  IntV d=2 (rectangles)  M=58,  l_I=16, l_S=22
+  8 gdacs shape      CoV  d=2 (points)      M=9,   l_I=16, l_S=16
+  9 weather-usa shape IdM                   M=304, l_I=16, l_S=128
 Seeds: keys 1000 + cfg, data 2000 + cfg (overridable).
 """
 from __future__ import annotations
@@ -45,6 +52,10 @@ CONFIGS = {
     2: dict(name="intv1d_1024", mode=MODE_INTV, M=1024, l_I=16, l_S=16, d=1),
     3: dict(name="rect2d_4096", mode=MODE_INTV, M=4096, l_I=16, l_S=32, d=2),
     4: dict(name="idm_65536", mode=MODE_IDM, M=65536, l_I=20, l_S=32, d=1),
+    6: dict(name="kor_shape_intv2d_9", mode=MODE_INTV, M=9, l_I=16, l_S=9, d=2),
+    7: dict(name="usa_shape_intv2d_58", mode=MODE_INTV, M=58, l_I=16, l_S=22, d=2),
+    8: dict(name="gdacs_shape_cov_9", mode=MODE_COV, M=9, l_I=16, l_S=16, d=2),
+    9: dict(name="weather_shape_idm_304", mode=MODE_IDM, M=304, l_I=16, l_S=128, d=1),
 }
 
 
@@ -76,7 +87,13 @@ def make_workload(cfg: int, data_seed: int | None = None, key_seed: int | None =
     rng = np.random.default_rng(data_seed)
     l_I, l_S, d, mode = c["l_I"], c["l_S"], c["d"], c["mode"]
     top = 1 << l_I
-    payloads = rng.integers(0, 1 << l_S, size=M, dtype=np.uint64)
+    if l_S <= 64:
+        payloads = rng.integers(0, 1 << l_S, size=M, dtype=np.uint64) if l_S < 64 else \
+            rng.integers(0, 2 ** 64, size=M, dtype=np.uint64)
+    else:  # l_S up to 128: Python ints (two 64-bit draws)
+        lo = rng.integers(0, 2 ** 64, size=M, dtype=np.uint64)
+        hi = rng.integers(0, 1 << (l_S - 64), size=M, dtype=np.uint64)
+        payloads = np.array([int(a) | (int(b) << 64) for a, b in zip(lo, hi)], dtype=object)
     forced = []
     if cfg == 1:
         x = int(rng.integers(0, top))
@@ -121,6 +138,39 @@ def make_workload(cfg: int, data_seed: int | None = None, key_seed: int | None =
                 if q not in idset:
                     break
             query = [q]
+    elif cfg in (6, 7):  # disjoint boxes: distinct cells of a 16 x 16 grid, a random sub-box in each
+        cells = rng.choice(256, size=M, replace=False)
+        recs = np.zeros((M, 4), np.uint64)
+        for i, c in enumerate(cells):
+            row = []
+            for a, cell in enumerate((int(c) % 16, int(c) // 16)):
+                side = int(rng.integers(256, 4097))
+                lo = cell * 4096 + int(rng.integers(0, 4096 - side + 1))
+                row += [lo, lo + side - 1]
+            recs[i] = [row[0], row[1], row[2], row[3]]
+        if bool(rng.integers(0, 4)) if hits is None else hits > 0:  # hit with probability 3/4
+            k = int(rng.integers(0, M))
+            forced = [k]
+            query = [int(rng.integers(recs[k][0], recs[k][1] + 1)), int(rng.integers(recs[k][2], recs[k][3] + 1))]
+        else:
+            while True:
+                query = [int(rng.integers(0, top)), int(rng.integers(0, top))]
+                if not any(r[0] <= query[0] <= r[1] and r[2] <= query[1] <= r[3] for r in recs.tolist()):
+                    break
+    elif cfg in (8, 9):  # distinct points (CoV, d = 2) or distinct ids (IdM)
+        W = 2 if cfg == 8 else 1
+        flat = rng.choice(top ** W, size=M, replace=False)
+        recs = np.array([[(int(v) >> (16 * a)) & (top - 1) for a in range(W)] for v in flat], np.uint64)
+        if bool(rng.integers(0, 4)) if hits is None else hits > 0:
+            k = int(rng.integers(0, M))
+            forced = [k]
+            query = [int(v) for v in recs[k]]
+        else:
+            seen = set(tuple(int(v) for v in r) for r in recs)
+            while True:
+                query = [int(rng.integers(0, top)) for _ in range(W)]
+                if tuple(query) not in seen:
+                    break
     else:
         raise ValueError(f"config {cfg} is not a circuit config")
     return Workload(cfg, mode, M, l_I, l_S, d, flags, query, recs, payloads, key_seed, data_seed, forced)

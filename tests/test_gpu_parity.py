@@ -417,3 +417,18 @@ def test_single_record_min_width_full_parity(server):
     result), the minimum comparator width l_I = 2 and a 1-bit payload."""
     want = _full_parity_small(server, OC.MODE_INTV, 1, 2, 1, OC.CONFIG_FLAGS, [(1, 3)], [1], [2])
     assert want == 1
+
+
+@pytest.mark.parametrize("cfg", [6, 7, 8, 9])
+def test_dataset_shapes_predicate(server, cfg):
+    """Synthetic stand-ins with the shapes of the paper's datasets (covid-kor / covid-usa IntV rectangles,
+    gdacs CoV points, weather-usa IdM with a 128-bit payload): the decrypted answer equals the plain
+    predicate; for the gdacs shape, record 0's validation bit and masked payload are byte-equal to the oracle."""
+    sample = [0] if cfg == 8 else []
+    wl = make_workload(cfg, key_seed=SEED)
+    if sample:
+        _full_size_sampled(server, cfg, sample)
+        return
+    prog, q, db, out = _run_config(server, wl)
+    want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+    assert server.keys.decrypt_value(out) == want
