@@ -162,15 +162,15 @@ __host__ __device__ constexpr uint32_t cC(int r) { return static_cast<uint32_t>(
 typedef uint32_t Poly3[3][8];
 
 // Stages 0-2 (layout A): pair (r, r | rb), rb = 4 >> s; twiddle k = 2^s + (r >> (3 - s)), uniform.
-template <int S, bool INV>
-__device__ __forceinline__ void stage_A(Poly3& d, Rc z) {
+template <int S, bool INV, int NP>
+__device__ __forceinline__ void stage_A(uint32_t (&d)[NP][8], Rc z) {
   constexpr int rb = 4 >> S;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
     if (r & rb) continue;
     const uint2 w = c_tw[INV][(1 << S) + (r >> (3 - S))];
 #pragma unroll
-    for (int p = 0; p < 3; p++) {
+    for (int p = 0; p < NP; p++) {
       if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
       else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
     }
@@ -179,8 +179,8 @@ __device__ __forceinline__ void stage_A(Poly3& d, Rc z) {
 
 // Lane-varying stages 3-8: layout B (S = 3..5) or C (S = 6..8); rb = 4 >> (S % 3); twiddle slot
 // q = r >> (3 - S % 3) at table row kSlotBase[S] + q, column t.
-template <int S, bool INV>
-__device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl, Rc z) {
+template <int S, bool INV, int NP>
+__device__ __forceinline__ void stage_BC(uint32_t (&d)[NP][8], const uint2* __restrict__ twl, Rc z) {
   constexpr int rb = 4 >> (S % 3);
   constexpr int base = S == 3 ? 0 : S == 4 ? 1 : S == 5 ? 3 : S == 6 ? 7 : S == 7 ? 8 : 10;
 #pragma unroll
@@ -188,7 +188,7 @@ __device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl
     if (r & rb) continue;
     const uint2 w = __ldg(twl + (base + (r >> (3 - S % 3))) * kBT);
 #pragma unroll
-    for (int p = 0; p < 3; p++) {
+    for (int p = 0; p < NP; p++) {
       if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
       else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
     }
@@ -197,13 +197,14 @@ __device__ __forceinline__ void stage_BC(Poly3& d, const uint2* __restrict__ twl
 
 // Stage 9 forward: lane-pair exchange (lower lane keeps pairs r = 0..3, upper lane r = 4..7), then
 // butterflies on (d[i], d[4+i]) with twiddle slots 14..17.
-__device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __restrict__ twl, Rc z) {
+template <int NP>
+__device__ __forceinline__ void stage9_fwd(uint32_t (&d)[NP][8], uint32_t t, const uint2* __restrict__ twl, Rc z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const uint2 w = __ldg(twl + (14 + i) * kBT);
 #pragma unroll
-    for (int p = 0; p < 3; p++) {
+    for (int p = 0; p < NP; p++) {
       const uint32_t send = lo ? d[p][4 + i] : d[p][i];
       const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
       uint32_t x = lo ? d[p][i] : recv;
@@ -216,13 +217,14 @@ __device__ __forceinline__ void stage9_fwd(Poly3& d, uint32_t t, const uint2* __
 }
 
 // Stage 9 inverse: butterflies on (d[i], d[4+i]), then the reverse lane-pair exchange (back to layout C).
-__device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __restrict__ twl, Rc z) {
+template <int NP>
+__device__ __forceinline__ void stage9_inv(uint32_t (&d)[NP][8], uint32_t t, const uint2* __restrict__ twl, Rc z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const uint2 w = __ldg(twl + (14 + i) * kBT);
 #pragma unroll
-    for (int p = 0; p < 3; p++) {
+    for (int p = 0; p < NP; p++) {
       gs_bfly(d[p][i], d[p][4 + i], w.x, w.y, z);
       const uint32_t send = lo ? d[p][4 + i] : d[p][i];
       const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
@@ -232,19 +234,20 @@ __device__ __forceinline__ void stage9_inv(Poly3& d, uint32_t t, const uint2* __
   }
 }
 
-// Layout change of 3 polynomials through shared memory (xb: 3 x 1024 words of this bootstrap).
-template <int FROM, int TO>
-__device__ __forceinline__ void exchange(Poly3& d, uint32_t* xb, uint32_t t, uint32_t g) {
+// Layout change of NP polynomials through shared memory (xb: NP x 1024 words; named barrier g + 1 over the
+// 128 threads that own them).
+template <int FROM, int TO, int NP>
+__device__ __forceinline__ void exchange(uint32_t (&d)[NP][8], uint32_t* xb, uint32_t t, uint32_t g) {
   const uint32_t bs = FROM == 0 ? baseA(t) : (FROM == 1 ? baseB(t) : baseC(t));
   const uint32_t bd = TO == 0 ? baseA(t) : (TO == 1 ? baseB(t) : baseC(t));
   bar_boot(g);
 #pragma unroll
-  for (int q = 0; q < 3; q++)
+  for (int q = 0; q < NP; q++)
 #pragma unroll
     for (int r = 0; r < 8; r++) xb[q * N + (bs ^ (FROM == 0 ? cA(r) : (FROM == 1 ? cB(r) : cC(r))))] = d[q][r];
   bar_boot(g);
 #pragma unroll
-  for (int q = 0; q < 3; q++)
+  for (int q = 0; q < NP; q++)
 #pragma unroll
     for (int r = 0; r < 8; r++) d[q][r] = xb[q * N + (bd ^ (TO == 0 ? cA(r) : (TO == 1 ? cB(r) : cC(r))))];
 }
@@ -498,6 +501,255 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kTmemCols) : "memory");
 }
 
+
+// ================================================================================ K2-LAT (latency mode)
+// One bootstrap per CTA for the narrow tail of a level (<= one bootstrap per SM): its 3 gadget digits (forward
+// rounds) and its 3 key limbs (inverse rounds) run on 3 warp groups of 128 threads, so each warp transforms 1
+// polynomial per round instead of 3.  The groups meet through TMEM: thread t of every group owns TMEM lane t
+// (warp 4G + t/32 sits in quadrant t/32), so the transformed digits (columns 8(3u + j) + s) and the lifted
+// limbs (48 + 8(3u + l) + r) written by one group are read by the others after a CTA barrier.  Group G
+// computes the MAC outputs of limb G (u_out = 0, 1).  Same arithmetic, layouts, key and bytes as the
+// throughput kernel.
+constexpr int kLatThreads = 3 * kBT;
+constexpr int kLatTmemCols = 128;
+__host__ __device__ constexpr int lat_smem_bytes() {
+  return kSlots * kChunkBytes + (2 * N * 4 + 6 * N * 4 + 640 * 2) + kSlots * 8 + kSlots * 4 + 8;
+}
+
+__global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(const BrArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* ring = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* acc = ring + kSlots * kBT * kChunkWords;
+  uint32_t* xb_all = acc + 2 * N;  // [group 3][2 polys][N]
+  uint16_t* abar = reinterpret_cast<uint16_t*>(xb_all + 6 * N);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(abar + 640);
+  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kSlots);
+  uint32_t* tmem_base_sh = rel + kSlots;
+
+  const uint32_t tid = threadIdx.x, G = tid / kBT, t = tid % kBT;
+  uint32_t* xb = xb_all + G * 2 * N;
+  const uint2* twf = a.twl_fwd + t;
+  const uint2* twi = a.twl_inv + t;
+  const Rc zr{a.zero, a.p2};
+  if (blockIdx.x >= a.njobs) return;
+  const uint32_t my_jobs = (a.njobs - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const uint32_t total_chunks = my_jobs * static_cast<uint32_t>(a.steps) * kChunks;
+
+  if (tid == 0) {
+    for (int s = 0; s < kSlots; s++) {
+      mbar_init(&mbar[s], 1);
+      rel[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "n"(kLatTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = *tmem_base_sh + ((32u * ((tid >> 5) & 3u)) << 16);  // lane t of every group
+
+  auto issue = [&](uint32_t nseq) {
+    const uint32_t step = (nseq / kChunks) % static_cast<uint32_t>(a.steps), c = nseq % kChunks;
+    const uint32_t s = nseq % kSlots;
+    bulk_load(ring + s * kBT * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * kBT * kChunkWords,
+              kChunkBytes, &mbar[s]);
+  };
+  if (tid == 0)
+    for (uint32_t q = 0; q < kSlots && q < total_chunks; q++) issue(q);
+  uint32_t nseq = 0, sl = 0, ph = 0;
+  auto cta_sync_tmem = [&]() {  // TMEM writes of one group -> reads of another
+    tmem_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  };
+
+  for (uint32_t jb = blockIdx.x; jb < a.njobs; jb += gridDim.x) {
+    // ---- S2 gate linear form + S3 mod-switch
+    {
+      const BrJob job = a.jobs[jb];
+      const uint32_t* x = slot_ptr(a.reg, job.x);
+      const uint32_t* y = slot_ptr(a.reg, job.y);
+      for (uint32_t w = tid; w <= static_cast<uint32_t>(n); w += kLatThreads) {
+        uint32_t c = static_cast<uint32_t>(static_cast<int32_t>(job.ax)) * x[w];
+        if (job.ay) c += static_cast<uint32_t>(static_cast<int32_t>(job.ay)) * y[w];
+        if (w == static_cast<uint32_t>(n)) c += job.k0;
+        abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
+      }
+    }
+    __syncthreads();
+    // ---- S4 accumulator init (R8)
+    {
+      const uint32_t bbar = abar[n];
+      for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kLatThreads) {
+        acc[k] = 0;
+        acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu);
+      }
+    }
+    __syncthreads();
+
+    // ---- S5: CMux steps
+    const uint32_t dshift = 25u - 7u * G;  // gadget digit G (R5)
+    for (int i = 0; i < a.steps; i++) {
+      const uint32_t ab = abar[i];
+      {  // digit G of both components, transformed together (2 polynomials per thread)
+        uint32_t d[2][8];
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+          for (int r = 0; r < 8; r++) {
+            const uint32_t j = t + 128u * r;
+            const uint32_t kk = (j - ab) & (2 * N - 1);
+            uint32_t v = acc[u * N + (kk & (N - 1))];
+            v = kk >= static_cast<uint32_t>(N) ? zr.z - v : v;
+            const uint32_t w = v - acc[u * N + j] + 0x81020400u;
+            d[u][r] = ((w >> dshift) & 127u) + (P - 64u);
+          }
+        stage_A<0, false>(d, zr);
+        stage_A<1, false>(d, zr);
+        stage_A<2, false>(d, zr);
+        exchange<0, 1>(d, xb, t, G);
+        stage_BC<3, false>(d, twf, zr);
+        stage_BC<4, false>(d, twf, zr);
+        stage_BC<5, false>(d, twf, zr);
+        exchange<1, 2>(d, xb, t, G);
+        stage_BC<6, false>(d, twf, zr);
+        stage_BC<7, false>(d, twf, zr);
+        stage_BC<8, false>(d, twf, zr);
+        stage9_fwd(d, t, twf, zr);
+        tmem_st8(tm + 8 * G, d[0]);        // transformed digit (0, G)
+        tmem_st8(tm + 8 * (3 + G), d[1]);  // transformed digit (1, G)
+      }
+      cta_sync_tmem();
+      // MAC for limb G of both output components: o = G (u_out 0) and 3 + G (u_out 1)
+      uint32_t mac[2][8];
+#pragma unroll
+      for (int pp = 0; pp < kChunks; pp++) {
+        uint32_t xr[6][2];
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                       : "=r"(xr[q][0]), "=r"(xr[q][1])
+                       : "r"(tm + 8 * q + 2 * pp)
+                       : "memory");
+        }
+        tmem_wait_ld();
+        uint32_t x[2][6];
+#pragma unroll
+        for (int e = 0; e < 2; e++)
+#pragma unroll
+          for (int q = 0; q < 6; q++) {
+            uint32_t v = umin(xr[q][e], xr[q][e] - P2);
+            x[e][q] = umin(v, v - P);
+          }
+        mbar_wait(&mbar[sl], ph);
+        const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
+#pragma unroll
+        for (int oi = 0; oi < 2; oi++) {
+          const uint4* kp = reinterpret_cast<const uint4*>(rec + (3 * oi + G) * 12);  // [e 2][q 6]
+          const uint4 k0 = kp[0], k1 = kp[1], k2 = kp[2];
+          const uint32_t kv[2][6] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y}, {k1.z, k1.w, k2.x, k2.y, k2.z, k2.w}};
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            uint64_t T = static_cast<uint64_t>(x[e][0]) * kv[e][0];
+#pragma unroll
+            for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(x[e][q]) * kv[e][q];
+            const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
+            mac[oi][2 * pp + e] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
+          }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) {
+          __threadfence_block();
+          if (atomicAdd(&rel[sl], 1u) == kLatThreads / 32 - 1) {
+            atomicExch(&rel[sl], 0u);
+            if (nseq + kSlots < total_chunks) {
+              fence_proxy_async();
+              issue(nseq + kSlots);
+            }
+          }
+        }
+        nseq++;
+        if (++sl == kSlots) {
+          sl = 0;
+          ph ^= 1u;
+        }
+      }
+      // inverse NTT of limb G of both components, centered lift, park in TMEM
+      {  // inverse NTT of limb G of both components together, centered lift, park in TMEM
+        uint32_t d[2][8];
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+          for (int s = 0; s < 8; s++) d[u][s] = umin(mac[u][s], mac[u][s] - P2);
+        stage9_inv(d, t, twi, zr);
+        stage_BC<8, true>(d, twi, zr);
+        stage_BC<7, true>(d, twi, zr);
+        stage_BC<6, true>(d, twi, zr);
+        exchange<2, 1>(d, xb, t, G);
+        stage_BC<5, true>(d, twi, zr);
+        stage_BC<4, true>(d, twi, zr);
+        stage_BC<3, true>(d, twi, zr);
+        exchange<1, 0>(d, xb, t, G);
+        stage_A<2, true>(d, zr);
+        stage_A<1, true>(d, zr);
+        stage_A<0, true>(d, zr);
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+          for (int r = 0; r < 8; r++) {
+            const uint32_t v = umin(d[u][r], d[u][r] - P);
+            d[u][r] = v > (P >> 1) ? v - P : v;  // centered, two's complement
+          }
+        tmem_st8(tm + 48 + 8 * G, d[0]);
+        tmem_st8(tm + 48 + 8 * (3 + G), d[1]);
+      }
+      cta_sync_tmem();
+      // recombine R0 + 2^11 R1 + 2^22 R2 and acc_u += (layout A: j = t + 128 r); group G takes r = G, G+3, G+6
+      {
+        uint32_t lv[2][3][8];
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+          for (int l = 0; l < 3; l++) tmem_ld8(tm + 48 + 8 * (3 * u + l), lv[u][l]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+          for (int r = 0; r < 8; r++) {
+            if (static_cast<uint32_t>(r % 3) != G) continue;
+            const uint32_t hi = __funnelshift_l(0u, lv[u][1][r], 11) + __funnelshift_l(0u, lv[u][2][r], 22) + zr.z;
+            uint32_t& av = acc[u * N + t + 128u * r];
+            av = add_alu(av, lv[u][0][r], hi);
+          }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();  // acc complete before the next step's digit gather
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+
+    // ---- S6 SampleExtract
+    if (a.raw_acc) {
+      uint32_t* o = a.raw_acc + static_cast<size_t>(jb) * 2 * N;
+      for (uint32_t k = tid; k < 2u * N; k += kLatThreads) o[k] = acc[k];
+    } else {
+      uint32_t* o = a.nlwe + static_cast<size_t>(a.jobs[jb].out) * kNlwe;
+      for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kLatThreads) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+      if (tid == 0) o[N] = acc[N];
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kLatTmemCols) : "memory");
+}
+
 // ================================================================================ K3' key switch on tensor cores
 // (a) one-hot digit indicator: CTA per ciphertext; coefficient i -> 24 bytes ind[c][i*24 + j*3 + v-1].
 //     MUX combine (S7) and the 16-bit rounding (R6) in the prologue, as in K3.
@@ -667,8 +919,31 @@ static cudaError_t launch_br_b(const BrArgs& a, int sm_count, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static cudaError_t launch_br_lat(const BrArgs& a, int sm_count, cudaStream_t st) {
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    e = cudaFuncSetAttribute(vlp_blind_rotate_lat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lat_smem_bytes());
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit);
+  }
+  if (a.njobs == 0) return cudaSuccess;
+  const int grid = static_cast<int>(a.njobs < static_cast<uint32_t>(sm_count) ? a.njobs : sm_count);
+  if ((static_cast<uint64_t>(a.njobs) + grid - 1) / grid * static_cast<uint64_t>(a.steps) * kChunks >= (1ull << 32))
+    return cudaErrorInvalidValue;
+  BrArgs b = a;
+  b.zero = 0;
+  b.p2 = P2;
+  vlp_blind_rotate_lat_kernel<<<grid, kLatThreads, lat_smem_bytes(), st>>>(b);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_br_width(const BrArgs& a, int B, int sm_count, cudaStream_t st) {
   switch (B) {
+    case 0: return launch_br_lat(a, sm_count, st);
     case 1: return launch_br_b<1>(a, sm_count, st);
     case 2: return launch_br_b<2>(a, sm_count, st);
     case 3: return launch_br_b<3>(a, sm_count, st);
@@ -691,7 +966,7 @@ static int forced_boot() {
 
 int br_launch_count(uint32_t njobs, int sm_count) {
   if (njobs == 0) return 0;
-  if (forced_boot() >= 1 && forced_boot() <= kBrBoot) return 1;
+  if ((forced_boot() >= 1 && forced_boot() <= kBrBoot) || forced_boot() == -1) return 1;
   const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
   return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
 }
@@ -700,6 +975,7 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
   if (a.njobs == 0) return cudaSuccess;
   const int forced = forced_boot();
   if (forced >= 1 && forced <= kBrBoot) return launch_br_width(a, forced, sm_count, st);
+  if (forced == -1) return launch_br_width(a, 0, sm_count, st);  // VLP_BR_BOOT=-1: latency mode
   const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
   const uint32_t full = a.njobs / wave * wave, tail = a.njobs - full;
   cudaError_t e = cudaSuccess;
@@ -713,7 +989,8 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
     r.jobs = a.jobs + full;
     r.njobs = tail;
     if (r.raw_acc) r.raw_acc = a.raw_acc + static_cast<size_t>(full) * 2 * N;
-    const int b = static_cast<int>((tail + sm_count - 1) / sm_count);
+    // a tail of at most one bootstrap per SM runs in latency mode (3 warp groups per bootstrap)
+    const int b = tail <= static_cast<uint32_t>(sm_count) ? 0 : static_cast<int>((tail + sm_count - 1) / sm_count);
     e = launch_br_width(r, b, sm_count, st);
   }
   return e;
