@@ -27,7 +27,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from synth import make_workload, nand_inputs  # noqa: E402
-from synth.workloads import expected_result  # noqa: E402
+from synth.workloads import expected_result, extra_queries  # noqa: E402
 
 METRIC = "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
 UNIT = "gate bootstraps/s"
@@ -235,6 +235,8 @@ def main():
                     help="1-4: BASELINE.json configs; 5: NAND sweep; 6-9: synthetic stand-ins shaped like the paper's "
                          "datasets (covid-kor, covid-usa, gdacs, weather-usa; synth/workloads.py)")
     ap.add_argument("--nand", type=int, default=1 << 17, help="config 5: NAND gates per step (split over ranks)")
+    ap.add_argument("--queries", type=int, default=1,
+                    help="queries per step (multi-query packing on one GPU: every level launch carries all of them)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -271,13 +273,17 @@ def main():
     per = A.record_cts(m)
     db = A.to_device(keys.encrypt_db(m, wl.records[first:first + shard], wl.payloads[first:first + shard],
                                      pk_seed=wl.key_seed + 1, first=first, count=shard), local)
-    q_host = keys.encrypt_query(m, wl.query, 7)
+    nq = args.queries
+    if nq > 1 and world > 1:
+        raise SystemExit("--queries > 1 is single-GPU (multi-query packing of one shard)")
+    qvals = [list(wl.query)] + extra_queries(wl, nq - 1)
+    q_host = np.concatenate([keys.encrypt_query(m, qv, 7 + i) for i, qv in enumerate(qvals)])
     q = A.to_device(q_host, local)
-    prog = A.Program.velopir(srv, m, first, shard)
+    prog = A.Program.velopir(srv, m, first, shard) if nq == 1 else A.Program.queries(srv, m, nq)
     comb = A.Program.combine(srv, m, world) if (world > 1 and rank == 0) else None
     part = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
     gathered = torch.zeros((world * wl.l_S, 632), dtype=torch.int32, device=dev) if world > 1 else None
-    out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
+    out = torch.zeros((nq * wl.l_S, 632), dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     setup_s = time.time() - t_setup
 
@@ -298,10 +304,16 @@ def main():
     if world > 1:
         dist.barrier()
     # correctness of the measured computation
-    want = expected_result(wl)
+    wants = [expected_result(wl, qv) for qv in qvals]
+    want = wants[0]
+
+    def check_all(res):
+        for i in range(nq):
+            got = keys.decrypt_value(res[i * wl.l_S:(i + 1) * wl.l_S])
+            assert got == wants[i], f"query {i}: wrong result {got} != {wants[i]}"
+
     if rank == 0:
-        got = keys.decrypt_value(A.to_host(out))
-        assert got == want, f"wrong result {got} != {want}"
+        check_all(A.to_host(out))
 
     # ---- timed region: K steps, L2 flushed between steps (untimed), per-step CUDA events
     sampler = ClockSampler(local) if rank == 0 else None
@@ -329,19 +341,22 @@ def main():
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms = float(tot.item())
     ms_per_step = total_ms / args.steps
-    br_per_query = CONFIG_BR.get(args.config) or prog.info.br * world + (comb.info.br if comb else 0)
-    value = br_per_query / (ms_per_step / 1e3)
-    records_per_s = wl.M / (ms_per_step / 1e3)
+    br_per_query = CONFIG_BR.get(args.config) or prog.info.br // nq * world + (comb.info.br if comb else 0)
+    value = nq * br_per_query / (ms_per_step / 1e3)
+    records_per_s = nq * wl.M / (ms_per_step / 1e3)
 
     # ---- e2e: query H2D from pinned host memory + server_eval (+ combine) + result D2H, every step, through
     # the problem-statement calls a user makes (vlp_server_eval / vlp_server_combine)
     e2e = None
     if not args.no_e2e:
         q_pin = torch.from_numpy(q_host.view(np.int32)).pin_memory()
-        out_pin = torch.empty((wl.l_S, 632), dtype=torch.int32).pin_memory()
+        out_pin = torch.empty((nq * wl.l_S, 632), dtype=torch.int32).pin_memory()
         qd = torch.empty_like(q)
 
         def eval_api(qdev):
+            if nq > 1:
+                srv.eval_batch(m, qdev, db, out, nq, stream=stream)
+                return out
             srv.eval(m, qdev, db, part if world > 1 else out, first=first, count=shard, stream=stream)
             return part if world > 1 else out
 
@@ -371,9 +386,9 @@ def main():
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_ms = float(et.item()) / args.steps
         if rank == 0:
-            assert keys.decrypt_value(out_pin.numpy().view(np.uint32)) == want
-        e2e = {"value": br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": wl.M / (e2e_ms / 1e3),
-               "h2d_bytes_per_step": int(q_host.nbytes), "d2h_bytes_per_step": int(wl.l_S * 632 * 4)}
+            check_all(out_pin.numpy().view(np.uint32))
+        e2e = {"value": nq * br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": nq * wl.M / (e2e_ms / 1e3),
+               "h2d_bytes_per_step": int(q_host.nbytes), "d2h_bytes_per_step": int(nq * wl.l_S * 632 * 4)}
 
     if rank == 0:
         peak, peak_how = int_peak()
@@ -386,9 +401,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "records_per_s": records_per_s, "ks_per_s": (prog.info.ks * world + (comb.info.ks if comb else 0)) / (ms_per_step / 1e3),
+            "records_per_s": records_per_s, "ks_per_s": (prog.info.ks * world + (comb.info.ks if comb else 0)) / (ms_per_step / 1e3),  # all queries
             "config": {"workload": f"cfg{args.config}_{wl.name}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S,
-                       "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels,
+                       "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels, "queries_per_step": nq,
                        "parallelism": f"records sharded x{world}" if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)",
                        "params": "TFHE n=630 N=1024 Bg=2^7 l=3 ks 2^2x8 (tab:tfhe_params)"},

@@ -148,6 +148,12 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
  * `server` may be NULL to compile only (vlp_program_get_info works; vlp_program_eval fails). */
 int vlp_program_create(vlp_server* server, const vlp_meta* meta, size_t first, size_t count,
                        vlp_program** out);
+/* Multi-query packing: nq queries against the same shard in one schedule, so every
+ * level launch carries the gates of all nq queries.  in0 = nq query sets back to back ([nq][query cts]),
+ * out = [nq][l_S] result ciphertexts; each query's result is byte-identical to its single-query evaluation
+ * (ciphertexts do not depend on the schedule).  nq in [1, 4096]. */
+int vlp_program_create_queries(vlp_server* server, const vlp_meta* meta, size_t first, size_t count, uint32_t nq,
+                               vlp_program** out);
 /* A single level of `count` independent gates `op` (config 5): out[i] = op(in0[i], in1[i]); for
  * VLP_MUX, out[i] = MUX(in0[i], in1[i], in2[i]) where in2 = in1 + count rows. */
 int vlp_program_create_gates(vlp_server* server, int op, size_t count, vlp_program** out);
@@ -200,6 +206,12 @@ int vlp_server_workspace_bytes(const vlp_meta* meta, size_t count, size_t* evk_b
 int vlp_server_eval(vlp_server* server, const vlp_meta* meta, size_t first, size_t count,
                     const uint32_t* query_dev, const uint32_t* db_dev, uint32_t* out_dev, void* scratch_dev,
                     size_t scratch_bytes, uint64_t stream);
+/* server_eval for nq queries at once (multi-query packing): queries_dev [nq][query cts][632],
+ * out_dev [nq][l_S][632]; scratch from vlp_server_batch_workspace_bytes. */
+int vlp_server_batch_workspace_bytes(const vlp_meta* meta, size_t count, uint32_t nq, size_t* scratch_bytes);
+int vlp_server_eval_batch(vlp_server* server, const vlp_meta* meta, uint32_t nq, size_t first, size_t count,
+                          const uint32_t* queries_dev, const uint32_t* db_dev, uint32_t* out_dev, void* scratch_dev,
+                          size_t scratch_bytes, uint64_t stream);
 /* Scratch bytes of vlp_server_combine for G shard roots. */
 int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t* scratch_bytes);
 /* The top log2(G) XOR-tree levels over the G shard roots partials_dev [G][l_S][632] (rank order, G a power

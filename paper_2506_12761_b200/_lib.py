@@ -60,6 +60,7 @@ SIGNATURES = {
     "vlp_server_evk_bytes": (_sz, []),
     "vlp_server_create": (_i, [_i, _vp, _vp, _sz, _u64, _pp]),
     "vlp_program_create": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _pp]),
+    "vlp_program_create_queries": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, ctypes.c_uint32, _pp]),
     "vlp_program_create_gates": (_i, [_vp, _i, _sz, _pp]),
     "vlp_program_create_combine": (_i, [_vp, ctypes.POINTER(VlpMeta), ctypes.c_uint32, _pp]),
     "vlp_program_get_info": (_i, [_vp, ctypes.POINTER(VlpProgramInfo)]),
@@ -75,6 +76,10 @@ SIGNATURES = {
     "vlp_server_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t),
                                         ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_server_eval": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _vp, _vp, _vp, _vp, _sz, _u64]),
+    "vlp_server_batch_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.c_uint32,
+                                              ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_server_eval_batch": (_i, [_vp, ctypes.POINTER(VlpMeta), ctypes.c_uint32, _sz, _sz, _vp, _vp, _vp, _vp, _sz,
+                                   _u64]),
     "vlp_server_combine_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), ctypes.c_uint32,
                                                 ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_server_combine": (_i, [_vp, ctypes.POINTER(VlpMeta), ctypes.c_uint32, _vp, _vp, _vp, _sz, _u64]),

@@ -163,6 +163,21 @@ class Server:
                                     ctypes.c_void_p(db_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
                                     ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream)))
 
+    def eval_batch(self, m: VlpMeta, queries_dev, db_dev, out_dev, nq: int, first: int = 0,
+                   count: int | None = None, stream=None):
+        """Multi-query packing: nq queries (queries_dev [nq * query cts, 632]) -> out_dev [nq * l_S, 632]."""
+        count = m.M - first if count is None else count
+        key = ("batch", bytes(m), first, count, nq)
+        if key not in self.__dict__.setdefault("_ws", {}):
+            sb = ctypes.c_size_t()
+            check(lib().vlp_server_batch_workspace_bytes(ctypes.byref(m), count, nq, ctypes.byref(sb)))
+            self._ws[key] = sb.value
+        sc = self._scratch(key, self._ws[key])
+        check(lib().vlp_server_eval_batch(self.h, ctypes.byref(m), nq, first, count,
+                                          ctypes.c_void_p(queries_dev.data_ptr()), ctypes.c_void_p(db_dev.data_ptr()),
+                                          ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(sc.data_ptr()),
+                                          sc.numel(), _stream_handle(stream)))
+
     def combine(self, m: VlpMeta, G: int, partials_dev, out_dev, stream=None):
         key = ("combine", bytes(m), G)
         if key not in self.__dict__.setdefault("_ws", {}):
@@ -225,6 +240,13 @@ class Program:
         count = m.M - first if count is None else count
         h = ctypes.c_void_p()
         check(lib().vlp_program_create(server.h, ctypes.byref(m), first, count, ctypes.byref(h)))
+        return cls(server, h)
+
+    @classmethod
+    def queries(cls, server: Server, m: VlpMeta, nq: int, first: int = 0, count: int | None = None):
+        count = m.M - first if count is None else count
+        h = ctypes.c_void_p()
+        check(lib().vlp_program_create_queries(server.h, ctypes.byref(m), first, count, nq, ctypes.byref(h)))
         return cls(server, h)
 
     @classmethod

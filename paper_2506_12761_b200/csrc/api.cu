@@ -319,6 +319,14 @@ int vlp_program_create(vlp_server* server, const vlp_meta* meta, size_t first, s
   return finish_program(server, p, out);
 }
 
+int vlp_program_create_queries(vlp_server* server, const vlp_meta* meta, size_t first, size_t count, uint32_t nq,
+                               vlp_program** out) {
+  if (!meta || !out) return fail(VLP_EINVAL, "null argument");
+  auto p = std::make_unique<vlp_program>();
+  if (int rc = compile_velopir(*meta, first, count, &p->sched, nq)) return rc;
+  return finish_program(server, p, out);
+}
+
 int vlp_program_create_gates(vlp_server* server, int op, size_t count, vlp_program** out) {
   if (!out) return fail(VLP_EINVAL, "null argument");
   auto p = std::make_unique<vlp_program>();
@@ -568,6 +576,27 @@ int vlp_server_eval(vlp_server* s, const vlp_meta* meta, size_t first, size_t co
                               [&](vlp_program** o) { return vlp_program_create(s, meta, first, count, o); }, &p))
     return rc;
   return vlp_program_eval(p, scratch, scratch_bytes, query_dev, db_dev, out_dev, stream);
+}
+
+int vlp_server_batch_workspace_bytes(const vlp_meta* meta, size_t count, uint32_t nq, size_t* scratch_bytes) {
+  if (!meta || !scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  vlp_program* p = nullptr;
+  if (int rc = vlp_program_create_queries(nullptr, meta, 0, count, nq, &p)) return rc;
+  *scratch_bytes = p->bytes;
+  delete p;
+  return VLP_OK;
+}
+
+int vlp_server_eval_batch(vlp_server* s, const vlp_meta* meta, uint32_t nq, size_t first, size_t count,
+                          const uint32_t* queries_dev, const uint32_t* db_dev, uint32_t* out_dev, void* scratch,
+                          size_t scratch_bytes, uint64_t stream) {
+  if (!s || !meta) return fail(VLP_EINVAL, "null argument");
+  vlp_program* p = nullptr;
+  if (int rc = cached_program(s, meta_key("batch", *meta, first, count) + "," + std::to_string(nq),
+                              [&](vlp_program** o) { return vlp_program_create_queries(s, meta, first, count, nq, o); },
+                              &p))
+    return rc;
+  return vlp_program_eval(p, scratch, scratch_bytes, queries_dev, db_dev, out_dev, stream);
 }
 
 int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t* scratch_bytes) {

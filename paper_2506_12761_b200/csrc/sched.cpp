@@ -190,35 +190,47 @@ Word aggregate(Builder& B, std::vector<Word> S, size_t l_S, uint32_t flags) {
 
 }  // namespace
 
-int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s) {
+int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, uint32_t nq) {
   if (int rc = check_meta(&m)) return rc;
   if (count == 0 || first + count > m.M) return fail(VLP_EINVAL, "bad record range");
+  if (nq < 1 || nq > 4096) return fail(VLP_EINVAL, "query count must be in [1, 4096]");
   Builder B;
   const size_t l = m.l_I, W = record_words(m), QW = query_words(m), per = W * l + m.l_S;
-  std::vector<Word> q(QW, Word(l));
-  for (size_t w = 0; w < QW; w++)
-    for (size_t j = 0; j < l; j++) q[w][j] = B.leaf(slot(kRegIn0, static_cast<uint32_t>(w * l + j)));
-  std::vector<Word> masked(count);
-  std::vector<uint32_t> vs(count);
-  for (size_t r = 0; r < count; r++) {  // alg:VeLoPIR record loop
+  // the shard's record ciphertexts are shared by all nq queries (multi-query packing)
+  std::vector<std::vector<Word>> recs(count, std::vector<Word>(W, Word(l)));
+  std::vector<Word> pays(count, Word(m.l_S));
+  for (size_t r = 0; r < count; r++) {
     const uint32_t base = static_cast<uint32_t>(r * per);
-    std::vector<Word> rec(W, Word(l));
     for (size_t k = 0; k < W; k++)
-      for (size_t j = 0; j < l; j++) rec[k][j] = B.leaf(slot(kRegIn1, base + static_cast<uint32_t>(k * l + j)));
-    const uint32_t v = validate(B, m, q, rec);
-    vs[r] = v;
-    masked[r].resize(m.l_S);
-    for (size_t j = 0; j < m.l_S; j++)  // alg:HomBitwiseAND with the record's own v (R16)
-      masked[r][j] = B.AND(v, B.leaf(slot(kRegIn1, base + static_cast<uint32_t>(W * l + j))));
+      for (size_t j = 0; j < l; j++) recs[r][k][j] = B.leaf(slot(kRegIn1, base + static_cast<uint32_t>(k * l + j)));
+    for (size_t j = 0; j < m.l_S; j++) pays[r][j] = B.leaf(slot(kRegIn1, base + static_cast<uint32_t>(W * l + j)));
   }
-  const Word root = aggregate(B, masked, m.l_S, m.flags);
-  B.finalize(root, s);
-  s->in0_cts = QW * l;
+  Word outs;
+  std::vector<uint32_t> vs(count);
+  std::vector<Word> masked0;
+  for (uint32_t qi = 0; qi < nq; qi++) {
+    std::vector<Word> q(QW, Word(l));
+    for (size_t w = 0; w < QW; w++)
+      for (size_t j = 0; j < l; j++)
+        q[w][j] = B.leaf(slot(kRegIn0, static_cast<uint32_t>((qi * QW + w) * l + j)));
+    std::vector<Word> masked(count);
+    for (size_t r = 0; r < count; r++) {  // alg:VeLoPIR record loop
+      const uint32_t v = validate(B, m, q, recs[r]);
+      if (qi == 0) vs[r] = v;
+      masked[r].resize(m.l_S);
+      for (size_t j = 0; j < m.l_S; j++) masked[r][j] = B.AND(v, pays[r][j]);  // alg:HomBitwiseAND (R16)
+    }
+    const Word root = aggregate(B, masked, m.l_S, m.flags);
+    outs.insert(outs.end(), root.begin(), root.end());
+    if (qi == 0) masked0 = masked;
+  }
+  B.finalize(outs, s);
+  s->in0_cts = static_cast<uint64_t>(nq) * QW * l;
   s->in1_cts = count * per;
   s->l_S = m.l_S;
-  for (size_t r = 0; r < count; r++) {
+  for (size_t r = 0; r < count; r++) {  // parity dumps: the first query's nodes
     s->v_rows.push_back(B.nodes[vs[r]].slot);
-    for (size_t j = 0; j < m.l_S; j++) s->mask_rows.push_back(B.nodes[masked[r][j]].slot);
+    for (size_t j = 0; j < m.l_S; j++) s->mask_rows.push_back(B.nodes[masked0[r][j]].slot);
   }
   return VLP_OK;
 }

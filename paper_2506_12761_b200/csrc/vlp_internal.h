@@ -100,7 +100,7 @@ struct Schedule {
   uint32_t l_S = 0;
 };
 
-int compile_velopir(const vlp_meta& meta, size_t first, size_t count, Schedule* out);
+int compile_velopir(const vlp_meta& meta, size_t first, size_t count, Schedule* out, uint32_t nq = 1);
 int compile_gates(int op, size_t count, Schedule* out);
 int compile_combine(const vlp_meta& meta, uint32_t G, Schedule* out);
 

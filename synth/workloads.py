@@ -184,19 +184,35 @@ def nand_inputs(count: int, data_seed: int = 2005):
     return a, b
 
 
-def expected_result(wl: Workload) -> int:
+def extra_queries(wl: Workload, count: int, seed: int = 7):
+    """``count`` further plaintext queries for multi-query packing runs: uniform points for IntV, a random
+    record's point / id (probability 1/2) or a uniform one for CoV / IdM."""
+    rng = np.random.default_rng(seed)
+    out = []
+    top = 1 << wl.l_I
+    W = len(wl.query)
+    for _ in range(count):
+        if wl.mode != MODE_INTV and rng.integers(0, 2):
+            out.append([int(v) for v in wl.records[int(rng.integers(0, wl.M))]])
+        else:
+            out.append([int(rng.integers(0, top)) for _ in range(W)])
+    return out
+
+
+def expected_result(wl: Workload, query=None) -> int:
     """The plaintext answer the query must decrypt to (thm:VeLoPIR; R12/R13/R19): XOR (OR with
     F_OR_REDUCE) of the payloads of the records whose plaintext bounds match the query; 0 if none.
     Ground truth of the drawn inputs (used by bench.py's sanity check), not the homomorphic method."""
+    q = wl.query if query is None else query
     r = 0
     for rec, pay in zip(wl.records.tolist(), wl.payloads.tolist()):
         if wl.mode == MODE_INTV:
-            ok = all(rec[2 * a] <= wl.query[a] and (wl.query[a] <= rec[2 * a + 1] if wl.flags & F_CLOSED_UPPER
-                                                    else wl.query[a] < rec[2 * a + 1]) for a in range(wl.d))
+            ok = all(rec[2 * a] <= q[a] and (q[a] <= rec[2 * a + 1] if wl.flags & F_CLOSED_UPPER
+                                             else q[a] < rec[2 * a + 1]) for a in range(wl.d))
         elif wl.mode == MODE_COV:
-            ok = all(wl.query[a] == rec[a] for a in range(wl.d))
+            ok = all(q[a] == rec[a] for a in range(wl.d))
         else:
-            ok = wl.query[0] == rec[0]
+            ok = q[0] == rec[0]
         if ok:
             r = (r | int(pay)) if wl.flags & F_OR_REDUCE else (r ^ int(pay))
     return r

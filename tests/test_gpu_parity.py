@@ -432,3 +432,25 @@ def test_dataset_shapes_predicate(server, cfg):
     prog, q, db, out = _run_config(server, wl)
     want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
     assert server.keys.decrypt_value(out) == want
+
+
+def test_multi_query_batch_equals_single(server):
+    """Multi-query packing (vlp_server_eval_batch): 3 queries against the gdacs-shaped DB in one schedule; each
+    result is byte-equal to its own single-query vlp_server_eval and decrypts to its plain predicate."""
+    wl = make_workload(8, key_seed=SEED)
+    k = server.keys
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    db = A.to_device(k.encrypt_db(m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1))
+    qvals = [[int(v) for v in wl.records[0]], [int(v) for v in wl.records[5]], [123, 456]]
+    qs = [k.encrypt_query(m, qv, 40 + i) for i, qv in enumerate(qvals)]
+    out = torch.zeros((3 * wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    server.eval_batch(m, A.to_device(np.concatenate(qs)), db, out, 3)
+    torch.cuda.synchronize()
+    got = A.to_host(out)
+    for i, qv in enumerate(qvals):
+        one = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+        server.eval(m, A.to_device(qs[i]), db, one)
+        torch.cuda.synchronize()
+        assert np.array_equal(got[i * wl.l_S:(i + 1) * wl.l_S], A.to_host(one)), i
+        want = OC.plain_result(wl.mode, qv, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+        assert k.decrypt_value(got[i * wl.l_S:(i + 1) * wl.l_S]) == want, i

@@ -141,3 +141,18 @@ def test_shard_schedules_sum_to_whole():
     L.lib().vlp_free_program(h)
     assert sum(s.br for s in shards) + ci.br == whole.br
     assert ci.br == (G - 1) * 16 and ci.levels == 3
+
+
+def test_multi_query_schedule():
+    """Multi-query packing: nq queries against one shard -> nq x the gates of one query in the same number of
+    levels (every level launch carries all queries' gates)."""
+    m = A.meta(L.MODE_INTV, 58, 16, 22, 2)
+    one = _info(m)
+    h = ctypes.c_void_p()
+    L.check(L.lib().vlp_program_create_queries(None, ctypes.byref(m), 0, 58, 5, ctypes.byref(h)))
+    info = L.VlpProgramInfo()
+    L.check(L.lib().vlp_program_get_info(h, ctypes.byref(info)))
+    L.lib().vlp_free_program(h)
+    assert (info.br, info.ks, info.levels) == (5 * one.br, 5 * one.ks, one.levels)
+    assert info.in0_cts == 5 * one.in0_cts and info.out_cts == 5 * one.out_cts and info.in1_cts == one.in1_cts
+    assert L.lib().vlp_program_create_queries(None, ctypes.byref(m), 0, 58, 0, ctypes.byref(h)) == L.VLP_EINVAL
