@@ -454,3 +454,28 @@ def test_multi_query_batch_equals_single(server):
         assert np.array_equal(got[i * wl.l_S:(i + 1) * wl.l_S], A.to_host(one)), i
         want = OC.plain_result(wl.mode, qv, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
         assert k.decrypt_value(got[i * wl.l_S:(i + 1) * wl.l_S]) == want, i
+
+
+def test_noise_over_depth_at_scale(server):
+    """P6 at scale on the GPU path: 20 levels of AND(x, Enc(1)) over 16,384 independent chains (327,680 gate
+    bootstraps) never mis-decrypt, and the output phase error has the bootstrapped level predicted by the
+    noise model (sigma ~ 3.5e-3; band [2e-3, 5e-3]) at every depth (no growth)."""
+    k = server.keys
+    s_bits = k.export()[0]
+    s = s_bits.astype(np.int64)
+    count = 16384
+    x = A.to_device(k.encrypt_bits(np.ones(count, np.uint8), 3001, 0))
+    sds = []
+    for lvl in range(20):
+        one = A.to_device(k.encrypt_bits(np.ones(count, np.uint8), 3002 + lvl, 0))
+        out = torch.zeros((count, 632), dtype=torch.int32, device="cuda:0")
+        server.gate_batch(L.AND, x, one, out)
+        torch.cuda.synchronize()
+        h = A.to_host(out).astype(np.int64)
+        phase = (h[:, 630] - (h[:, :630] * s).sum(axis=1)) % 2 ** 32
+        err = ((phase - 0x20000000 + 2 ** 31) % 2 ** 32 - 2 ** 31) / 2 ** 32
+        assert np.all(np.abs(err) < 1 / 8), lvl  # every output still decrypts to 1
+        sds.append(float(np.sqrt(np.mean(err ** 2))))
+        x = out
+    assert all(2e-3 < v < 5e-3 for v in sds), sds
+    assert max(sds) / min(sds) < 1.1, sds  # bootstrapping refreshes: no growth with depth
