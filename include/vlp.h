@@ -169,7 +169,9 @@ int vlp_program_node_row(const vlp_program* prog, int kind, size_t record, uint3
 int vlp_program_intermediate_offset(const vlp_program* prog, uint64_t* byte_offset);
 
 /* Evaluate the program on `stream` (asynchronous).  scratch_dev: >= info.scratch_bytes of device
- * memory (job arrays are uploaded into it on the first call with a given scratch pointer). */
+ * memory (job arrays are uploaded into it on the first call with a given scratch pointer; it also holds the
+ * intermediates, the N-LWE staging and the key-switch GEMM staging, so two evaluations in flight at the same
+ * time need two scratch buffers). */
 int vlp_program_eval(vlp_program* prog, void* scratch_dev, size_t scratch_bytes, const uint32_t* in0_dev,
                      const uint32_t* in1_dev, uint32_t* out_dev, uint64_t stream);
 
