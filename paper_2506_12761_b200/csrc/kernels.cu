@@ -1,7 +1,10 @@
 // kernels.cu -- the sm_100a kernels of the hot path.
 //
-//  K2 vlp_blind_rotate_kernel : gate linear form (S2) + mod-switch (S3) + accumulator init (S4) +
-//                               630 CMux steps (S5) with the accumulator on chip + SampleExtract (S6)
+//  K2 vlp_blind_rotate_kernel<B> : gate linear form (S2) + mod-switch (S3) + accumulator init (S4) +
+//                               630 CMux steps (S5) with the accumulator on chip + SampleExtract (S6);
+//                               B = 5 bootstraps per CTA for whole waves, 1-4 for narrow tails
+//  K2 vlp_blind_rotate_lat_kernel : the same for a tail of <= 1 bootstrap per SM, one bootstrap on 3 warp
+//                               groups (latency mode)
 //  K3 vlp_ks_indicator_kernel + cuBLASLt int8 GEMM + vlp_ks_combine_kernel : MUX combine (S7) + key
 //                               switch (S8) as a one-hot-indicator x byte-limb-ksk GEMM on the tensor cores
 //  K4 vlp_bsk_convert_kernel  : bsk -> 3-limb NTT domain (setup)
@@ -124,7 +127,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t ta, uint32_t (&v)[8]) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Per-bootstrap named barrier (ids 1..kBrBoot; 128 threads): the 4 bootstraps of a CTA only meet at the bsk ring.
+// Per-bootstrap named barrier (ids 1..B; 128 threads): the bootstraps of a CTA only meet at the bsk ring.
 __device__ __forceinline__ void bar_boot(uint32_t g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kBT) : "memory");
 }
@@ -257,7 +260,7 @@ __device__ __forceinline__ void exchange(uint32_t (&d)[NP][8], uint32_t* xb, uin
 // ================================================================================ K2 blind rotation
 // Per CMux step and bootstrap: two forward rounds (component u of D = X^abar acc - acc: its 3 gadget digit
 // polynomials -> forward NTT -> Montgomery MAC into the 6 output accumulators, bsk chunks streamed by TMA
-// into a smem ring shared by the CTA's 4 bootstraps), then two inverse rounds (output component u: its 3
+// into a smem ring shared by the CTA's bootstraps), then two inverse rounds (output component u: its 3
 // key limbs -> inverse NTT -> centered lift -> recombine mod 2^32 -> acc_u += ...).  The round loops are
 // not unrolled: each round body is ~25 KB of SASS (the instruction cache, not the ALUs, limited the fully
 // unrolled form; profiles/).
