@@ -271,8 +271,9 @@ def main():
     keys = A.Keys(wl.key_seed)                 # client (every rank regenerates the same keys from the seed)
     srv = A.Server(keys, local)
     per = A.record_cts(m)
-    db = A.to_device(keys.encrypt_db(m, wl.records[first:first + shard], wl.payloads[first:first + shard],
-                                     pk_seed=wl.key_seed + 1, first=first, count=shard), local)
+    # device PubKeyGen + ServerEnc (byte-identical to the host calls; tests/test_gpu_parity.py)
+    db = A.encrypt_db_device(keys, m, wl.records[first:first + shard], wl.payloads[first:first + shard],
+                             pk_seed=wl.key_seed + 1, first=first, count=shard, device=local)
     nq = args.queries
     if nq > 1 and world > 1:
         raise SystemExit("--queries > 1 is single-GPU (multi-query packing of one shard)")

@@ -133,6 +133,17 @@ int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);
  * a second call returns VLP_EPKUSED.  Server side: needs no secret key. */
 int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* out);
 
+/* Device PubKeyGen + ServerEnc (both roles on one machine, e.g. to build benchmark
+ * DBs): the encrypted DB of records [first, first+count) written straight to out_dev ([count][per_record]
+ * [632], the vlp_server_encrypt_db layout), byte-identical to vlp_pubkeygen(sk, meta, pk_seed, first, count)
+ * followed by vlp_server_encrypt_db.  The Gaussian noise is drawn on the host (the same libm Box-Muller),
+ * the PRNG mask words and inner products on the device.  words / payloads as in vlp_server_encrypt_db.
+ * scratch_dev >= vlp_encrypt_db_device_scratch_bytes(meta, count).  Synchronous. */
+int vlp_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes);
+int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_seed, size_t first, size_t count,
+                          const uint64_t* words, const uint64_t* payloads, uint32_t* out_dev, void* scratch_dev,
+                          size_t scratch_bytes, uint64_t stream);
+
 /* Server: the evaluation key on one device.  evk_dev must hold vlp_server_evk_bytes() bytes (device
  * memory on `device`); the bootstrapping key is uploaded and converted to the NTT domain in place
  * (kernel vlp_bsk_convert_kernel), the key-switching key uploaded.  Synchronous. */

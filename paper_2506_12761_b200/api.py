@@ -112,6 +112,29 @@ class Keys:
         return out
 
 
+def encrypt_db_device(keys: "Keys", m: VlpMeta, words, payloads, pk_seed: int, first: int = 0,
+                      count: int | None = None, device: int = 0, stream=None):
+    """Device PubKeyGen + ServerEnc: the encrypted DB as a torch int32 [count * per, 632] tensor on `device`,
+    byte-identical to Keys.encrypt_db."""
+    import torch
+    words = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+    count = len(payloads) if count is None else count
+    pw = (m.l_S + 63) // 64
+    if pw == 1:
+        pays = np.ascontiguousarray(np.asarray(payloads, dtype=np.uint64))
+    else:
+        pays = np.array([[(int(v) >> (64 * w)) & (2 ** 64 - 1) for w in range(pw)] for v in payloads], dtype=np.uint64)
+    per = record_cts(m)
+    out = torch.empty((count * per, CT_STRIDE), dtype=torch.int32, device=f"cuda:{device}")
+    sb = ctypes.c_size_t()
+    check(lib().vlp_encrypt_db_device_scratch_bytes(ctypes.byref(m), count, ctypes.byref(sb)))
+    sc = torch.empty(max(256, sb.value), dtype=torch.uint8, device=f"cuda:{device}")
+    check(lib().vlp_encrypt_db_device(keys.sk, ctypes.byref(m), pk_seed, first, count, _u64p(words), _u64p(pays),
+                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(sc.data_ptr()), sc.numel(),
+                                      _stream_handle(stream)))
+    return out
+
+
 def record_cts(m: VlpMeta) -> int:
     v = ctypes.c_size_t()
     check(lib().vlp_db_record_cts(ctypes.byref(m), ctypes.byref(v)))

@@ -260,6 +260,43 @@ using namespace vlp;
 
 extern "C" {
 
+int vlp_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
+  size_t per = 0;
+  if (int rc = vlp_db_record_cts(meta, &per)) return rc;
+  if (!scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  *scratch_bytes = align256(n * 4) + align256(count * per * 4) + align256(count * per);
+  return VLP_OK;
+}
+
+int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_seed, size_t first, size_t count,
+                          const uint64_t* words, const uint64_t* payloads, uint32_t* out_dev, void* scratch,
+                          size_t scratch_bytes, uint64_t stream) {
+  if (!out_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  std::vector<uint32_t> nz;
+  std::vector<uint8_t> bits;
+  uint64_t h1 = 0;
+  if (int rc = prepare_encrypt_db(sk, meta, pk_seed, first, count, words, payloads, nz, bits, &h1)) return rc;
+  size_t need = 0;
+  vlp_encrypt_db_device_scratch_bytes(meta, count, &need);
+  if (scratch_bytes < need) return fail(VLP_ENOMEM, "scratch too small");
+  const size_t per = nz.size() / count, W = record_words(*meta);
+  uint8_t* sc = static_cast<uint8_t*>(scratch);
+  uint32_t* s_dev = reinterpret_cast<uint32_t*>(sc);
+  uint32_t* nz_dev = reinterpret_cast<uint32_t*>(sc + align256(n * 4));
+  uint8_t* bits_dev = sc + align256(n * 4) + align256(nz.size() * 4);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(s_dev, sk->s, n * 4, cudaMemcpyHostToDevice, st)) ||
+      (e = cudaMemcpyAsync(nz_dev, nz.data(), nz.size() * 4, cudaMemcpyHostToDevice, st)) ||
+      (e = cudaMemcpyAsync(bits_dev, bits.data(), bits.size(), cudaMemcpyHostToDevice, st)))
+    return cuda_fail(e, "upload");
+  if ((e = launch_encrypt_db(s_dev, nz_dev, bits_dev, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
+                             meta->l_I, first, nz.size(), out_dev, st)))
+    return cuda_fail(e, "encrypt db");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "encrypt db sync");
+  return VLP_OK;
+}
+
 size_t vlp_server_evk_bytes(void) { return kEvkBytes; }
 
 int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_bytes, uint64_t stream,

@@ -257,6 +257,50 @@ int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t 
   return VLP_OK;
 }
 
+}  // extern "C"
+
+namespace vlp {
+// Host half of vlp_encrypt_db_device (api.cu): range checks, the per-sample Gaussian noise of alg:PubKeyGen
+// (exactly the values vlp_pubkeygen draws), the plaintext bit of every DB row, and the PRNG prefix
+// h1 = mix(seed ^ PK_A * C1) the device continues from.
+int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                       const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
+                       std::vector<uint8_t>& bits, uint64_t* h1) {
+  if (!sk) return fail(VLP_EINVAL, "null argument");
+  if (int rc = check_meta(meta)) return rc;
+  if (count == 0 || first + count > meta->M) return fail(VLP_EINVAL, "bad record range");
+  if (!words || !payloads) return fail(VLP_EINVAL, "null argument");
+  const size_t W = record_words(*meta), lI = meta->l_I, lS = meta->l_S, per = W * lI + lS;
+  const size_t PW = (lS + 63) / 64, top = lS - 64 * (PW - 1);
+  for (size_t r = 0; r < count; r++) {
+    for (size_t k = 0; k < W; k++)
+      if (lI < 64 && words[r * W + k] >> lI) return fail(VLP_ERANGE, "record word >= 2^l_I");
+    if (top < 64 && payloads[r * PW + PW - 1] >> top) return fail(VLP_ERANGE, "payload >= 2^l_S");
+  }
+  try {
+    nz.resize(count * per);
+    bits.resize(count * per);
+  } catch (...) {
+    return fail(VLP_ENOMEM, "out of host memory");
+  }
+  parallel_for(count * per, [&](size_t idx) {
+    const size_t rec = idx / per, row = idx % per;
+    const size_t local = row < W * lI ? (row % lI) * W + row / lI : row;
+    nz[idx] = noise(seed, kPkE, (first + rec) * per + local, 0, sk->params.sigma_lwe);
+    if (row < W * lI) {
+      bits[idx] = static_cast<uint8_t>((words[rec * W + row / lI] >> (row % lI)) & 1);
+    } else {
+      const size_t j = row - W * lI;
+      bits[idx] = static_cast<uint8_t>((payloads[rec * PW + j / 64] >> (j % 64)) & 1);
+    }
+  });
+  *h1 = mix(seed ^ (kPkA * 0x9E3779B97F4A7C15ull));
+  return VLP_OK;
+}
+}  // namespace vlp
+
+extern "C" {
+
 int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* out) {
   if (!pk || !out || (pk->count && (!words || !payloads))) return fail(VLP_EINVAL, "null argument");
   if (pk->used) return fail(VLP_EPKUSED, "public-key samples already used (single-use, alg:PubKeyGen)");

@@ -816,6 +816,51 @@ __global__ void vlp_ksk_to_i8_kernel(const uint32_t* __restrict__ ksk, int8_t* _
   }
 }
 
+// ================================================================================ device PubKeyGen + ServerEnc
+// (setup) one warp per DB ciphertext: the TLWE(0) public-key sample of alg:PubKeyGen
+// (mask words from the counter PRNG of R3, b = <a, s> + e with e computed on the host by the same libm
+// Box-Muller as vlp_pubkeygen) plus (0, Ecd(bit)) of alg:ServerEnc -- byte-identical to the host calls.
+__device__ __forceinline__ uint64_t prng_mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void __launch_bounds__(256) vlp_encrypt_db_kernel(const uint32_t* __restrict__ s, const uint32_t* __restrict__ noise,
+                                                            const uint8_t* __restrict__ bits, uint64_t h1, uint32_t per,
+                                                            uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples,
+                                                            uint32_t* __restrict__ out) {
+  const uint64_t idx = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (idx >= nsamples) return;
+  const uint64_t rec = idx / per, row = idx % per;
+  const uint64_t local = row < static_cast<uint64_t>(W) * lI ? (row % lI) * W + row / lI : row;  // alg:PubKeyGen order
+  const uint64_t obj = (first + rec) * per + local;
+  const uint64_t h2 = prng_mix(h1 ^ (obj * 0xC2B2AE3D27D4EB4Full));
+  uint32_t* ct = out + idx * kCt;
+  uint32_t b = 0;
+  for (uint32_t w = lane; w < static_cast<uint32_t>(n); w += 32) {
+    const uint32_t a = static_cast<uint32_t>(prng_mix(h2 ^ (w * 0x165667B19E3779F9ull)) >> 32);
+    ct[w] = a;
+    b += a * s[w];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  if (lane == 0) {
+    ct[n] = b + noise[idx] + (bits[idx] ? kMu : 0u - kMu);
+    ct[n + 1] = 0;
+  }
+}
+
+cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
+                              uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st) {
+  if (!nsamples) return cudaSuccess;
+  const uint64_t blocks = (nsamples * 32 + 255) / 256;
+  vlp_encrypt_db_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(s, noise, bits, h1, per, W, lI, first, nsamples, out);
+  return cudaGetLastError();
+}
+
 // ================================================================================ K4 bsk conversion
 // One CTA per (i, key row q, component u): split the 1024 torus32 coefficients into 3 signed limbs, forward
 // NTT each limb polynomial mod p (plain, fully reduced; natural twiddle table), multiply by

@@ -76,6 +76,8 @@ void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
 // one level: whole waves of kBrBoot bootstraps per CTA + a narrower tail wave (1 or 2 kernel launches)
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st);
 int br_launch_count(uint32_t njobs, int sm_count);
+cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
+                              uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st);
 void launch_ksk_to_i8(const uint32_t* ksk, int8_t* kmat, cudaStream_t st);
 cudaError_t launch_ks_indicator(const KsArgs& a, uint32_t c0, uint32_t cnt, int8_t* ind, cudaStream_t st);
 cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const int32_t* d, cudaStream_t st);

@@ -32,6 +32,9 @@ enum : uint64_t {
 };
 uint64_t prng(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word);
 uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma);
+int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                       const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
+                       std::vector<uint8_t>& bits, uint64_t* h1);
 
 int check_meta(const vlp_meta* m);
 // Bound words per record (R17) and query words.

@@ -479,3 +479,20 @@ def test_noise_over_depth_at_scale(server):
         x = out
     assert all(2e-3 < v < 5e-3 for v in sds), sds
     assert max(sds) / min(sds) < 1.1, sds  # bootstrapping refreshes: no growth with depth
+
+
+@pytest.mark.parametrize("cfg,count", [(1, None), (9, 16), (4, 4096)])
+def test_device_encrypt_db_equals_host(server, cfg, count):
+    """Device PubKeyGen + ServerEnc (vlp_encrypt_db_device) is byte-identical to the host vlp_pubkeygen +
+    vlp_server_encrypt_db (which test_library_host pins to the oracle): config 1, 16 records of the 128-bit
+    payload weather shape, and 4096 records of config 4 starting at record 1000."""
+    wl = make_workload(cfg, key_seed=SEED)
+    k = server.keys
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    first = 1000 if cfg == 4 else 0
+    count = wl.M if count is None else count
+    recs, pays = wl.records[first:first + count], wl.payloads[first:first + count]
+    host = k.encrypt_db(m, recs, pays, pk_seed=77, first=first, count=count)
+    dev = A.encrypt_db_device(k, m, recs, pays, pk_seed=77, first=first, count=count)
+    torch.cuda.synchronize()
+    assert np.array_equal(A.to_host(dev), host)
