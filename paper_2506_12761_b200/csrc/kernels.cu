@@ -506,31 +506,32 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
 
 
 // ================================================================================ K2-LAT (latency mode)
-// One bootstrap per CTA for the narrow tail of a level (<= one bootstrap per SM): its 3 gadget digits (forward
-// rounds) and its 3 key limbs (inverse rounds) run on 3 warp groups of 128 threads, so each warp transforms 1
-// polynomial per round instead of 3.  The groups meet through TMEM: thread t of every group owns TMEM lane t
-// (warp 4G + t/32 sits in quadrant t/32), so the transformed digits (columns 8(3u + j) + s) and the lifted
-// limbs (48 + 8(3u + l) + r) written by one group are read by the others after a CTA barrier.  Group G
-// computes the MAC outputs of limb G (u_out = 0, 1).  Same arithmetic, layouts, key and bytes as the
-// throughput kernel.
-constexpr int kLatThreads = 3 * kBT;
+// One bootstrap per CTA for the narrow tail of a level (<= one bootstrap per SM): its 6 digit polynomials
+// (forward: group G = 3u + j transforms digit j of component u) and its 6 output limbs (MAC + inverse: group
+// G = 3 u_out + l) run on 6 warp groups of 128 threads, one polynomial per warp per phase.  The groups meet
+// through TMEM: thread t of every group owns TMEM lane t (warp 4G + t/32 sits in quadrant t/32), so the
+// transformed digits (columns 8G + s) and the lifted limbs (48 + 8G + r) written by one group are read by
+// the others after a CTA barrier.  Same arithmetic, layouts, key and bytes as the throughput kernel.
+constexpr int kLatGroups = 6;
+constexpr int kLatSlots = 4;  // a whole CMux step of bsk chunks in flight: a lone bootstrap never waits on TMA
+constexpr int kLatThreads = kLatGroups * kBT;
 constexpr int kLatTmemCols = 128;
 __host__ __device__ constexpr int lat_smem_bytes() {
-  return kSlots * kChunkBytes + (2 * N * 4 + 6 * N * 4 + 640 * 2) + kSlots * 8 + kSlots * 4 + 8;
+  return kLatSlots * kChunkBytes + (2 * N * 4 + kLatGroups * N * 4 + 640 * 2) + kLatSlots * 8 + kLatSlots * 4 + 8;
 }
 
 __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(const BrArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* ring = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* acc = ring + kSlots * kBT * kChunkWords;
-  uint32_t* xb_all = acc + 2 * N;  // [group 3][2 polys][N]
-  uint16_t* abar = reinterpret_cast<uint16_t*>(xb_all + 6 * N);
+  uint32_t* acc = ring + kLatSlots * kBT * kChunkWords;
+  uint32_t* xb_all = acc + 2 * N;  // [group 6][N]
+  uint16_t* abar = reinterpret_cast<uint16_t*>(xb_all + kLatGroups * N);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(abar + 640);
-  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kSlots);
-  uint32_t* tmem_base_sh = rel + kSlots;
+  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kLatSlots);
+  uint32_t* tmem_base_sh = rel + kLatSlots;
 
   const uint32_t tid = threadIdx.x, G = tid / kBT, t = tid % kBT;
-  uint32_t* xb = xb_all + G * 2 * N;
+  uint32_t* xb = xb_all + G * N;
   const uint2* twf = a.twl_fwd + t;
   const uint2* twi = a.twl_inv + t;
   const Rc zr{a.zero, a.p2};
@@ -539,7 +540,7 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
   const uint32_t total_chunks = my_jobs * static_cast<uint32_t>(a.steps) * kChunks;
 
   if (tid == 0) {
-    for (int s = 0; s < kSlots; s++) {
+    for (int s = 0; s < kLatSlots; s++) {
       mbar_init(&mbar[s], 1);
       rel[s] = 0;
     }
@@ -558,12 +559,12 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
 
   auto issue = [&](uint32_t nseq) {
     const uint32_t step = (nseq / kChunks) % static_cast<uint32_t>(a.steps), c = nseq % kChunks;
-    const uint32_t s = nseq % kSlots;
+    const uint32_t s = nseq % kLatSlots;
     bulk_load(ring + s * kBT * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * kBT * kChunkWords,
               kChunkBytes, &mbar[s]);
   };
   if (tid == 0)
-    for (uint32_t q = 0; q < kSlots && q < total_chunks; q++) issue(q);
+    for (uint32_t q = 0; q < kLatSlots && q < total_chunks; q++) issue(q);
   uint32_t nseq = 0, sl = 0, ph = 0;
   auto cta_sync_tmem = [&]() {  // TMEM writes of one group -> reads of another
     tmem_wait_st();
@@ -597,22 +598,21 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
     __syncthreads();
 
     // ---- S5: CMux steps
-    const uint32_t dshift = 25u - 7u * G;  // gadget digit G (R5)
+    const uint32_t uc = G / 3, jl = G % 3;          // forward: component uc, digit jl; MAC/inverse: u_out uc, limb jl
+    const uint32_t dshift = 25u - 7u * jl;          // gadget digit jl (R5)
     for (int i = 0; i < a.steps; i++) {
       const uint32_t ab = abar[i];
-      {  // digit G of both components, transformed together (2 polynomials per thread)
-        uint32_t d[2][8];
+      {  // digit jl of component uc
+        uint32_t d[1][8];
 #pragma unroll
-        for (int u = 0; u < 2; u++)
-#pragma unroll
-          for (int r = 0; r < 8; r++) {
-            const uint32_t j = t + 128u * r;
-            const uint32_t kk = (j - ab) & (2 * N - 1);
-            uint32_t v = acc[u * N + (kk & (N - 1))];
-            v = kk >= static_cast<uint32_t>(N) ? zr.z - v : v;
-            const uint32_t w = v - acc[u * N + j] + 0x81020400u;
-            d[u][r] = ((w >> dshift) & 127u) + (P - 64u);
-          }
+        for (int r = 0; r < 8; r++) {
+          const uint32_t j = t + 128u * r;
+          const uint32_t kk = (j - ab) & (2 * N - 1);
+          uint32_t v = acc[uc * N + (kk & (N - 1))];
+          v = kk >= static_cast<uint32_t>(N) ? zr.z - v : v;
+          const uint32_t w = v - acc[uc * N + j] + 0x81020400u;
+          d[0][r] = ((w >> dshift) & 127u) + (P - 64u);
+        }
         stage_A<0, false>(d, zr);
         stage_A<1, false>(d, zr);
         stage_A<2, false>(d, zr);
@@ -625,12 +625,11 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
         stage_BC<7, false>(d, twf, zr);
         stage_BC<8, false>(d, twf, zr);
         stage9_fwd(d, t, twf, zr);
-        tmem_st8(tm + 8 * G, d[0]);        // transformed digit (0, G)
-        tmem_st8(tm + 8 * (3 + G), d[1]);  // transformed digit (1, G)
+        tmem_st8(tm + 8 * G, d[0]);  // transformed digit (uc, jl) = digit row G
       }
       cta_sync_tmem();
-      // MAC for limb G of both output components: o = G (u_out 0) and 3 + G (u_out 1)
-      uint32_t mac[2][8];
+      // MAC for output o = G = 3 u_out + limb
+      uint32_t mac[8];
 #pragma unroll
       for (int pp = 0; pp < kChunks; pp++) {
         uint32_t xr[6][2];
@@ -652,9 +651,8 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
           }
         mbar_wait(&mbar[sl], ph);
         const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
-#pragma unroll
-        for (int oi = 0; oi < 2; oi++) {
-          const uint4* kp = reinterpret_cast<const uint4*>(rec + (3 * oi + G) * 12);  // [e 2][q 6]
+        {
+          const uint4* kp = reinterpret_cast<const uint4*>(rec + G * 12);  // [e 2][q 6]
           const uint4 k0 = kp[0], k1 = kp[1], k2 = kp[2];
           const uint32_t kv[2][6] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y}, {k1.z, k1.w, k2.x, k2.y, k2.z, k2.w}};
 #pragma unroll
@@ -663,7 +661,7 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
 #pragma unroll
             for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(x[e][q]) * kv[e][q];
             const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
-            mac[oi][2 * pp + e] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
+            mac[2 * pp + e] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
           }
         }
         __syncwarp();
@@ -671,25 +669,23 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
           __threadfence_block();
           if (atomicAdd(&rel[sl], 1u) == kLatThreads / 32 - 1) {
             atomicExch(&rel[sl], 0u);
-            if (nseq + kSlots < total_chunks) {
+            if (nseq + kLatSlots < total_chunks) {
               fence_proxy_async();
-              issue(nseq + kSlots);
+              issue(nseq + kLatSlots);
             }
           }
         }
         nseq++;
-        if (++sl == kSlots) {
+        if (++sl == kLatSlots) {
           sl = 0;
           ph ^= 1u;
         }
       }
       // inverse NTT of limb G of both components, centered lift, park in TMEM
-      {  // inverse NTT of limb G of both components together, centered lift, park in TMEM
-        uint32_t d[2][8];
+      {  // inverse NTT of limb jl of component uc, centered lift, park in TMEM
+        uint32_t d[1][8];
 #pragma unroll
-        for (int u = 0; u < 2; u++)
-#pragma unroll
-          for (int s = 0; s < 8; s++) d[u][s] = umin(mac[u][s], mac[u][s] - P2);
+        for (int s = 0; s < 8; s++) d[0][s] = umin(mac[s], mac[s] - P2);
         stage9_inv(d, t, twi, zr);
         stage_BC<8, true>(d, twi, zr);
         stage_BC<7, true>(d, twi, zr);
@@ -703,33 +699,27 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
         stage_A<1, true>(d, zr);
         stage_A<0, true>(d, zr);
 #pragma unroll
-        for (int u = 0; u < 2; u++)
-#pragma unroll
-          for (int r = 0; r < 8; r++) {
-            const uint32_t v = umin(d[u][r], d[u][r] - P);
-            d[u][r] = v > (P >> 1) ? v - P : v;  // centered, two's complement
-          }
+        for (int r = 0; r < 8; r++) {
+          const uint32_t v = umin(d[0][r], d[0][r] - P);
+          d[0][r] = v > (P >> 1) ? v - P : v;  // centered, two's complement
+        }
         tmem_st8(tm + 48 + 8 * G, d[0]);
-        tmem_st8(tm + 48 + 8 * (3 + G), d[1]);
       }
       cta_sync_tmem();
-      // recombine R0 + 2^11 R1 + 2^22 R2 and acc_u += (layout A: j = t + 128 r); group G takes r = G, G+3, G+6
+      // recombine R0 + 2^11 R1 + 2^22 R2 and acc_uc += (layout A: j = t + 128 r); the 3 groups of component
+      // uc take r = jl, jl + 3, jl + 6
       {
-        uint32_t lv[2][3][8];
+        uint32_t lv[3][8];
 #pragma unroll
-        for (int u = 0; u < 2; u++)
-#pragma unroll
-          for (int l = 0; l < 3; l++) tmem_ld8(tm + 48 + 8 * (3 * u + l), lv[u][l]);
+        for (int l = 0; l < 3; l++) tmem_ld8(tm + 48 + 8 * (3 * uc + l), lv[l]);
         tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 2; u++)
-#pragma unroll
-          for (int r = 0; r < 8; r++) {
-            if (static_cast<uint32_t>(r % 3) != G) continue;
-            const uint32_t hi = __funnelshift_l(0u, lv[u][1][r], 11) + __funnelshift_l(0u, lv[u][2][r], 22) + zr.z;
-            uint32_t& av = acc[u * N + t + 128u * r];
-            av = add_alu(av, lv[u][0][r], hi);
-          }
+        for (int r = 0; r < 8; r++) {
+          if (static_cast<uint32_t>(r % 3) != jl) continue;
+          const uint32_t hi = __funnelshift_l(0u, lv[1][r], 11) + __funnelshift_l(0u, lv[2][r], 22) + zr.z;
+          uint32_t& av = acc[uc * N + t + 128u * r];
+          av = add_alu(av, lv[0][r], hi);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncthreads();  // acc complete before the next step's digit gather
