@@ -3,8 +3,10 @@
 //  K2 vlp_blind_rotate_kernel<B> : gate linear form (S2) + mod-switch (S3) + accumulator init (S4) +
 //                               630 CMux steps (S5) with the accumulator on chip + SampleExtract (S6);
 //                               B = 5 bootstraps per CTA for whole waves, 1-4 for narrow tails
-//  K2 vlp_blind_rotate_lat_kernel : the same for a tail of <= 1 bootstrap per SM, one bootstrap on 3 warp
+//  K2 vlp_blind_rotate_lat_kernel : the same for a tail of <= 1 bootstrap per SM, one bootstrap on 6 warp
 //                               groups (latency mode)
+//  K2 vlp_blind_rotate_clat_kernel : a tail of <= 1 bootstrap per 2 SMs, one bootstrap on a 2-CTA cluster
+//                               (one accumulator component per SM, DSMEM exchange of the MAC inputs)
 //  K3 vlp_ks_indicator_kernel + cuBLASLt int8 GEMM + vlp_ks_combine_kernel : MUX combine (S7) + key
 //                               switch (S8) as a one-hot-indicator x byte-limb-ksk GEMM on the tensor cores
 //  K4 vlp_bsk_convert_kernel  : bsk -> 3-limb NTT domain (setup)
@@ -17,6 +19,7 @@
 // [0, 2p); N^-1 and the Montgomery factor are folded into the stored key.
 //
 // Thread layout of one bootstrap: see "layouts / swizzle" below (128 threads x 8 coefficients).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -26,6 +29,7 @@
 #include "kernels.cuh"
 
 namespace vlp {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr uint32_t P = kP;
@@ -743,6 +747,241 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kLatTmemCols) : "memory");
 }
 
+
+// ================================================================================ K2-CLAT (cluster latency mode)
+// For the narrowest level tails (<= 74 bootstraps): one bootstrap on a cluster of 2 CTAs (2 SMs).  CTA rank
+// r owns accumulator component r: its 3 digit polynomials (forward, one per warp group), the 3 limbs of
+// output component r (MAC + inverse, one per group) and the update of acc_r -- so the next step's digits
+// need only local data.  The one cross-SM exchange per step is the MAC input: each CTA publishes its 3
+// transformed digit polynomials in shared memory (double-buffered, [q][slot][thread]) and reads the peer's
+// through distributed shared memory after a cluster barrier.  Same arithmetic, key layout and bytes.
+constexpr int kClatGroups = 3;
+constexpr int kClatThreads = kClatGroups * kBT;
+constexpr int kClatTmemCols = 32;
+__host__ __device__ constexpr int clat_smem_bytes() {
+  return kLatSlots * kChunkBytes + (N * 4 + kClatGroups * N * 4 + 2 * 3 * N * 4 + 640 * 2) + kLatSlots * 8 +
+         kLatSlots * 4 + 8;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
+    vlp_blind_rotate_clat_kernel(const BrArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* ring = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* acc = ring + kLatSlots * kBT * kChunkWords;  // component r only
+  uint32_t* xb_all = acc + N;                            // [group 3][N]
+  uint32_t* dig = xb_all + kClatGroups * N;              // [buf 2][q 3][slot 8][thread 128]
+  uint16_t* abar = reinterpret_cast<uint16_t*>(dig + 2 * 3 * N);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(abar + 640);
+  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kLatSlots);
+  uint32_t* tmem_base_sh = rel + kLatSlots;
+
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t rk = cl.block_rank();  // accumulator component owned by this CTA
+  const uint32_t* dig_peer = cl.map_shared_rank(dig, rk ^ 1u);
+  const uint32_t tid = threadIdx.x, G = tid / kBT, t = tid % kBT;
+  uint32_t* xb = xb_all + G * N;
+  const uint2* twf = a.twl_fwd + t;
+  const uint2* twi = a.twl_inv + t;
+  const Rc zr{a.zero, a.p2};
+  const uint32_t nclusters = gridDim.x / 2, cid = blockIdx.x / 2;
+  if (cid >= a.njobs) return;  // both CTAs of a cluster take the same branch
+  const uint32_t my_jobs = (a.njobs - cid + nclusters - 1) / nclusters;
+  const uint32_t total_chunks = my_jobs * static_cast<uint32_t>(a.steps) * kChunks;
+
+  if (tid == 0) {
+    for (int s = 0; s < kLatSlots; s++) {
+      mbar_init(&mbar[s], 1);
+      rel[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "n"(kClatTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = *tmem_base_sh + ((32u * ((tid >> 5) & 3u)) << 16);
+
+  auto issue = [&](uint32_t nseq) {
+    const uint32_t step = (nseq / kChunks) % static_cast<uint32_t>(a.steps), c = nseq % kChunks;
+    const uint32_t s = nseq % kLatSlots;
+    bulk_load(ring + s * kBT * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * kBT * kChunkWords,
+              kChunkBytes, &mbar[s]);
+  };
+  if (tid == 0)
+    for (uint32_t q = 0; q < kLatSlots && q < total_chunks; q++) issue(q);
+  uint32_t nseq = 0, sl = 0, ph = 0, buf = 0;
+  const uint32_t dshift = 25u - 7u * G;  // forward: gadget digit G of component rk (R5)
+
+  for (uint32_t jb = cid; jb < a.njobs; jb += nclusters) {
+    {  // S2 + S3 (both CTAs need every abar)
+      const BrJob job = a.jobs[jb];
+      const uint32_t* x = slot_ptr(a.reg, job.x);
+      const uint32_t* y = slot_ptr(a.reg, job.y);
+      for (uint32_t w = tid; w <= static_cast<uint32_t>(n); w += kClatThreads) {
+        uint32_t c = static_cast<uint32_t>(static_cast<int32_t>(job.ax)) * x[w];
+        if (job.ay) c += static_cast<uint32_t>(static_cast<int32_t>(job.ay)) * y[w];
+        if (w == static_cast<uint32_t>(n)) c += job.k0;
+        abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
+      }
+    }
+    __syncthreads();
+    {  // S4 for component rk: acc_0 = 0, acc_1 = X^{-bbar} testv (R8)
+      const uint32_t bbar = abar[n];
+      for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kClatThreads)
+        acc[k] = rk == 0 ? 0u : ((((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu));
+    }
+    __syncthreads();
+
+    for (int i = 0; i < a.steps; i++) {
+      const uint32_t ab = abar[i];
+      uint32_t* mydig = dig + buf * 3 * N;
+      {  // digit G of component rk -> forward NTT -> publish [q][slot][thread]
+        uint32_t d[1][8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const uint32_t j = t + 128u * r;
+          const uint32_t kk = (j - ab) & (2 * N - 1);
+          uint32_t v = acc[kk & (N - 1)];
+          v = kk >= static_cast<uint32_t>(N) ? zr.z - v : v;
+          const uint32_t w = v - acc[j] + 0x81020400u;
+          d[0][r] = ((w >> dshift) & 127u) + (P - 64u);
+        }
+        stage_A<0, false>(d, zr);
+        stage_A<1, false>(d, zr);
+        stage_A<2, false>(d, zr);
+        exchange<0, 1>(d, xb, t, G);
+        stage_BC<3, false>(d, twf, zr);
+        stage_BC<4, false>(d, twf, zr);
+        stage_BC<5, false>(d, twf, zr);
+        exchange<1, 2>(d, xb, t, G);
+        stage_BC<6, false>(d, twf, zr);
+        stage_BC<7, false>(d, twf, zr);
+        stage_BC<8, false>(d, twf, zr);
+        stage9_fwd(d, t, twf, zr);
+#pragma unroll
+        for (int s8 = 0; s8 < 8; s8++) mydig[(G * 8 + s8) * kBT + t] = d[0][s8];
+      }
+      cl.sync();  // both CTAs' digits published (release / acquire across the cluster)
+      const uint32_t* peerdig = dig_peer + buf * 3 * N;
+      // MAC for output o = 3 rk + G (component rk, limb G); digit rows q = 3u + j, u = 0 from CTA 0, 1 from CTA 1
+      uint32_t mac[8];
+#pragma unroll
+      for (int pp = 0; pp < kChunks; pp++) {
+        uint32_t x[2][6];
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+          const uint32_t* src = (static_cast<uint32_t>(q / 3) == rk) ? mydig : peerdig;
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            uint32_t v = src[((q % 3) * 8 + 2 * pp + e) * kBT + t];
+            v = umin(v, v - P2);
+            x[e][q] = umin(v, v - P);
+          }
+        }
+        mbar_wait(&mbar[sl], ph);
+        const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
+        {
+          const uint4* kp = reinterpret_cast<const uint4*>(rec + (3 * rk + G) * 12);  // [e 2][q 6]
+          const uint4 k0 = kp[0], k1 = kp[1], k2 = kp[2];
+          const uint32_t kv[2][6] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y}, {k1.z, k1.w, k2.x, k2.y, k2.z, k2.w}};
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            uint64_t T = static_cast<uint64_t>(x[e][0]) * kv[e][0];
+#pragma unroll
+            for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(x[e][q]) * kv[e][q];
+            const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
+            mac[2 * pp + e] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
+          }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) {
+          __threadfence_block();
+          if (atomicAdd(&rel[sl], 1u) == kClatThreads / 32 - 1) {
+            atomicExch(&rel[sl], 0u);
+            if (nseq + kLatSlots < total_chunks) {
+              fence_proxy_async();
+              issue(nseq + kLatSlots);
+            }
+          }
+        }
+        nseq++;
+        if (++sl == kLatSlots) {
+          sl = 0;
+          ph ^= 1u;
+        }
+      }
+      buf ^= 1u;
+      {  // inverse NTT of limb G of component rk, centered lift, park in TMEM
+        uint32_t d[1][8];
+#pragma unroll
+        for (int s8 = 0; s8 < 8; s8++) d[0][s8] = umin(mac[s8], mac[s8] - P2);
+        stage9_inv(d, t, twi, zr);
+        stage_BC<8, true>(d, twi, zr);
+        stage_BC<7, true>(d, twi, zr);
+        stage_BC<6, true>(d, twi, zr);
+        exchange<2, 1>(d, xb, t, G);
+        stage_BC<5, true>(d, twi, zr);
+        stage_BC<4, true>(d, twi, zr);
+        stage_BC<3, true>(d, twi, zr);
+        exchange<1, 0>(d, xb, t, G);
+        stage_A<2, true>(d, zr);
+        stage_A<1, true>(d, zr);
+        stage_A<0, true>(d, zr);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const uint32_t v = umin(d[0][r], d[0][r] - P);
+          d[0][r] = v > (P >> 1) ? v - P : v;
+        }
+        tmem_st8(tm + 8 * G, d[0]);
+      }
+      tmem_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      {  // acc_rk += R0 + 2^11 R1 + 2^22 R2; group G takes r = G, G + 3, G + 6
+        uint32_t lv[3][8];
+#pragma unroll
+        for (int l = 0; l < 3; l++) tmem_ld8(tm + 8 * l, lv[l]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          if (static_cast<uint32_t>(r % 3) != G) continue;
+          const uint32_t hi = __funnelshift_l(0u, lv[1][r], 11) + __funnelshift_l(0u, lv[2][r], 22) + zr.z;
+          uint32_t& av = acc[t + 128u * r];
+          av = add_alu(av, lv[0][r], hi);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+
+    // ---- S6: CTA 0 holds the mask a (a'_0 = a_0, a'_k = -a_{N-k}), CTA 1 the body b (b' = b_0)
+    if (a.raw_acc) {
+      uint32_t* o = a.raw_acc + static_cast<size_t>(jb) * 2 * N + rk * N;
+      for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kClatThreads) o[k] = acc[k];
+    } else {
+      uint32_t* o = a.nlwe + static_cast<size_t>(a.jobs[jb].out) * kNlwe;
+      if (rk == 0) {
+        for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kClatThreads) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+      } else if (tid == 0) {
+        o[N] = acc[0];
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();  // the peer may still read this CTA's digits
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kClatTmemCols) : "memory");
+}
+
 // ================================================================================ K3' key switch on tensor cores
 // (a) one-hot digit indicator: CTA per ciphertext; coefficient i -> 24 bytes ind[c][i*24 + j*3 + v-1].
 //     MUX combine (S7) and the 16-bit rounding (R6) in the prologue, as in K3.
@@ -979,8 +1218,32 @@ static cudaError_t launch_br_lat(const BrArgs& a, int sm_count, cudaStream_t st)
   return cudaGetLastError();
 }
 
+static cudaError_t launch_br_clat(const BrArgs& a, int sm_count, cudaStream_t st) {
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    e = cudaFuncSetAttribute(vlp_blind_rotate_clat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, clat_smem_bytes());
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit);
+  }
+  if (a.njobs == 0) return cudaSuccess;
+  const uint32_t half = static_cast<uint32_t>(sm_count / 2);
+  const uint32_t clusters = a.njobs < half ? a.njobs : half;
+  if ((static_cast<uint64_t>(a.njobs) + clusters - 1) / clusters * static_cast<uint64_t>(a.steps) * kChunks >= (1ull << 32))
+    return cudaErrorInvalidValue;
+  BrArgs b = a;
+  b.zero = 0;
+  b.p2 = P2;
+  vlp_blind_rotate_clat_kernel<<<2 * clusters, kClatThreads, clat_smem_bytes(), st>>>(b);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_br_width(const BrArgs& a, int B, int sm_count, cudaStream_t st) {
   switch (B) {
+    case -1: return launch_br_clat(a, sm_count, st);
     case 0: return launch_br_lat(a, sm_count, st);
     case 1: return launch_br_b<1>(a, sm_count, st);
     case 2: return launch_br_b<2>(a, sm_count, st);
@@ -1004,7 +1267,7 @@ static int forced_boot() {
 
 int br_launch_count(uint32_t njobs, int sm_count) {
   if (njobs == 0) return 0;
-  if ((forced_boot() >= 1 && forced_boot() <= kBrBoot) || forced_boot() == -1) return 1;
+  if ((forced_boot() >= 1 && forced_boot() <= kBrBoot) || forced_boot() == -1 || forced_boot() == -2) return 1;
   const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
   return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
 }
@@ -1013,7 +1276,8 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
   if (a.njobs == 0) return cudaSuccess;
   const int forced = forced_boot();
   if (forced >= 1 && forced <= kBrBoot) return launch_br_width(a, forced, sm_count, st);
-  if (forced == -1) return launch_br_width(a, 0, sm_count, st);  // VLP_BR_BOOT=-1: latency mode
+  if (forced == -1) return launch_br_width(a, 0, sm_count, st);   // VLP_BR_BOOT=-1: latency mode
+  if (forced == -2) return launch_br_width(a, -1, sm_count, st);  // VLP_BR_BOOT=-2: cluster latency mode
   const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
   const uint32_t full = a.njobs / wave * wave, tail = a.njobs - full;
   cudaError_t e = cudaSuccess;
@@ -1027,8 +1291,11 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
     r.jobs = a.jobs + full;
     r.njobs = tail;
     if (r.raw_acc) r.raw_acc = a.raw_acc + static_cast<size_t>(full) * 2 * N;
-    // a tail of at most one bootstrap per SM runs in latency mode (3 warp groups per bootstrap)
-    const int b = tail <= static_cast<uint32_t>(sm_count) ? 0 : static_cast<int>((tail + sm_count - 1) / sm_count);
+    // a tail of at most one bootstrap per SM runs in latency mode (warp groups per bootstrap); at most one per
+    // two SMs, on a 2-CTA cluster per bootstrap
+    const int b = tail <= static_cast<uint32_t>(sm_count / 2) ? -1
+                  : tail <= static_cast<uint32_t>(sm_count) ? 0
+                                                             : static_cast<int>((tail + sm_count - 1) / sm_count);
     e = launch_br_width(r, b, sm_count, st);
   }
   return e;
