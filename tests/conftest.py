@@ -11,6 +11,11 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200); parity tests through the C-ABI")
     config.addinivalue_line("markers", "slow: long-running (minutes)")
+    # a fresh checkout has no libvlp.so (built artefacts are git-ignored): compile it (nvcc sm_100a) before
+    # any test loads it.  The library itself never builds or falls back: it raises if the .so is missing.
+    from paper_2506_12761_b200 import build as B
+    if not os.path.exists(B.LIB):
+        B.build()
 
 
 @pytest.fixture(scope="session")
