@@ -176,6 +176,22 @@ int vlp_program_get_info(const vlp_program* prog, vlp_program_info* info);
  * program, for sampled parity dumps: kind 0 = validation bit v of record r (bit ignored), kind 1 =
  * masked payload bit (r, bit).  Returns VLP_EINVAL if absent. */
 int vlp_program_node_row(const vlp_program* prog, int kind, size_t record, uint32_t bit, uint64_t* row);
+/* The compiled schedule, for pure-function parity checks (SURVEY 4 layer 3): level `level`'s gate
+ * bootstraps and key switches.  vlp_br_job: output c = (0, k0) + ax*in[x] + ay*in[y] is bootstrapped into
+ * N-LWE row `row`; vlp_ks_job: out slot = KS((0, add) + nlwe[n0] (+ nlwe[n1] if n1 != 0xFFFFFFFF)).  Slot ids
+ * are region << 28 | row with regions 0 = in0, 1 = in1, 2 = intermediates (vlp_program_intermediate_offset),
+ * 3 = out.  Pass NULL arrays to get the counts. */
+typedef struct {
+  uint32_t x, y, k0;
+  int8_t ax, ay;
+  uint16_t pad;
+  uint32_t row;
+} vlp_br_job;
+typedef struct {
+  uint32_t n0, n1, add, out;
+} vlp_ks_job;
+int vlp_program_level_jobs(const vlp_program* prog, uint32_t level, vlp_br_job* br, uint64_t* nbr, vlp_ks_job* ks,
+                           uint64_t* nks);
 /* Pointer to the intermediate region inside `scratch_dev` (rows of 632 words). */
 int vlp_program_intermediate_offset(const vlp_program* prog, uint64_t* byte_offset);
 

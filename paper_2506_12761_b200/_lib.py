@@ -40,6 +40,15 @@ class VlpProgramInfo(ctypes.Structure):
                 ("max_level_br", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint32)]
 
 
+class VlpBrJob(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_uint32), ("y", ctypes.c_uint32), ("k0", ctypes.c_uint32), ("ax", ctypes.c_int8),
+                ("ay", ctypes.c_int8), ("pad", ctypes.c_uint16), ("row", ctypes.c_uint32)]
+
+
+class VlpKsJob(ctypes.Structure):
+    _fields_ = [("n0", ctypes.c_uint32), ("n1", ctypes.c_uint32), ("add", ctypes.c_uint32), ("out", ctypes.c_uint32)]
+
+
 # every symbol include/vlp.h declares: name -> (restype, argtypes)
 _vp, _u32p, _u64p, _u8p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64), \
     ctypes.POINTER(ctypes.c_uint8)
@@ -68,6 +77,8 @@ SIGNATURES = {
     "vlp_program_get_info": (_i, [_vp, ctypes.POINTER(VlpProgramInfo)]),
     "vlp_program_node_row": (_i, [_vp, _i, _sz, ctypes.c_uint32, _u64p]),
     "vlp_program_intermediate_offset": (_i, [_vp, _u64p]),
+    "vlp_program_level_jobs": (_i, [_vp, ctypes.c_uint32, ctypes.POINTER(VlpBrJob), _u64p, ctypes.POINTER(VlpKsJob),
+                                    _u64p]),
     "vlp_program_eval": (_i, [_vp, _vp, _sz, _vp, _vp, _vp, _u64]),
     "vlp_program_profile": (_i, [_vp, _i]),
     "vlp_program_profile_read": (_i, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),

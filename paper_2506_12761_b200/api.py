@@ -311,6 +311,21 @@ class Program:
         check(lib().vlp_program_node_row(self.h, kind, record, bit, ctypes.byref(r)))
         return r.value
 
+    def level_jobs(self, level: int):
+        """(br jobs, ks jobs) of one level of the compiled schedule as numpy structured arrays with the fields
+        of vlp_br_job (x, y, k0, ax, ay, pad, row) and vlp_ks_job (n0, n1, add, out)."""
+        nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().vlp_program_level_jobs(self.h, level, None, ctypes.byref(nb), None, ctypes.byref(nk)))
+        br_t = np.dtype([("x", "<u4"), ("y", "<u4"), ("k0", "<u4"), ("ax", "i1"), ("ay", "i1"), ("pad", "<u2"),
+                         ("row", "<u4")])
+        ks_t = np.dtype([("n0", "<u4"), ("n1", "<u4"), ("add", "<u4"), ("out", "<u4")])
+        br = np.zeros(max(1, nb.value), br_t)
+        ks = np.zeros(max(1, nk.value), ks_t)
+        check(lib().vlp_program_level_jobs(self.h, level, br.ctypes.data_as(ctypes.POINTER(L.VlpBrJob)),
+                                           ctypes.byref(nb), ks.ctypes.data_as(ctypes.POINTER(L.VlpKsJob)),
+                                           ctypes.byref(nk)))
+        return br[:nb.value], ks[:nk.value]
+
     def intermediate(self):
         """The intermediate-row region of the scratch as an int32 [rows, 632] view (parity dumps)."""
         off = ctypes.c_uint64()

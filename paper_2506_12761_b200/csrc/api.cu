@@ -408,6 +408,19 @@ int vlp_program_node_row(const vlp_program* p, int kind, size_t record, uint32_t
   return VLP_OK;
 }
 
+int vlp_program_level_jobs(const vlp_program* p, uint32_t level, vlp_br_job* br, uint64_t* nbr, vlp_ks_job* ks,
+                           uint64_t* nks) {
+  static_assert(sizeof(vlp_br_job) == sizeof(BrJob) && sizeof(vlp_ks_job) == sizeof(KsJob), "job layout");
+  if (!p || !nbr || !nks) return fail(VLP_EINVAL, "null argument");
+  if (level >= p->sched.levels.size()) return fail(VLP_EINVAL, "no such level");
+  const Level& lv = p->sched.levels[level];
+  *nbr = lv.br.size();
+  *nks = lv.ks.size();
+  if (br) std::memcpy(br, lv.br.data(), lv.br.size() * sizeof(BrJob));
+  if (ks) std::memcpy(ks, lv.ks.data(), lv.ks.size() * sizeof(KsJob));
+  return VLP_OK;
+}
+
 int vlp_program_intermediate_offset(const vlp_program* p, uint64_t* off) {
   if (!p || !off) return fail(VLP_EINVAL, "null argument");
   *off = p->off_mid;

@@ -241,6 +241,9 @@ def _full_size_sampled(server, cfg, sample):
         assert np.array_equal(mid[prog.node_row(0, i), :631], v), ("v", i)
         for j in range(wl.l_S):
             assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j]), ("mask", i, j)
+    # plus pure-function parity of 4 random gates of every level (SURVEY 4 layer 3)
+    regions = {0: q, 1: db, 2: mid, 3: out}
+    assert _gate_checks(prog, regions, okeys, per_level=4, seed=cfg) >= 4 * (prog.info.levels - 6)
     return wl, want
 
 
@@ -497,3 +500,69 @@ def test_device_encrypt_db_equals_host(server, cfg, count):
     dev = A.encrypt_db_device(k, m, recs, pays, pk_seed=77, first=first, count=count)
     torch.cuda.synchronize()
     assert np.array_equal(A.to_host(dev), host)
+
+
+# ------------------------------------------------------------------ pure-function parity of every gate
+_FORMS = {(0xE0000000, 1, 1): O.AND, (0x20000000, -1, -1): O.NAND, (0x20000000, 1, 1): O.OR,
+          (0x40000000, 2, 2): O.XOR, (0xC0000000, -2, -2): O.XNOR}
+
+
+def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
+    """For every key switch (= gate output) of the chosen levels: rebuild the gate from the schedule's jobs
+    (linear form -> op; two half bootstraps -> MUX), recompute it with the oracle from the GPU's own input
+    ciphertexts and compare with the GPU's output ciphertext.  Returns the number of gates checked."""
+    rng = random.Random(seed)
+
+    def ct(slot):
+        return regions[slot >> 28][slot & 0x0FFFFFFF, :631]
+
+    todo = []
+    jobs = [prog.level_jobs(lvl) for lvl in range(prog.info.levels)]
+    nrows = sum(len(b) for b, _ in jobs)
+    by_row = np.zeros(nrows, jobs[0][0].dtype)  # N-LWE row -> its bootstrap job (rows are unique)
+    for b, _ in jobs:
+        by_row[b["row"]] = b
+    for lvl in (range(prog.info.levels) if levels is None else levels):
+        ks = jobs[lvl][1]
+        idx = range(len(ks)) if per_level is None or len(ks) <= per_level else rng.sample(range(len(ks)), per_level)
+        for i in idx:
+            k = ks[i]
+            if int(k["n1"]) == 0xFFFFFFFF:
+                j = by_row[int(k["n0"])]
+                op = _FORMS[(int(j["k0"]), int(j["ax"]), int(j["ay"]))]
+                todo.append((int(k["out"]), "gate", op, int(j["x"]), int(j["y"])))
+            else:
+                j1, j2 = by_row[int(k["n0"])], by_row[int(k["n1"])]
+                assert (int(j1["k0"]), int(j1["ax"]), int(j1["ay"])) == (0xE0000000, 1, 1)
+                assert (int(j2["k0"]), int(j2["ax"]), int(j2["ay"])) == (0xE0000000, -1, 1)
+                assert int(j1["x"]) == int(j2["x"])
+                todo.append((int(k["out"]), "mux", int(j1["x"]), int(j1["y"]), int(j2["y"])))
+
+    def one(t):
+        if t[1] == "gate":
+            return okeys.gate(t[2], ct(t[3]), ct(t[4]))
+        return okeys.mux(ct(t[2]), ct(t[3]), ct(t[4]))
+
+    for t, want in zip(todo, POOL.map(one, todo)):
+        assert np.array_equal(ct(t[0]), want), t
+    return len(todo)
+
+
+def test_config1_every_gate_pure_function(server):
+    """SURVEY 4 layer 3: every one of config 1's 188 gate outputs (every level) is byte-equal to the oracle's
+    gate recomputed from the GPU's own inputs."""
+    wl = make_workload(1, key_seed=SEED)
+    prog, q, db, out = _run_config(server, wl)
+    okeys = O.OracleKeys(SEED)
+    regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
+    assert _gate_checks(prog, regions, okeys) == 188
+
+
+def test_config2_sampled_gates_pure_function(server):
+    """SURVEY 4 layer 3 at full size: 16 random gates of each of config 2's 29 levels (all of the narrow
+    tree levels) are recomputed by the oracle from the GPU's own input ciphertexts and byte-equal."""
+    wl = make_workload(2, key_seed=SEED)
+    prog, q, db, out = _run_config(server, wl)
+    okeys = O.OracleKeys(SEED)
+    regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
+    assert _gate_checks(prog, regions, okeys, per_level=16, seed=3) >= 16 * 25
