@@ -393,22 +393,18 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
         for (int j = 0; j < 3; j++) tmem_ld8(tm + 64 + 8 * j, d0[j]);
         tmem_wait_ld();
         // MAC: mac[o][s] = sum_{q<6} Dhat_q[s] * B[q][o][s] (Montgomery, one REDC per output; the key holds
-        // N^-1 * 2^32).  T < 6p^2 and T + m p < 2^64; output < 2.5p.
+        // N^-1 * 2^32).  Inputs in [0, 2p): T < 12p^2 < 2^63.6, T + m p < 2^64, output < (12p/2^32 + 1)p < 4p.
 #pragma unroll
         for (int pp = 0; pp < kChunks; pp++) {
           mbar_wait(&mbar[sl], ph);
           const uint32_t* rec = ring + sl * kBT * kChunkWords + t * kChunkWords;
-          uint32_t x[2][6];  // the 6 transformed digit polynomials at positions 2pp + e, reduced to [0, p)
+          uint32_t x[2][6];  // the 6 transformed digit polynomials at positions 2pp + e, reduced to [0, 2p)
 #pragma unroll
           for (int e = 0; e < 2; e++)
 #pragma unroll
             for (int j = 0; j < 3; j++) {
-              uint32_t v = d0[j][2 * pp + e];
-              v = umin(v, v - P2);
-              x[e][j] = umin(v, v - P);
-              v = d[j][2 * pp + e];
-              v = umin(v, v - P2);
-              x[e][3 + j] = umin(v, v - P);
+              x[e][j] = umin(d0[j][2 * pp + e], d0[j][2 * pp + e] - P2);
+              x[e][3 + j] = umin(d[j][2 * pp + e], d[j][2 * pp + e] - P2);
             }
 #pragma unroll
           for (int o = 0; o < 6; o++) {
@@ -457,7 +453,7 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
 #pragma unroll
         for (int l = 0; l < 3; l++)
 #pragma unroll
-          for (int s = 0; s < 8; s++) d[l][s] = umin(d[l][s], d[l][s] - P2);  // [0, 2p) (mac < 2.5p)
+          for (int s = 0; s < 8; s++) d[l][s] = umin(d[l][s], d[l][s] - P2);  // [0, 2p) (mac < 4p)
         stage9_inv(d, t, twi, zr);
         stage_BC<8, true>(d, twi, zr);
         stage_BC<7, true>(d, twi, zr);
