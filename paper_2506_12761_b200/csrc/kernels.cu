@@ -61,9 +61,11 @@ __device__ __forceinline__ uint32_t add_alu(uint32_t a, uint32_t b, uint32_t zer
 struct Rc {
   uint32_t z, p2;
 };
-// Forward CT butterfly, inputs / outputs in [0, 4p).
+// Forward CT butterfly, inputs / outputs in [0, 4p).  X_SMALL: x is known to be < 2p already (stage 0 on
+// gadget digits, which enter as p + d with |d| <= 64), so its conditional subtraction is skipped.
+template <bool X_SMALL = false>
 __device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t w, uint32_t ws, Rc z) {
-  const uint32_t xr = umin(x, x - P2);
+  const uint32_t xr = X_SMALL ? x : umin(x, x - P2);
   const uint32_t t = shoup(y, w, ws);
   x = add_alu(xr, t, z.z);
   y = xr - t + z.p2;
@@ -179,7 +181,7 @@ __device__ __forceinline__ void stage_A(uint32_t (&d)[NP][8], Rc z) {
 #pragma unroll
     for (int p = 0; p < NP; p++) {
       if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
-      else ct_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
+      else ct_bfly<S == 0>(d[p][r], d[p][r | rb], w.x, w.y, z);
     }
   }
 }
