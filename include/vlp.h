@@ -247,7 +247,8 @@ int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t*
  * of two): the query's l_S result ciphertexts to out_dev (R15). */
 int vlp_server_combine(vlp_server* server, const vlp_meta* meta, uint32_t G, const uint32_t* partials_dev,
                        uint32_t* out_dev, void* scratch_dev, size_t scratch_bytes, uint64_t stream);
-/* Scratch bytes of vlp_gate_batch (includes room to stage b and c contiguously for VLP_MUX). */
+/* Scratch bytes of vlp_gate_batch (includes room to stage b and c contiguously for VLP_MUX); 0 for an empty
+ * batch, which vlp_gate_batch accepts as a no-op. */
 int vlp_gate_batch_workspace_bytes(int op, size_t count, size_t* scratch_bytes);
 /* A batch of `count` independent gates (BASELINE config 5): out[i] = op(a[i], b[i]), or for VLP_MUX
  * out[i] = MUX(a[i], b[i], c[i]) = a ? b : c (R10).  c_dev is ignored unless op == VLP_MUX. */

@@ -533,7 +533,8 @@ size_t vlp_debug_scratch_bytes(size_t count) {
 
 int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, int steps, uint32_t* acc_dev,
                            void* scratch, uint64_t stream) {
-  if (!s || !in_dev || !acc_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (!s || !scratch || (count && (!in_dev || !acc_dev))) return fail(VLP_EINVAL, "null argument");
+  if (count == 0) return VLP_OK;
   if (steps < 0 || steps > n) return fail(VLP_EINVAL, "steps out of range");
   cudaError_t e;
   if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
@@ -558,7 +559,8 @@ int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, 
 
 int vlp_debug_keyswitch(vlp_server* s, const uint32_t* nlwe_dev, size_t count, uint32_t* out_dev, void* scratch,
                         uint64_t stream) {
-  if (!s || !nlwe_dev || !out_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (!s || !scratch || (count && (!nlwe_dev || !out_dev))) return fail(VLP_EINVAL, "null argument");
+  if (count == 0) return VLP_OK;
   cudaError_t e;
   if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -670,6 +672,10 @@ int vlp_server_combine(vlp_server* s, const vlp_meta* meta, uint32_t G, const ui
 
 int vlp_gate_batch_workspace_bytes(int op, size_t count, size_t* scratch_bytes) {
   if (!scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  if (count == 0) {  // an empty batch needs no scratch (vlp_gate_batch is a no-op)
+    *scratch_bytes = 0;
+    return VLP_OK;
+  }
   vlp_program* p = nullptr;
   if (int rc = vlp_program_create_gates(nullptr, op, count, &p)) return rc;
   *scratch_bytes = align256(p->bytes) + gate_stage_bytes(op, count);

@@ -566,3 +566,31 @@ def test_config2_sampled_gates_pure_function(server):
     okeys = O.OracleKeys(SEED)
     regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
     assert _gate_checks(prog, regions, okeys, per_level=16, seed=3) >= 16 * 25
+
+
+def test_nand_max_config5_size_sampled(server, okeys):
+    """Config 5's largest batch (2^20 NAND gates on one GPU): every output decrypts to NAND of its inputs, and
+    sampled outputs (incl. the first and last) are byte-equal to the oracle's gate."""
+    count = 1 << 20
+    a_bits, b_bits = nand_inputs(count, 91)
+    k = server.keys
+    a = k.encrypt_bits(a_bits, 4005, 0)
+    b = k.encrypt_bits(b_bits, 4005, count)
+    out = torch.zeros((count, 632), dtype=torch.int32, device="cuda:0")
+    server.gate_batch(L.NAND, A.to_device(a), A.to_device(b), out)
+    torch.cuda.synchronize()
+    got = A.to_host(out)
+    assert np.array_equal(k.decrypt_bits(got), 1 - (a_bits & b_bits))
+    idx = [0, count - 1] + sorted(random.Random(9).sample(range(1, count - 1), 14))
+    want = list(POOL.map(lambda i: okeys.gate(O.NAND, a[i, :631], b[i, :631]), idx))
+    for i, w in zip(idx, want):
+        assert np.array_equal(got[i, :631], w), i
+
+
+def test_empty_inputs_are_no_ops(server):
+    """Degenerate sizes: an empty gate batch and an empty blind-rotation batch launch nothing and succeed."""
+    e = torch.zeros((0, 632), dtype=torch.int32, device="cuda:0")
+    server.gate_batch(L.NAND, e, e, e)
+    acc = server.debug_blind_rotate(e, 630)
+    torch.cuda.synchronize()
+    assert acc.shape[0] == 0
