@@ -594,3 +594,28 @@ def test_empty_inputs_are_no_ops(server):
     acc = server.debug_blind_rotate(e, 630)
     torch.cuda.synchronize()
     assert acc.shape[0] == 0
+
+
+def test_gate_truth_tables_100_trials(server, okeys):
+    """P5 at the SPEC's trial count: every gate type on every input combination, 100
+    independent fresh encryptions each (800 for MUX) -- zero decryption errors -- plus byte parity of the
+    first trial of each combination with the oracle."""
+    k = server.keys
+    f = {L.AND: lambda x, y: x & y, L.NAND: lambda x, y: 1 - (x & y), L.OR: lambda x, y: x | y,
+         L.XOR: lambda x, y: x ^ y, L.XNOR: lambda x, y: 1 - (x ^ y)}
+    for op in (L.AND, L.NAND, L.OR, L.XOR, L.XNOR, L.MUX):
+        combos = [(x, y, z) for x in (0, 1) for y in (0, 1) for z in ((0, 1) if op == L.MUX else (0,))]
+        bits = np.array([c for c in combos for _ in range(100)], np.uint8).T  # [3][n]
+        n = bits.shape[1]
+        a, b, c = (k.encrypt_bits(bits[i], 6000 + 10 * op + i, 0) for i in range(3))
+        out = torch.zeros((n, 632), dtype=torch.int32, device="cuda:0")
+        server.gate_batch(op, A.to_device(a), A.to_device(b), out, c_dev=A.to_device(c) if op == L.MUX else None)
+        torch.cuda.synchronize()
+        got = A.to_host(out)
+        truth = np.where(bits[0] == 1, bits[1], bits[2]) if op == L.MUX else f[op](bits[0], bits[1])
+        assert np.array_equal(k.decrypt_bits(got), truth), op
+        firsts = list(range(0, n, 100))
+        want = list(POOL.map(lambda i: okeys.mux(a[i, :631], b[i, :631], c[i, :631]) if op == L.MUX
+                             else okeys.gate(op, a[i, :631], b[i, :631]), firsts))
+        for i, w in zip(firsts, want):
+            assert np.array_equal(got[i, :631], w), (op, i)
