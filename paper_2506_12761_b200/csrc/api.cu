@@ -3,7 +3,9 @@
 // and the debug entry points used by the parity tests.
 #include <cublasLt.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -461,8 +463,17 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
   const Regions reg = regions(p, scratch, in0, in1, out);
   if ((e = launch_init_constants(reg.base[kRegMid], st))) return cuda_fail(e, "init constants");
   uint32_t* nlwe = reinterpret_cast<uint32_t*>(sc + p->off_nlwe);
+  struct NvtxLevel {  // one NVTX range per circuit level (host-side launch span; nsys / ncu show it)
+    explicit NvtxLevel(size_t L, size_t br, size_t ks) {
+      char name[96];
+      snprintf(name, sizeof(name), "vlp level %zu: %zu BR, %zu KS", L, br, ks);
+      nvtxRangePushA(name);
+    }
+    ~NvtxLevel() { nvtxRangePop(); }
+  };
   for (size_t L = 0; L < p->sched.levels.size(); L++) {
     const Level& lv = p->sched.levels[L];
+    const NvtxLevel range(L, lv.br.size(), lv.ks.size());
     BrArgs ba{};
     ba.jobs = reinterpret_cast<const BrJob*>(sc + p->off_br) + p->br_first[L];
     ba.njobs = static_cast<uint32_t>(lv.br.size());

@@ -619,3 +619,21 @@ def test_gate_truth_tables_100_trials(server, okeys):
                              else okeys.gate(op, a[i, :631], b[i, :631]), firsts))
         for i, w in zip(firsts, want):
             assert np.array_equal(got[i, :631], w), (op, i)
+
+
+def test_mismatched_evaluation_key_is_detectable(server):
+    """Failure detection: bootstrapping a key-A ciphertext with key B's evaluation key gives
+    garbage -- about half of the decrypted NAND outputs are wrong -- while the matching key gives none."""
+    other = A.Server(A.Keys(SEED + 1000), 0)
+    k = server.keys
+    count = 740
+    a_bits, b_bits = nand_inputs(count, 17)
+    a = A.to_device(k.encrypt_bits(a_bits, 7001, 0))
+    b = A.to_device(k.encrypt_bits(b_bits, 7001, count))
+    want = 1 - (a_bits & b_bits)
+    for srv, lo, hi in ((server, 0.0, 0.0), (other, 0.3, 0.7)):
+        out = torch.zeros((count, 632), dtype=torch.int32, device="cuda:0")
+        srv.gate_batch(L.NAND, a, b, out)
+        torch.cuda.synchronize()
+        err = float(np.mean(k.decrypt_bits(A.to_host(out)) != want))
+        assert lo <= err <= hi, err
