@@ -186,6 +186,22 @@ __device__ __forceinline__ void stage_A(uint32_t (&d)[NP][8], Rc z) {
   }
 }
 
+// Stage 0 of the forward transform on gadget digits: y = p + d with d in [-64, 64) (field f = d + 64), so
+// w0 * y mod p = T[f] from a 128-entry shared table (T[f] = w0 (f - 64) mod p) instead of a Shoup product
+// (an LDS instead of IMAD.HI + 2 IMAD on the heavy pipe).  x < 2p (digits), outputs < 3p.
+template <int NP>
+__device__ __forceinline__ void stage0_digits(uint32_t (&d)[NP][8], const uint32_t* __restrict__ t0, Rc z) {
+#pragma unroll
+  for (int r = 0; r < 4; r++)
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+      const uint32_t x = d[p][r];
+      const uint32_t t = t0[d[p][r + 4] - (P - 64u)];
+      d[p][r] = add_alu(x, t, z.z);
+      d[p][r + 4] = x - t + z.p2;
+    }
+}
+
 // Lane-varying stages 3-8: layout B (S = 3..5) or C (S = 6..8); rb = 4 >> (S % 3); twiddle slot
 // q = r >> (3 - S % 3) at table row kSlotBase[S] + q, column t.
 template <int S, bool INV, int NP>
@@ -278,7 +294,8 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
   uint32_t* acc_all = ring + kSlots * kBT * kChunkWords;
   uint32_t* xb_all = acc_all + kBrBoot * 2 * N;
   uint16_t* abar_all = reinterpret_cast<uint16_t*>(xb_all + kBrBoot * 3 * N);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(abar_all + kBrBoot * 640);
+  uint32_t* t0tab = reinterpret_cast<uint32_t*>(abar_all + kBrBoot * 640);  // [128] stage-0 digit products
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(t0tab + 128);
   uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kSlots);  // per-slot release counters (warps)
   uint32_t* tmem_base_sh = rel + kSlots;
 
@@ -301,6 +318,10 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
       rel[s] = 0;
     }
     fence_mbar_init();
+  }
+  if (tid < 128) {
+    const uint64_t w0 = c_tw[0][1].x;  // the stage-0 twiddle
+    t0tab[tid] = static_cast<uint32_t>(w0 * ((tid + P - 64u) % P) % P);
   }
   if (tid < 32) {  // warp 0 allocates the CTA's TMEM (one CTA per SM: smem-bound)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
@@ -372,7 +393,7 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
           d[1][r] = ((w >> 18) & 127u) + (P - 64u);
           d[2][r] = ((w >> 11) & 127u) + (P - 64u);
         }
-        stage_A<0, false>(d, zr);
+        stage0_digits(d, t0tab, zr);
         stage_A<1, false>(d, zr);
         stage_A<2, false>(d, zr);
         exchange<0, 1>(d, xb, t, g);
@@ -519,7 +540,7 @@ constexpr int kLatSlots = 4;  // a whole CMux step of bsk chunks in flight: a lo
 constexpr int kLatThreads = kLatGroups * kBT;
 constexpr int kLatTmemCols = 128;
 __host__ __device__ constexpr int lat_smem_bytes() {
-  return kLatSlots * kChunkBytes + (2 * N * 4 + kLatGroups * N * 4 + 640 * 2) + kLatSlots * 8 + kLatSlots * 4 + 8;
+  return kLatSlots * kChunkBytes + (2 * N * 4 + kLatGroups * N * 4 + 640 * 2) + 128 * 4 + kLatSlots * 8 + kLatSlots * 4 + 8;
 }
 
 __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(const BrArgs a) {
@@ -528,7 +549,8 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
   uint32_t* acc = ring + kLatSlots * kBT * kChunkWords;
   uint32_t* xb_all = acc + 2 * N;  // [group 6][N]
   uint16_t* abar = reinterpret_cast<uint16_t*>(xb_all + kLatGroups * N);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(abar + 640);
+  uint32_t* t0tab = reinterpret_cast<uint32_t*>(abar + 640);  // [128] stage-0 digit products
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(t0tab + 128);
   uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kLatSlots);
   uint32_t* tmem_base_sh = rel + kLatSlots;
 
@@ -547,6 +569,10 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
       rel[s] = 0;
     }
     fence_mbar_init();
+  }
+  if (tid < 128) {
+    const uint64_t w0 = c_tw[0][1].x;  // the stage-0 twiddle
+    t0tab[tid] = static_cast<uint32_t>(w0 * ((tid + P - 64u) % P) % P);
   }
   if (tid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
@@ -615,7 +641,7 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
           const uint32_t w = v - acc[uc * N + j] + 0x81020400u;
           d[0][r] = ((w >> dshift) & 127u) + (P - 64u);
         }
-        stage_A<0, false>(d, zr);
+        stage0_digits(d, t0tab, zr);
         stage_A<1, false>(d, zr);
         stage_A<2, false>(d, zr);
         exchange<0, 1>(d, xb, t, G);
@@ -757,7 +783,7 @@ constexpr int kClatGroups = 3;
 constexpr int kClatThreads = kClatGroups * kBT;
 constexpr int kClatTmemCols = 32;
 __host__ __device__ constexpr int clat_smem_bytes() {
-  return kLatSlots * kChunkBytes + (N * 4 + kClatGroups * N * 4 + 2 * 3 * N * 4 + 640 * 2) + kLatSlots * 8 +
+  return kLatSlots * kChunkBytes + (N * 4 + kClatGroups * N * 4 + 2 * 3 * N * 4 + 640 * 2) + 128 * 4 + kLatSlots * 8 +
          kLatSlots * 4 + 8;
 }
 
@@ -769,7 +795,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
   uint32_t* xb_all = acc + N;                            // [group 3][N]
   uint32_t* dig = xb_all + kClatGroups * N;              // [buf 2][q 3][slot 8][thread 128]
   uint16_t* abar = reinterpret_cast<uint16_t*>(dig + 2 * 3 * N);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(abar + 640);
+  uint32_t* t0tab = reinterpret_cast<uint32_t*>(abar + 640);  // [128] stage-0 digit products
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(t0tab + 128);
   uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kLatSlots);
   uint32_t* tmem_base_sh = rel + kLatSlots;
 
@@ -792,6 +819,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
       rel[s] = 0;
     }
     fence_mbar_init();
+  }
+  if (tid < 128) {
+    const uint64_t w0 = c_tw[0][1].x;  // the stage-0 twiddle
+    t0tab[tid] = static_cast<uint32_t>(w0 * ((tid + P - 64u) % P) % P);
   }
   if (tid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
@@ -849,7 +880,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
           const uint32_t w = v - acc[j] + 0x81020400u;
           d[0][r] = ((w >> dshift) & 127u) + (P - 64u);
         }
-        stage_A<0, false>(d, zr);
+        stage0_digits(d, t0tab, zr);
         stage_A<1, false>(d, zr);
         stage_A<2, false>(d, zr);
         exchange<0, 1>(d, xb, t, G);

@@ -23,7 +23,7 @@ constexpr size_t kBskNttWords = static_cast<size_t>(n) * kChunks * kBT * kChunkW
 // shared memory of a blind-rotate CTA with B bootstraps: bsk ring + per bootstrap (accumulator, exchange
 // buffer, mod-switched mask) + mbarriers, release counters, TMEM base
 __host__ __device__ constexpr int br_smem_bytes(int B) {
-  return kSlots * kChunkBytes + B * (2 * N * 4 + 3 * N * 4 + 640 * 2) + kSlots * 8 + kSlots * 4 + 8;
+  return kSlots * kChunkBytes + B * (2 * N * 4 + 3 * N * 4 + 640 * 2) + 128 * 4 + kSlots * 8 + kSlots * 4 + 8;
 }
 constexpr int kBrSmemBytes = br_smem_bytes(kBrBoot);
 // TMEM (tcgen05.ld/st, no MMA) as per-thread spill space: per warp slot 96 columns -- MAC outputs of
