@@ -389,7 +389,10 @@ def main():
         if rank == 0:
             check_all(out_pin.numpy().view(np.uint32))
         e2e = {"value": nq * br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": nq * wl.M / (e2e_ms / 1e3),
-               "h2d_bytes_per_step": int(q_host.nbytes), "d2h_bytes_per_step": int(nq * wl.l_S * 632 * 4)}
+               # the query, plus the job tables every server_eval / combine copies into its scratch
+               "h2d_bytes_per_step": int(q_host.nbytes) + int(prog.info.table_bytes)
+                                     + (int(comb.info.table_bytes) if comb else 0),
+               "d2h_bytes_per_step": int(nq * wl.l_S * 632 * 4)}
 
     if rank == 0:
         peak, peak_how = int_peak()

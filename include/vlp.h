@@ -90,6 +90,7 @@ typedef struct {
   uint64_t scratch_bytes;   /* device scratch the caller must provide */
   uint64_t max_level_br;    /* widest level */
   uint32_t kernel_launches; /* kernels launched per evaluation */
+  uint64_t table_bytes;     /* job tables every evaluation copies host -> device into scratch */
 } vlp_program_info;
 
 const char* vlp_last_error(void);
@@ -196,9 +197,10 @@ int vlp_program_level_jobs(const vlp_program* prog, uint32_t level, vlp_br_job* 
 int vlp_program_intermediate_offset(const vlp_program* prog, uint64_t* byte_offset);
 
 /* Evaluate the program on `stream` (asynchronous).  scratch_dev: >= info.scratch_bytes of device
- * memory (job arrays are uploaded into it on the first call with a given scratch pointer; it also holds the
- * intermediates, the N-LWE staging and the key-switch GEMM staging, so two evaluations in flight at the same
- * time need two scratch buffers). */
+ * memory.  Every call first copies the program's job tables (info.table_bytes, from a pinned host image the
+ * library keeps) into the scratch on `stream`, so no state carries over between calls and one buffer may
+ * serve several programs in turn; the scratch also holds the intermediates, the N-LWE staging and the
+ * key-switch GEMM staging, so two evaluations in flight at the same time need two scratch buffers. */
 int vlp_program_eval(vlp_program* prog, void* scratch_dev, size_t scratch_bytes, const uint32_t* in0_dev,
                      const uint32_t* in1_dev, uint32_t* out_dev, uint64_t stream);
 

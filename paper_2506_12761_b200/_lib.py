@@ -37,7 +37,8 @@ class VlpProgramInfo(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_uint32), ("br", ctypes.c_uint64), ("ks", ctypes.c_uint64),
                 ("gates", ctypes.c_uint64), ("in0_cts", ctypes.c_uint64), ("in1_cts", ctypes.c_uint64),
                 ("out_cts", ctypes.c_uint64), ("scratch_bytes", ctypes.c_uint64),
-                ("max_level_br", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint32)]
+                ("max_level_br", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint32),
+                ("table_bytes", ctypes.c_uint64)]
 
 
 class VlpBrJob(ctypes.Structure):

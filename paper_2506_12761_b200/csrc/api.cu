@@ -44,7 +44,11 @@ struct vlp_program {
   uint32_t ks_chunk = 0;
   std::vector<size_t> br_first, ks_first;  // per level, index of the level's first job
   std::vector<uint32_t> copy_slots;        // outputs that are not written in place
-  void* bound = nullptr;
+  // host image of the scratch's job-table region [0, off_mid) in pinned memory (allocated on the first
+  // evaluation), copied into the caller's scratch by every evaluation: nothing is assumed about what a
+  // scratch buffer held before, so one buffer may serve several programs in turn
+  std::mutex tables_mu;
+  uint8_t* tables = nullptr;
   uint32_t launches = 0;
   // optional per-kernel timing with CUDA events recorded on the launch stream (vlp_program_profile)
   bool profile = false;
@@ -53,6 +57,7 @@ struct vlp_program {
   double br_ms = 0, ks_ms = 0;
   uint64_t br_launches = 0, ks_launches = 0;
   ~vlp_program() {
+    if (tables) cudaFreeHost(tables);
     for (auto& e : pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : pool) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   }
@@ -350,34 +355,55 @@ static int finish_program(vlp_server* server, std::unique_ptr<vlp_program>& p, v
   *out = p.release();
   return VLP_OK;
 }
+// No C++ exception crosses the C ABI: allocation failures while compiling become VLP_ENOMEM.
+extern "C++" {
+template <class F>
+static int no_throw(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(VLP_ENOMEM, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(VLP_EINVAL, e.what());
+  }
+}
+}  // extern "C++"
 
 int vlp_program_create(vlp_server* server, const vlp_meta* meta, size_t first, size_t count, vlp_program** out) {
   if (!meta || !out) return fail(VLP_EINVAL, "null argument");  // server may be NULL: compile only
-  auto p = std::make_unique<vlp_program>();
-  if (int rc = compile_velopir(*meta, first, count, &p->sched)) return rc;
-  return finish_program(server, p, out);
+  return no_throw([&] {
+    auto p = std::make_unique<vlp_program>();
+    if (int rc = compile_velopir(*meta, first, count, &p->sched)) return rc;
+    return finish_program(server, p, out);
+  });
 }
 
 int vlp_program_create_queries(vlp_server* server, const vlp_meta* meta, size_t first, size_t count, uint32_t nq,
                                vlp_program** out) {
   if (!meta || !out) return fail(VLP_EINVAL, "null argument");
-  auto p = std::make_unique<vlp_program>();
-  if (int rc = compile_velopir(*meta, first, count, &p->sched, nq)) return rc;
-  return finish_program(server, p, out);
+  return no_throw([&] {
+    auto p = std::make_unique<vlp_program>();
+    if (int rc = compile_velopir(*meta, first, count, &p->sched, nq)) return rc;
+    return finish_program(server, p, out);
+  });
 }
 
 int vlp_program_create_gates(vlp_server* server, int op, size_t count, vlp_program** out) {
   if (!out) return fail(VLP_EINVAL, "null argument");
-  auto p = std::make_unique<vlp_program>();
-  if (int rc = compile_gates(op, count, &p->sched)) return rc;
-  return finish_program(server, p, out);
+  return no_throw([&] {
+    auto p = std::make_unique<vlp_program>();
+    if (int rc = compile_gates(op, count, &p->sched)) return rc;
+    return finish_program(server, p, out);
+  });
 }
 
 int vlp_program_create_combine(vlp_server* server, const vlp_meta* meta, uint32_t G, vlp_program** out) {
   if (!meta || !out) return fail(VLP_EINVAL, "null argument");
-  auto p = std::make_unique<vlp_program>();
-  if (int rc = compile_combine(*meta, G, &p->sched)) return rc;
-  return finish_program(server, p, out);
+  return no_throw([&] {
+    auto p = std::make_unique<vlp_program>();
+    if (int rc = compile_combine(*meta, G, &p->sched)) return rc;
+    return finish_program(server, p, out);
+  });
 }
 
 int vlp_program_get_info(const vlp_program* p, vlp_program_info* info) {
@@ -393,6 +419,7 @@ int vlp_program_get_info(const vlp_program* p, vlp_program_info* info) {
   info->scratch_bytes = p->bytes;
   for (auto& L : p->sched.levels) info->max_level_br = std::max<uint64_t>(info->max_level_br, L.br.size());
   info->kernel_launches = p->launches;
+  info->table_bytes = p->off_mid;
   return VLP_OK;
 }
 
@@ -429,6 +456,25 @@ int vlp_program_intermediate_offset(const vlp_program* p, uint64_t* off) {
   return VLP_OK;
 }
 
+extern "C++" {
+// Build the pinned host image of the job tables once per program (thread-safe).
+static int stage_tables(vlp_program* p) {
+  std::lock_guard<std::mutex> lock(p->tables_mu);
+  if (p->tables) return VLP_OK;
+  uint8_t* h = nullptr;
+  if (cudaError_t e = cudaMallocHost(&h, std::max<size_t>(p->off_mid, 1))) return cuda_fail(e, "pinned job tables");
+  std::memset(h, 0, p->off_mid);
+  for (size_t L = 0; L < p->sched.levels.size(); L++) {
+    const Level& lv = p->sched.levels[L];
+    if (!lv.br.empty()) std::memcpy(h + p->off_br + p->br_first[L] * sizeof(BrJob), lv.br.data(), lv.br.size() * sizeof(BrJob));
+    if (!lv.ks.empty()) std::memcpy(h + p->off_ks + p->ks_first[L] * sizeof(KsJob), lv.ks.data(), lv.ks.size() * sizeof(KsJob));
+  }
+  if (!p->copy_slots.empty()) std::memcpy(h + p->off_outslots, p->copy_slots.data(), p->copy_slots.size() * 4);
+  p->tables = h;
+  return VLP_OK;
+}
+}  // extern "C++"
+
 int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const uint32_t* in0,
                      const uint32_t* in1, uint32_t* out, uint64_t stream) {
   if (!p || !scratch) return fail(VLP_EINVAL, "null argument");
@@ -441,25 +487,10 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
   if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* sc = static_cast<uint8_t*>(scratch);
-  if (p->bound != scratch) {  // upload the job arrays once per scratch buffer
-    for (size_t L = 0; L < p->sched.levels.size(); L++) {
-      const Level& lv = p->sched.levels[L];
-      if (!lv.br.empty() &&
-          (e = cudaMemcpyAsync(sc + p->off_br + p->br_first[L] * sizeof(BrJob), lv.br.data(),
-                               lv.br.size() * sizeof(BrJob), cudaMemcpyHostToDevice, st)))
-        return cuda_fail(e, "upload br jobs");
-      if (!lv.ks.empty() &&
-          (e = cudaMemcpyAsync(sc + p->off_ks + p->ks_first[L] * sizeof(KsJob), lv.ks.data(),
-                               lv.ks.size() * sizeof(KsJob), cudaMemcpyHostToDevice, st)))
-        return cuda_fail(e, "upload ks jobs");
-    }
-    if (!p->copy_slots.empty() &&
-        (e = cudaMemcpyAsync(sc + p->off_outslots, p->copy_slots.data(), p->copy_slots.size() * 4,
-                             cudaMemcpyHostToDevice, st)))
-      return cuda_fail(e, "upload out slots");
-    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "upload sync");
-    p->bound = scratch;
-  }
+  if (int rc = stage_tables(p)) return rc;
+  // the job tables into this scratch, every evaluation (asynchronous, from pinned memory, stream-ordered
+  // before the kernels that read them; 20 B per BR + 16 B per KS)
+  if ((e = cudaMemcpyAsync(sc, p->tables, p->off_mid, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "upload jobs");
   const Regions reg = regions(p, scratch, in0, in1, out);
   if ((e = launch_init_constants(reg.base[kRegMid], st))) return cuda_fail(e, "init constants");
   uint32_t* nlwe = reinterpret_cast<uint32_t*>(sc + p->off_nlwe);
@@ -603,15 +634,17 @@ static std::string meta_key(const char* kind, const vlp_meta& m, size_t a, size_
 
 template <class Make>
 static int cached_program(vlp_server* s, const std::string& key, Make make, vlp_program** out) {
-  std::lock_guard<std::mutex> lock(s->mu);
-  auto it = s->cache.find(key);
-  if (it == s->cache.end()) {
-    vlp_program* p = nullptr;
-    if (int rc = make(&p)) return rc;
-    it = s->cache.emplace(key, std::unique_ptr<vlp_program>(p)).first;
-  }
-  *out = it->second.get();
-  return VLP_OK;
+  return no_throw([&] {
+    std::lock_guard<std::mutex> lock(s->mu);
+    auto it = s->cache.find(key);
+    if (it == s->cache.end()) {
+      vlp_program* p = nullptr;
+      if (int rc = make(&p)) return rc;
+      it = s->cache.emplace(key, std::unique_ptr<vlp_program>(p)).first;
+    }
+    *out = it->second.get();
+    return static_cast<int>(VLP_OK);
+  });
 }
 static size_t gate_stage_bytes(int op, size_t count) { return op == VLP_MUX ? 2 * count * kCt * 4 : 0; }
 }  // extern "C++"

@@ -6,6 +6,7 @@
 // support of the binary key z (the oracle uses an NTT), and are exact mod 2^32.
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <thread>
 
 #include "vlp_internal.h"
@@ -108,19 +109,27 @@ int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk
       return fail(VLP_EINVAL, "only the 128-bit parameter set of tab:tfhe_params is supported");
     p = *params;
   }
-  vlp_sk* sk = new (std::nothrow) vlp_sk;
-  vlp_evk* evk = new (std::nothrow) vlp_evk;
-  if (!sk || !evk) return fail(VLP_ENOMEM, "out of memory");
+  std::unique_ptr<vlp_sk> skp(new (std::nothrow) vlp_sk);
+  std::unique_ptr<vlp_evk> evkp(new (std::nothrow) vlp_evk);
+  if (!skp || !evkp) return fail(VLP_ENOMEM, "out of memory");
+  vlp_sk* sk = skp.get();
+  vlp_evk* evk = evkp.get();
+  try {  // the key vectors (124 MB): no exception crosses the C ABI
+    evk->bsk.assign(static_cast<size_t>(n) * kRows * 2 * N, 0);
+    evk->ksk.assign(static_cast<size_t>(N) * kKsT * 3 * kCt, 0);
+  } catch (const std::bad_alloc&) {
+    return fail(VLP_ENOMEM, "out of memory for the evaluation key");
+  }
   sk->params = p;
   evk->params = p;
   for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(prng(seed, kSkLwe, 0, i) >> 63);
   for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(prng(seed, kSkRing, 0, j) >> 63);
   std::vector<int> support;
+  support.reserve(N);
   for (int j = 0; j < N; j++)
     if (sk->z[j]) support.push_back(j);
 
   // bsk_i row r = u*3 + j: (a, a*z + e) + s_i * g_j on component u's constant term (R4, O7).
-  evk->bsk.assign(static_cast<size_t>(n) * kRows * 2 * N, 0);
   parallel_for(static_cast<size_t>(n) * kRows, [&](size_t ir) {
     const uint64_t obj = ir;
     uint32_t* a = evk->bsk.data() + ir * 2 * N;
@@ -138,15 +147,14 @@ int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk
   });
 
   // ksk[i][j][v] = TLWE_s(v z_i 2^(32-2(j+1))), sigma_ks (R6, O10).
-  evk->ksk.assign(static_cast<size_t>(N) * kKsT * 3 * kCt, 0);
   parallel_for(static_cast<size_t>(N) * kKsT * 3, [&](size_t idx) {
     const int i = static_cast<int>(idx / (kKsT * 3)), j = static_cast<int>((idx / 3) % kKsT);
     const uint32_t v = static_cast<uint32_t>(idx % 3) + 1;
     const uint32_t mu = v * sk->z[i] * (1u << (32 - kKsBaseBits * (j + 1)));
     tlwe_sample(sk->s, mu, p.sigma_ks, seed, kKskA, kKskE, idx, evk->ksk.data() + idx * kCt);
   });
-  *sk_out = sk;
-  *evk_out = evk;
+  *sk_out = skp.release();
+  *evk_out = evkp.release();
   return VLP_OK;
 }
 

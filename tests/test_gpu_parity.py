@@ -637,3 +637,29 @@ def test_mismatched_evaluation_key_is_detectable(server):
         torch.cuda.synchronize()
         err = float(np.mean(k.decrypt_bits(A.to_host(out)) != want))
         assert lo <= err <= hi, err
+
+
+@pytest.mark.gpu
+def test_shared_scratch_between_programs(server):
+    """One scratch buffer serving two programs in turn (AND, then XOR, then AND again), and a scratch filled
+    with garbage between calls: every evaluation reloads its own job tables, so the outputs stay the truth
+    tables (include/vlp.h vlp_program_eval)."""
+    count = 37
+    rng = np.random.default_rng(11)
+    bits = rng.integers(0, 2, (2, count), dtype=np.uint8)
+    k = server.keys
+    a = A.to_device(k.encrypt_bits(bits[0], 901, 0))
+    b = A.to_device(k.encrypt_bits(bits[1], 902, 0))
+    p_and = A.Program.gates(server, L.AND, count)
+    p_xor = A.Program.gates(server, L.XOR, count)
+    shared = torch.empty(max(p_and.info.scratch_bytes, p_xor.info.scratch_bytes), dtype=torch.uint8, device="cuda:0")
+    assert p_and.info.table_bytes >= count * 20 and p_xor.info.table_bytes >= count * 20
+    p_and.scratch = shared
+    p_xor.scratch = shared
+    want = {L.AND: bits[0] & bits[1], L.XOR: bits[0] ^ bits[1]}
+    for prog, op in [(p_and, L.AND), (p_xor, L.XOR), (p_and, L.AND), (p_xor, L.XOR)]:
+        out = torch.zeros((count, 632), dtype=torch.int32, device="cuda:0")
+        prog.eval(a, b, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(k.decrypt_bits(A.to_host(out)), want[op]), op
+        shared.random_(0, 256)  # whatever the buffer holds next time must not matter
