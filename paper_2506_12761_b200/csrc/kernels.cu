@@ -1260,6 +1260,7 @@ static cudaError_t launch_br_clat(const BrArgs& a, int sm_count, cudaStream_t st
   }
   if (a.njobs == 0) return cudaSuccess;
   const uint32_t half = static_cast<uint32_t>(sm_count / 2);
+  if (half == 0) return launch_br_lat(a, sm_count, st);  // a 2-CTA cluster needs two SMs
   const uint32_t clusters = a.njobs < half ? a.njobs : half;
   if ((static_cast<uint64_t>(a.njobs) + clusters - 1) / clusters * static_cast<uint64_t>(a.steps) * kChunks >= (1ull << 32))
     return cudaErrorInvalidValue;

@@ -23,6 +23,7 @@ namespace vlp {
 namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr size_t kMaxRows = size_t{1} << 28;  // rows addressable by a slot id (region << 28 | row)
 
 struct LinForm {
   uint32_t k0;
@@ -77,8 +78,13 @@ class Builder {
   uint32_t XOR(uint32_t x, uint32_t y) { return gate(VLP_XOR, x, y); }
   uint32_t XNOR(uint32_t x, uint32_t y) { return gate(VLP_XNOR, x, y); }
 
-  // Assign slots (outputs listed in `outs` go to the out region, in order) and emit the levels.
-  void finalize(const std::vector<uint32_t>& outs, Schedule* s) {
+  // Assign slots (outputs listed in `outs` go to the out region, in order) and emit the levels.  Slot ids
+  // hold a 28-bit row (slot()): a schedule with more intermediate rows is refused.
+  int finalize(const std::vector<uint32_t>& outs, Schedule* s) {
+    size_t gates = 0;
+    for (auto& nd : nodes) gates += nd.kind != 0;
+    if (gates + 2 > kMaxRows || outs.size() > kMaxRows)
+      return fail(VLP_EINVAL, "schedule too large: more than 2^28 ciphertext rows in one region");
     std::vector<uint32_t> out_index(nodes.size(), kNone);
     for (size_t j = 0; j < outs.size(); j++)
       if (nodes[outs[j]].kind != 0) out_index[outs[j]] = static_cast<uint32_t>(j);
@@ -115,6 +121,7 @@ class Builder {
     s->nlwe_rows = nl;
     s->out_cts = outs.size();
     for (uint32_t o : outs) s->out_slots.push_back(nodes[o].slot);
+    return VLP_OK;
   }
 
  private:
@@ -196,6 +203,8 @@ int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, 
   if (nq < 1 || nq > 4096) return fail(VLP_EINVAL, "query count must be in [1, 4096]");
   Builder B;
   const size_t l = m.l_I, W = record_words(m), QW = query_words(m), per = W * l + m.l_S;
+  if (count * per > kMaxRows || static_cast<size_t>(nq) * QW * l > kMaxRows)
+    return fail(VLP_EINVAL, "shard too large: more than 2^28 input ciphertexts");
   // the shard's record ciphertexts are shared by all nq queries (multi-query packing)
   std::vector<std::vector<Word>> recs(count, std::vector<Word>(W, Word(l)));
   std::vector<Word> pays(count, Word(m.l_S));
@@ -224,7 +233,7 @@ int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, 
     outs.insert(outs.end(), root.begin(), root.end());
     if (qi == 0) masked0 = masked;
   }
-  B.finalize(outs, s);
+  if (int rc = B.finalize(outs, s)) return rc;
   s->in0_cts = static_cast<uint64_t>(nq) * QW * l;
   s->in1_cts = count * per;
   s->l_S = m.l_S;
@@ -248,7 +257,7 @@ int compile_gates(int op, size_t count, Schedule* s) {
     else
       outs[i] = B.gate(op, a, b);
   }
-  B.finalize(outs, s);
+  if (int rc = B.finalize(outs, s)) return rc;
   s->in0_cts = count;
   s->in1_cts = op == VLP_MUX ? 2 * count : count;
   return VLP_OK;
@@ -256,7 +265,7 @@ int compile_gates(int op, size_t count, Schedule* s) {
 
 int compile_combine(const vlp_meta& m, uint32_t G, Schedule* s) {
   if (int rc = check_meta(&m)) return rc;
-  if (G < 1 || (G & (G - 1))) return fail(VLP_EINVAL, "G must be a power of two");
+  if (G < 1 || G > 65536 || (G & (G - 1))) return fail(VLP_EINVAL, "G must be a power of two <= 65536");
   Builder B;
   std::vector<Word> S(G, Word(m.l_S));
   for (uint32_t g = 0; g < G; g++)
@@ -264,7 +273,7 @@ int compile_combine(const vlp_meta& m, uint32_t G, Schedule* s) {
   vlp_meta mm = m;
   mm.flags |= VLP_F_SUM_TREE;  // shard roots combine with the same pairing (R15)
   const Word root = aggregate(B, S, m.l_S, mm.flags);
-  B.finalize(root, s);
+  if (int rc = B.finalize(root, s)) return rc;
   s->in0_cts = static_cast<uint64_t>(G) * m.l_S;
   s->l_S = m.l_S;
   return VLP_OK;

@@ -156,3 +156,13 @@ def test_multi_query_schedule():
     assert (info.br, info.ks, info.levels) == (5 * one.br, 5 * one.ks, one.levels)
     assert info.in0_cts == 5 * one.in0_cts and info.out_cts == 5 * one.out_cts and info.in1_cts == one.in1_cts
     assert L.lib().vlp_program_create_queries(None, ctypes.byref(m), 0, 58, 0, ctypes.byref(h)) == L.VLP_EINVAL
+
+
+def test_oversized_schedules_are_refused():
+    """Slot ids address 2^28 rows per region: a shard with more input ciphertexts (or a combine over too many
+    shards) is refused with VLP_EINVAL instead of wrapping row indices."""
+    h = ctypes.c_void_p()
+    m = A.meta(L.MODE_INTV, 1 << 23, 16, 16, 1)  # 2^23 records x 48 ciphertexts > 2^28
+    assert L.lib().vlp_program_create(None, ctypes.byref(m), 0, 1 << 23, ctypes.byref(h)) == L.VLP_EINVAL
+    assert "too large" in L.lib().vlp_last_error().decode()
+    assert L.lib().vlp_program_create_combine(None, ctypes.byref(m), 1 << 20, ctypes.byref(h)) == L.VLP_EINVAL
