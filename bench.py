@@ -33,10 +33,10 @@ METRIC = "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
 UNIT = "gate bootstraps/s"
 CONFIG_BR = {1: 252, 2: 132080, 3: 1060832, 4: 6750176}
 # dram__bytes_read.sum + dram__bytes_write.sum of one vlp_blind_rotate_kernel launch from `ncu --set full`
-# (profiles/r1_br_v5_ncu_summary.txt: a one-wave launch of 740 bootstraps, i.e. one bsk pass per CTA; the bsk
+# (profiles/r1_br_v11_ncu_summary.txt: a one-wave launch of 740 bootstraps, i.e. one bsk pass per CTA; the bsk
 # itself is L2-resident, so DRAM sees about one 92.9 MB bsk read per launch plus the ciphertexts)
-TRAFFIC_BYTES_PER_LAUNCH = (102.109952 + 5.181696) * 1e6
-TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_kernel, 740-bootstrap launch (profiles/r1_br_v5_ncu_summary.txt)"
+TRAFFIC_BYTES_PER_LAUNCH = (102.260992 + 4.645376) * 1e6
+TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_kernel<5>, 740-bootstrap launch (profiles/r1_br_v11_ncu_summary.txt)"
 
 
 def ops_per_br():
