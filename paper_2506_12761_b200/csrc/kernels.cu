@@ -7,6 +7,8 @@
 //                               groups (latency mode)
 //  K2 vlp_blind_rotate_clat_kernel : a tail of <= 1 bootstrap per 2 SMs, one bootstrap on a 2-CTA cluster
 //                               (one accumulator component per SM, DSMEM exchange of the MAC inputs)
+//  K2 vlp_blind_rotate_c6_kernel : a tail of <= 1 bootstrap per resident 6-CTA cluster, one bootstrap on 6
+//                               SMs (one digit polynomial and one output limb per SM)
 //  K3 vlp_ks_indicator_kernel + cuBLASLt int8 GEMM + vlp_ks_combine_kernel : MUX combine (S7) + key
 //                               switch (S8) as a one-hot-indicator x byte-limb-ksk GEMM on the tensor cores
 //  K4 vlp_bsk_convert_kernel  : bsk -> 3-limb NTT domain (setup)
@@ -204,14 +206,15 @@ __device__ __forceinline__ void stage0_digits(uint32_t (&d)[NP][8], const uint32
 
 // Lane-varying stages 3-8: layout B (S = 3..5) or C (S = 6..8); rb = 4 >> (S % 3); twiddle slot
 // q = r >> (3 - S % 3) at table row kSlotBase[S] + q, column t.
-template <int S, bool INV, int NP>
+// SMTW: the twiddle table is in shared memory (cluster kernels: cluster barriers invalidate L1).
+template <int S, bool INV, int NP, bool SMTW = false>
 __device__ __forceinline__ void stage_BC(uint32_t (&d)[NP][8], const uint2* __restrict__ twl, Rc z) {
   constexpr int rb = 4 >> (S % 3);
   constexpr int base = S == 3 ? 0 : S == 4 ? 1 : S == 5 ? 3 : S == 6 ? 7 : S == 7 ? 8 : 10;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
     if (r & rb) continue;
-    const uint2 w = __ldg(twl + (base + (r >> (3 - S % 3))) * kBT);
+    const uint2 w = SMTW ? twl[(base + (r >> (3 - S % 3))) * kBT] : __ldg(twl + (base + (r >> (3 - S % 3))) * kBT);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
       if (INV) gs_bfly(d[p][r], d[p][r | rb], w.x, w.y, z);
@@ -222,12 +225,12 @@ __device__ __forceinline__ void stage_BC(uint32_t (&d)[NP][8], const uint2* __re
 
 // Stage 9 forward: lane-pair exchange (lower lane keeps pairs r = 0..3, upper lane r = 4..7), then
 // butterflies on (d[i], d[4+i]) with twiddle slots 14..17.
-template <int NP>
+template <int NP, bool SMTW = false>
 __device__ __forceinline__ void stage9_fwd(uint32_t (&d)[NP][8], uint32_t t, const uint2* __restrict__ twl, Rc z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    const uint2 w = __ldg(twl + (14 + i) * kBT);
+    const uint2 w = SMTW ? twl[(14 + i) * kBT] : __ldg(twl + (14 + i) * kBT);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
       const uint32_t send = lo ? d[p][4 + i] : d[p][i];
@@ -242,12 +245,12 @@ __device__ __forceinline__ void stage9_fwd(uint32_t (&d)[NP][8], uint32_t t, con
 }
 
 // Stage 9 inverse: butterflies on (d[i], d[4+i]), then the reverse lane-pair exchange (back to layout C).
-template <int NP>
+template <int NP, bool SMTW = false>
 __device__ __forceinline__ void stage9_inv(uint32_t (&d)[NP][8], uint32_t t, const uint2* __restrict__ twl, Rc z) {
   const bool lo = (t & 1u) == 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    const uint2 w = __ldg(twl + (14 + i) * kBT);
+    const uint2 w = SMTW ? twl[(14 + i) * kBT] : __ldg(twl + (14 + i) * kBT);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
       gs_bfly(d[p][i], d[p][4 + i], w.x, w.y, z);
@@ -780,33 +783,35 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
 // transformed digit polynomials in shared memory (double-buffered, [q][slot][thread]) and reads the peer's
 // through distributed shared memory after a cluster barrier.  Same arithmetic, key layout and bytes.
 constexpr int kClatGroups = 3;
+constexpr int kClatSlots = 3;  // with the twiddles in shared memory a 4th bsk slot no longer fits
 constexpr int kClatThreads = kClatGroups * kBT;
 constexpr int kClatTmemCols = 32;
 __host__ __device__ constexpr int clat_smem_bytes() {
-  return kLatSlots * kChunkBytes + (N * 4 + kClatGroups * N * 4 + 2 * 3 * N * 4 + 640 * 2) + 128 * 4 + kLatSlots * 8 +
-         kLatSlots * 4 + 8;
+  return 2 * kTwSlots * kBT * 8 + kClatSlots * kChunkBytes + (N * 4 + kClatGroups * N * 4 + 2 * 3 * N * 4 + 640 * 2) + 128 * 4 + kClatSlots * 8 +
+         kClatSlots * 4 + 8;
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
     vlp_blind_rotate_clat_kernel(const BrArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* ring = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* acc = ring + kLatSlots * kBT * kChunkWords;  // component r only
+  uint2* tw_s = reinterpret_cast<uint2*>(smem);  // [fwd, inv][kTwSlots][t] twiddles (cluster barriers flush L1)
+  uint32_t* ring = reinterpret_cast<uint32_t*>(tw_s + 2 * kTwSlots * kBT);
+  uint32_t* acc = ring + kClatSlots * kBT * kChunkWords;  // component r only
   uint32_t* xb_all = acc + N;                            // [group 3][N]
   uint32_t* dig = xb_all + kClatGroups * N;              // [buf 2][q 3][slot 8][thread 128]
   uint16_t* abar = reinterpret_cast<uint16_t*>(dig + 2 * 3 * N);
   uint32_t* t0tab = reinterpret_cast<uint32_t*>(abar + 640);  // [128] stage-0 digit products
   uint64_t* mbar = reinterpret_cast<uint64_t*>(t0tab + 128);
-  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kLatSlots);
-  uint32_t* tmem_base_sh = rel + kLatSlots;
+  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kClatSlots);
+  uint32_t* tmem_base_sh = rel + kClatSlots;
 
   cg::cluster_group cl = cg::this_cluster();
   const uint32_t rk = cl.block_rank();  // accumulator component owned by this CTA
   const uint32_t* dig_peer = cl.map_shared_rank(dig, rk ^ 1u);
   const uint32_t tid = threadIdx.x, G = tid / kBT, t = tid % kBT;
   uint32_t* xb = xb_all + G * N;
-  const uint2* twf = a.twl_fwd + t;
-  const uint2* twi = a.twl_inv + t;
+  const uint2* twf = tw_s + t;
+  const uint2* twi = tw_s + kTwSlots * kBT + t;
   const Rc zr{a.zero, a.p2};
   const uint32_t nclusters = gridDim.x / 2, cid = blockIdx.x / 2;
   if (cid >= a.njobs) return;  // both CTAs of a cluster take the same branch
@@ -814,7 +819,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
   const uint32_t total_chunks = my_jobs * static_cast<uint32_t>(a.steps) * kChunks;
 
   if (tid == 0) {
-    for (int s = 0; s < kLatSlots; s++) {
+    for (int s = 0; s < kClatSlots; s++) {
       mbar_init(&mbar[s], 1);
       rel[s] = 0;
     }
@@ -823,6 +828,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
   if (tid < 128) {
     const uint64_t w0 = c_tw[0][1].x;  // the stage-0 twiddle
     t0tab[tid] = static_cast<uint32_t>(w0 * ((tid + P - 64u) % P) % P);
+  }
+  for (uint32_t k = tid; k < static_cast<uint32_t>(kTwSlots * kBT); k += kClatThreads) {
+    tw_s[k] = a.twl_fwd[k];
+    tw_s[kTwSlots * kBT + k] = a.twl_inv[k];
   }
   if (tid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
@@ -837,12 +846,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
 
   auto issue = [&](uint32_t nseq) {
     const uint32_t step = (nseq / kChunks) % static_cast<uint32_t>(a.steps), c = nseq % kChunks;
-    const uint32_t s = nseq % kLatSlots;
+    const uint32_t s = nseq % kClatSlots;
     bulk_load(ring + s * kBT * kChunkWords, a.bsk + (static_cast<size_t>(step) * kChunks + c) * kBT * kChunkWords,
               kChunkBytes, &mbar[s]);
   };
   if (tid == 0)
-    for (uint32_t q = 0; q < kLatSlots && q < total_chunks; q++) issue(q);
+    for (uint32_t q = 0; q < kClatSlots && q < total_chunks; q++) issue(q);
   uint32_t nseq = 0, sl = 0, ph = 0, buf = 0;
   const uint32_t dshift = 25u - 7u * G;  // forward: gadget digit G of component rk (R5)
 
@@ -884,14 +893,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
         stage_A<1, false>(d, zr);
         stage_A<2, false>(d, zr);
         exchange<0, 1>(d, xb, t, G);
-        stage_BC<3, false>(d, twf, zr);
-        stage_BC<4, false>(d, twf, zr);
-        stage_BC<5, false>(d, twf, zr);
+        stage_BC<3, false, 1, true>(d, twf, zr);
+        stage_BC<4, false, 1, true>(d, twf, zr);
+        stage_BC<5, false, 1, true>(d, twf, zr);
         exchange<1, 2>(d, xb, t, G);
-        stage_BC<6, false>(d, twf, zr);
-        stage_BC<7, false>(d, twf, zr);
-        stage_BC<8, false>(d, twf, zr);
-        stage9_fwd(d, t, twf, zr);
+        stage_BC<6, false, 1, true>(d, twf, zr);
+        stage_BC<7, false, 1, true>(d, twf, zr);
+        stage_BC<8, false, 1, true>(d, twf, zr);
+        stage9_fwd<1, true>(d, t, twf, zr);
 #pragma unroll
         for (int s8 = 0; s8 < 8; s8++) mydig[(G * 8 + s8) * kBT + t] = d[0][s8];
       }
@@ -932,14 +941,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
           __threadfence_block();
           if (atomicAdd(&rel[sl], 1u) == kClatThreads / 32 - 1) {
             atomicExch(&rel[sl], 0u);
-            if (nseq + kLatSlots < total_chunks) {
+            if (nseq + kClatSlots < total_chunks) {
               fence_proxy_async();
-              issue(nseq + kLatSlots);
+              issue(nseq + kClatSlots);
             }
           }
         }
         nseq++;
-        if (++sl == kLatSlots) {
+        if (++sl == kClatSlots) {
           sl = 0;
           ph ^= 1u;
         }
@@ -949,14 +958,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
         uint32_t d[1][8];
 #pragma unroll
         for (int s8 = 0; s8 < 8; s8++) d[0][s8] = umin(mac[s8], mac[s8] - P2);
-        stage9_inv(d, t, twi, zr);
-        stage_BC<8, true>(d, twi, zr);
-        stage_BC<7, true>(d, twi, zr);
-        stage_BC<6, true>(d, twi, zr);
+        stage9_inv<1, true>(d, t, twi, zr);
+        stage_BC<8, true, 1, true>(d, twi, zr);
+        stage_BC<7, true, 1, true>(d, twi, zr);
+        stage_BC<6, true, 1, true>(d, twi, zr);
         exchange<2, 1>(d, xb, t, G);
-        stage_BC<5, true>(d, twi, zr);
-        stage_BC<4, true>(d, twi, zr);
-        stage_BC<3, true>(d, twi, zr);
+        stage_BC<5, true, 1, true>(d, twi, zr);
+        stage_BC<4, true, 1, true>(d, twi, zr);
+        stage_BC<3, true, 1, true>(d, twi, zr);
         exchange<1, 0>(d, xb, t, G);
         stage_A<2, true>(d, zr);
         stage_A<1, true>(d, zr);
@@ -1009,6 +1018,213 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
   __syncthreads();
   if (tid < 32)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kClatTmemCols) : "memory");
+}
+
+// ================================================================================ K2-C6 (6-CTA cluster latency mode)
+// For the narrowest level tails (at most one bootstrap per 6 SMs): one bootstrap on a cluster of 6 CTAs of
+// one warp group each.  CTA rank c = 3u + j owns digit polynomial j of component u (forward NTT) and output
+// o = c, i.e. limb j of component u (MAC + inverse NTT), and keeps a copy of acc_u.  Two exchanges per CMux
+// step through distributed shared memory, each after a cluster barrier: the 6 transformed digit polynomials
+// (the MAC inputs) and the 3 lifted limbs of each component (the accumulator update, which the 3 CTAs of a
+// component apply identically to their copies).  The CTA's 12 key words per thread and chunk (output o of
+// the [o 6][e 2][q 6] chunk row) are prefetched one CMux step ahead with cp.async (24 KB per step instead of
+// the 156 KB of whole chunks).  One buffer per exchange suffices: a CTA overwrites its digits only after the
+// step's second cluster barrier and its limbs only after the next step's first, when every peer has read
+// them.  Same arithmetic, key and bytes as the other blind-rotate kernels.
+constexpr int kC6 = 6;
+constexpr int kC6KeyWords = kChunks * kBT * 12;  // one step of this CTA's key words: [pp 4][t 128][12]
+__host__ __device__ constexpr int c6_smem_bytes() {
+  return 2 * kTwSlots * kBT * 8 + 2 * kC6KeyWords * 4 + (N * 4 + N * 4 + N * 4 + N * 4) + 640 * 2 + 128 * 4;
+}
+constexpr int kC6SmemRequest = 120 * 1024;  // > half an SM's shared memory: one CTA per SM
+static_assert(c6_smem_bytes() <= kC6SmemRequest, "C6 shared memory");
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory"); }
+
+__global__ void __cluster_dims__(kC6, 1, 1) __launch_bounds__(kBT, 1) vlp_blind_rotate_c6_kernel(const BrArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint2* tw_s = reinterpret_cast<uint2*>(smem);  // [fwd, inv][kTwSlots][t] twiddles (cluster barriers flush L1)
+  uint32_t* kbuf = reinterpret_cast<uint32_t*>(tw_s + 2 * kTwSlots * kBT);  // [seq & 1][pp][t][12]
+  uint32_t* acc = kbuf + 2 * kC6KeyWords;             // component u only
+  uint32_t* xb = acc + N;                             // layout exchanges of this CTA's NTTs
+  uint32_t* dig = xb + N;                             // published transformed digit poly [slot 8][t]
+  uint32_t* lim = dig + N;                            // published lifted limb [r 8][t]
+  uint16_t* abar = reinterpret_cast<uint16_t*>(lim + N);
+  uint32_t* t0tab = reinterpret_cast<uint32_t*>(abar + 640);  // [128] stage-0 digit products
+
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t rk = cl.block_rank(), u = rk / 3u, jl = rk % 3u;
+  const uint32_t t = threadIdx.x;
+  const uint2* twf = tw_s + t;
+  const uint2* twi = tw_s + kTwSlots * kBT + t;
+  const Rc zr{a.zero, a.p2};
+  const uint32_t nclusters = gridDim.x / kC6, cid = blockIdx.x / kC6;
+  if (cid >= a.njobs) return;  // all CTAs of a cluster take the same branch
+  const uint32_t dshift = 25u - 7u * jl;  // gadget digit jl (R5)
+
+  if (t < 128) {
+    const uint64_t w0 = c_tw[0][1].x;  // the stage-0 twiddle
+    t0tab[t] = static_cast<uint32_t>(w0 * ((t + P - 64u) % P) % P);
+  }
+  for (uint32_t k = t; k < static_cast<uint32_t>(kTwSlots * kBT); k += kBT) {
+    tw_s[k] = a.twl_fwd[k];
+    tw_s[kTwSlots * kBT + k] = a.twl_inv[k];
+  }
+  // this thread's 48 key bytes of output rk in chunk pp of bsk step `step` -> kbuf[buf]
+  auto prefetch = [&](uint32_t step, uint32_t buf) {
+#pragma unroll
+    for (int pp = 0; pp < kChunks; pp++) {
+      const uint32_t* src = a.bsk + ((static_cast<size_t>(step) * kChunks + pp) * kBT + t) * kChunkWords + rk * 12;
+      uint32_t* dst = kbuf + buf * kC6KeyWords + (pp * kBT + t) * 12;
+#pragma unroll
+      for (int v = 0; v < 3; v++) cp_async16(dst + 4 * v, src + 4 * v);
+    }
+    cp_async_commit();
+  };
+  uint32_t seq = 0;  // CMux steps run so far (kbuf[seq & 1] holds step seq's key words)
+  prefetch(0, 0);
+  __syncthreads();
+
+  for (uint32_t jb = cid; jb < a.njobs; jb += nclusters) {
+    {  // S2 + S3 (every CTA needs every abar)
+      const BrJob job = a.jobs[jb];
+      const uint32_t* x = slot_ptr(a.reg, job.x);
+      const uint32_t* y = slot_ptr(a.reg, job.y);
+      for (uint32_t w = t; w <= static_cast<uint32_t>(n); w += kBT) {
+        uint32_t c = static_cast<uint32_t>(static_cast<int32_t>(job.ax)) * x[w];
+        if (job.ay) c += static_cast<uint32_t>(static_cast<int32_t>(job.ay)) * y[w];
+        if (w == static_cast<uint32_t>(n)) c += job.k0;
+        abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
+      }
+    }
+    __syncthreads();
+    {  // S4 for component u: acc_0 = 0, acc_1 = X^{-bbar} testv (R8)
+      const uint32_t bbar = abar[n];
+      for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT)
+        acc[k] = u == 0 ? 0u : ((((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu));
+    }
+    __syncthreads();
+
+    for (int i = 0; i < a.steps; i++, seq++) {
+      prefetch((static_cast<uint32_t>(i) + 1u) % static_cast<uint32_t>(a.steps), (seq + 1u) & 1u);
+      const uint32_t ab = abar[i];
+      {  // digit jl of component u -> forward NTT -> publish [slot][t]
+        uint32_t d[1][8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const uint32_t j = t + 128u * r;
+          const uint32_t kk = (j - ab) & (2 * N - 1);
+          uint32_t v = acc[kk & (N - 1)];
+          v = kk >= static_cast<uint32_t>(N) ? zr.z - v : v;
+          const uint32_t w = v - acc[j] + 0x81020400u;
+          d[0][r] = ((w >> dshift) & 127u) + (P - 64u);
+        }
+        stage0_digits(d, t0tab, zr);
+        stage_A<1, false>(d, zr);
+        stage_A<2, false>(d, zr);
+        exchange<0, 1>(d, xb, t, 0);
+        stage_BC<3, false, 1, true>(d, twf, zr);
+        stage_BC<4, false, 1, true>(d, twf, zr);
+        stage_BC<5, false, 1, true>(d, twf, zr);
+        exchange<1, 2>(d, xb, t, 0);
+        stage_BC<6, false, 1, true>(d, twf, zr);
+        stage_BC<7, false, 1, true>(d, twf, zr);
+        stage_BC<8, false, 1, true>(d, twf, zr);
+        stage9_fwd<1, true>(d, t, twf, zr);
+#pragma unroll
+        for (int s8 = 0; s8 < 8; s8++) dig[s8 * kBT + t] = d[0][s8];
+      }
+      cl.sync();  // the 6 transformed digit polynomials are published
+      // MAC for output o = rk: digit rows q = 3u' + j' live in CTA q
+      uint32_t mac[8];
+      {
+        uint32_t xq[6][8];
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+          const uint32_t* src = cl.map_shared_rank(dig, static_cast<unsigned>(q));
+#pragma unroll
+          for (int s8 = 0; s8 < 8; s8++) {
+            const uint32_t v = src[s8 * kBT + t];
+            xq[q][s8] = umin(v, v - P2);  // [0, 2p)
+          }
+        }
+        cp_async_wait<1>();  // this step's key words (the newest group is the next step's)
+        const uint32_t* kb = kbuf + (seq & 1u) * kC6KeyWords + t * 12;
+#pragma unroll
+        for (int pp = 0; pp < kChunks; pp++) {
+          const uint4* kp = reinterpret_cast<const uint4*>(kb + pp * kBT * 12);  // [e 2][q 6]
+          const uint4 k0 = kp[0], k1 = kp[1], k2 = kp[2];
+          const uint32_t kv[2][6] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y}, {k1.z, k1.w, k2.x, k2.y, k2.z, k2.w}};
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            uint64_t T = static_cast<uint64_t>(xq[0][2 * pp + e]) * kv[e][0];
+#pragma unroll
+            for (int q = 1; q < 6; q++) T += static_cast<uint64_t>(xq[q][2 * pp + e]) * kv[e][q];
+            const uint32_t m = static_cast<uint32_t>(T) * PINV_NEG;
+            mac[2 * pp + e] = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * P) >> 32);
+          }
+        }
+      }
+      {  // inverse NTT of limb jl of component u, centered lift, publish [r][t]
+        uint32_t d[1][8];
+#pragma unroll
+        for (int s8 = 0; s8 < 8; s8++) d[0][s8] = umin(mac[s8], mac[s8] - P2);
+        stage9_inv<1, true>(d, t, twi, zr);
+        stage_BC<8, true, 1, true>(d, twi, zr);
+        stage_BC<7, true, 1, true>(d, twi, zr);
+        stage_BC<6, true, 1, true>(d, twi, zr);
+        exchange<2, 1>(d, xb, t, 0);
+        stage_BC<5, true, 1, true>(d, twi, zr);
+        stage_BC<4, true, 1, true>(d, twi, zr);
+        stage_BC<3, true, 1, true>(d, twi, zr);
+        exchange<1, 0>(d, xb, t, 0);
+        stage_A<2, true>(d, zr);
+        stage_A<1, true>(d, zr);
+        stage_A<0, true>(d, zr);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const uint32_t v = umin(d[0][r], d[0][r] - P);
+          lim[r * kBT + t] = v > (P >> 1) ? v - P : v;
+        }
+      }
+      cl.sync();  // the 6 lifted limbs are published
+      {  // acc_u += R0 + 2^11 R1 + 2^22 R2 (limb l from CTA 3u + l; the same update in all 3 CTAs of u)
+        const uint32_t* l0 = cl.map_shared_rank(lim, 3u * u);
+        const uint32_t* l1 = cl.map_shared_rank(lim, 3u * u + 1u);
+        const uint32_t* l2 = cl.map_shared_rank(lim, 3u * u + 2u);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const uint32_t hi = __funnelshift_l(0u, l1[r * kBT + t], 11) + __funnelshift_l(0u, l2[r * kBT + t], 22) + zr.z;
+          uint32_t& av = acc[t + 128u * r];
+          av = add_alu(av, l0[r * kBT + t], hi);
+        }
+      }
+      __syncthreads();  // acc complete before the next step's rotated reads
+    }
+
+    // ---- S6: CTA 0 holds the mask a (a'_0 = a_0, a'_k = -a_{N-k}), CTA 3 the body b (b' = b_0)
+    if (jl == 0) {
+      if (a.raw_acc) {
+        uint32_t* o = a.raw_acc + static_cast<size_t>(jb) * 2 * N + u * N;
+        for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT) o[k] = acc[k];
+      } else {
+        uint32_t* o = a.nlwe + static_cast<size_t>(a.jobs[jb].out) * kNlwe;
+        if (u == 0) {
+          for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+        } else if (t == 0) {
+          o[N] = acc[0];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  cl.sync();  // peers may still read this CTA's limbs
 }
 
 // ================================================================================ K3' key switch on tensor cores
@@ -1271,8 +1487,53 @@ static cudaError_t launch_br_clat(const BrArgs& a, int sm_count, cudaStream_t st
   return cudaGetLastError();
 }
 
+// Clusters of 6 CTAs that can be resident at once (GPC packing), per device (queried once).
+static uint32_t c6_max_clusters() {
+  static std::atomic<int> cached[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  int v = cached[dev & 63].load();
+  if (v == 0) {
+    if (cudaFuncSetAttribute(vlp_blind_rotate_c6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kC6SmemRequest) !=
+        cudaSuccess)
+      return 0;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kC6;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kC6, 1, 1);
+    cfg.blockDim = dim3(kBT, 1, 1);
+    cfg.dynamicSmemBytes = kC6SmemRequest;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, vlp_blind_rotate_c6_kernel, &cfg) != cudaSuccess || nc < 1) {
+      cudaGetLastError();
+      nc = -1;  // not available: never route to it
+    }
+    cached[dev & 63].store(nc);
+    v = nc;
+  }
+  return v > 0 ? static_cast<uint32_t>(v) : 0u;
+}
+
+static cudaError_t launch_br_c6(const BrArgs& a, int sm_count, cudaStream_t st) {
+  const uint32_t maxc = c6_max_clusters();
+  if (maxc == 0) return launch_br_clat(a, sm_count, st);
+  if (a.njobs == 0) return cudaSuccess;
+  const uint32_t clusters = a.njobs < maxc ? a.njobs : maxc;
+  BrArgs b = a;
+  b.zero = 0;
+  b.p2 = P2;
+  vlp_blind_rotate_c6_kernel<<<kC6 * clusters, kBT, kC6SmemRequest, st>>>(b);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_br_width(const BrArgs& a, int B, int sm_count, cudaStream_t st) {
   switch (B) {
+    case -2: return launch_br_c6(a, sm_count, st);
     case -1: return launch_br_clat(a, sm_count, st);
     case 0: return launch_br_lat(a, sm_count, st);
     case 1: return launch_br_b<1>(a, sm_count, st);
@@ -1297,7 +1558,9 @@ static int forced_boot() {
 
 int br_launch_count(uint32_t njobs, int sm_count) {
   if (njobs == 0) return 0;
-  if ((forced_boot() >= 1 && forced_boot() <= kBrBoot) || forced_boot() == -1 || forced_boot() == -2) return 1;
+  if ((forced_boot() >= 1 && forced_boot() <= kBrBoot) || forced_boot() == -1 || forced_boot() == -2 ||
+      forced_boot() == -3)
+    return 1;
   const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
   return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
 }
@@ -1308,6 +1571,7 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
   if (forced >= 1 && forced <= kBrBoot) return launch_br_width(a, forced, sm_count, st);
   if (forced == -1) return launch_br_width(a, 0, sm_count, st);   // VLP_BR_BOOT=-1: latency mode
   if (forced == -2) return launch_br_width(a, -1, sm_count, st);  // VLP_BR_BOOT=-2: cluster latency mode
+  if (forced == -3) return launch_br_width(a, -2, sm_count, st);  // VLP_BR_BOOT=-3: 6-CTA cluster mode
   const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
   const uint32_t full = a.njobs / wave * wave, tail = a.njobs - full;
   cudaError_t e = cudaSuccess;
@@ -1322,8 +1586,9 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
     r.njobs = tail;
     if (r.raw_acc) r.raw_acc = a.raw_acc + static_cast<size_t>(full) * 2 * N;
     // a tail of at most one bootstrap per SM runs in latency mode (warp groups per bootstrap); at most one per
-    // two SMs, on a 2-CTA cluster per bootstrap
-    const int b = tail <= static_cast<uint32_t>(sm_count / 2) ? -1
+    // two SMs, on a 2-CTA cluster per bootstrap; at most one per resident 6-CTA cluster, on a 6-CTA cluster
+    const int b = tail <= c6_max_clusters() ? -2
+                  : tail <= static_cast<uint32_t>(sm_count / 2) ? -1
                   : tail <= static_cast<uint32_t>(sm_count) ? 0
                                                              : static_cast<int>((tail + sm_count - 1) / sm_count);
     e = launch_br_width(r, b, sm_count, st);

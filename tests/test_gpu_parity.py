@@ -55,12 +55,12 @@ def test_blind_rotate_steps_bit_exact(server, okeys):
             assert np.array_equal(got[i], want[i]), (steps, i, np.flatnonzero(got[i] != want[i])[:8])
 
 
-@pytest.mark.parametrize("tail", [1, 100, 150, 300, 600])
+@pytest.mark.parametrize("tail", [1, 50, 100, 150, 300, 600])
 def test_blind_rotate_wave_split_bit_exact(server, okeys, tail):
     """A level of 5 x 148 + tail blind rotations runs as one whole wave (5 bootstraps per CTA) plus a tail
-    wave (kernels.cu launch_blind_rotate): tail 1 on the 2-CTA cluster kernel, 100 on the 6-group latency
-    kernel, 150 / 300 / 600 on 2 / 3 / 5 bootstraps per CTA.  2 CMux steps; sampled rows on both sides of
-    the split and the ragged end byte-equal to the oracle."""
+    wave (kernels.cu launch_blind_rotate): tail 1 on the 6-CTA cluster kernel, 50 on the 2-CTA cluster
+    kernel, 100 on the 6-group latency kernel, 150 / 300 / 600 on 2 / 3 / 5 bootstraps per CTA.  2 CMux
+    steps; sampled rows on both sides of the split and the ragged end byte-equal to the oracle."""
     count = 740 + tail
     rng = np.random.default_rng(tail)
     cts = rand_tlwe(rng, count)
