@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--nand", type=int, default=1 << 17, help="config 5: NAND gates per step (split over ranks)")
     ap.add_argument("--queries", type=int, default=1,
                     help="queries per step (multi-query packing on one GPU: every level launch carries all of them)")
+    ap.add_argument("--prefix-comparator", action="store_true",
+                    help="R23 (not in the paper): log-depth prefix comparators (VLP_F_PREFIX_COMP) for IntV configs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -265,6 +267,9 @@ def main():
     if args.config == 5:
         return run_nand(args, rank, world, local, dev, stream, A, L, dist)
     wl = make_workload(args.config)
+    if args.prefix_comparator:
+        wl = make_workload(args.config, flags=wl.flags | L.F_PREFIX_COMP)
+    wname = wl.name + ("_prefix" if args.prefix_comparator else "")
     m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
     first, shard = shard_range(wl.M, world, rank)
     t_setup = time.time()
@@ -406,7 +411,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "records_per_s": records_per_s, "ks_per_s": (prog.info.ks * world + (comb.info.ks if comb else 0)) / (ms_per_step / 1e3),  # all queries
-            "config": {"workload": f"cfg{args.config}_{wl.name}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S,
+            "config": {"workload": f"cfg{args.config}_{wname}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S,
                        "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels, "queries_per_step": nq,
                        "parallelism": f"records sharded x{world}" if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)",

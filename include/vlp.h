@@ -56,7 +56,9 @@ enum {
   VLP_F_UNSIGNED = 2,     /* R11: unsigned comparators (final MUX selects ct2[l-1]) */
   VLP_F_EQ_TREE = 4,      /* R14: alg:HomEqOPT pairwise AND tree instead of the serial HomEQ */
   VLP_F_SUM_TREE = 8,     /* R15: outermost XOR tree instead of the serial HomSum */
-  VLP_F_OR_REDUCE = 16    /* R19: OR instead of XOR in the aggregation */
+  VLP_F_OR_REDUCE = 16,   /* R19: OR instead of XOR in the aggregation */
+  VLP_F_PREFIX_COMP = 32  /* R23 (NOT in the paper): log-depth parallel-prefix unsigned
+                             comparators (depth 1 + ceil(log2 l) instead of l + 1; more gates; needs UNSIGNED) */
 };
 #define VLP_CONFIG_FLAGS (VLP_F_CLOSED_UPPER | VLP_F_UNSIGNED | VLP_F_EQ_TREE | VLP_F_SUM_TREE)
 

@@ -9,7 +9,8 @@ a gate backend.  Backends:
   gates and depth, used to pin the circuit topology against brute force.
 
 Readings: R11 (``unsigned``), R12 (``closed_upper``), R13 (rectangle = IntV d=2),
-R14 (``eq_tree``), R15/R19 (``sum_tree``, ``or_reduce``), R16 (mask S_i with its own v_i), R20 (LSB first).
+R14 (``eq_tree``), R15/R19 (``sum_tree``, ``or_reduce``), R16 (mask S_i with its own v_i), R20 (LSB first);
+R23 (``F_PREFIX_COMP``, the log-depth comparator of SURVEY 8(f) NEXT 4 -- not in the paper).
 """
 from __future__ import annotations
 
@@ -20,7 +21,7 @@ from . import AND, NAND, OR, XOR, XNOR, OracleKeys, trivial
 
 # Modes and flags (same values as the product's header, defined independently here).
 MODE_INTV, MODE_COV, MODE_IDM = 0, 1, 2
-F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE = 1, 2, 4, 8, 16
+F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP = 1, 2, 4, 8, 16, 32
 CONFIG_FLAGS = F_CLOSED_UPPER | F_UNSIGNED | F_EQ_TREE | F_SUM_TREE
 
 
@@ -101,6 +102,41 @@ def hom_comp_l(B, ct1, ct2, l, unsigned=True):
     return r
 
 
+def hom_comp_gt_prefix(B, ct1, ct2, l):
+    """Log-depth comparator, flag F_PREFIX_COMP -- NOT in the paper (DESIGN.md reading
+    R23): 1 iff z1 > z2 (unsigned).  Per bit i (LSB first): G_i = AND(ct1[i], NOT ct2[i]) (greater at bit i),
+    E_i = XNOR(ct1[i], ct2[i]) (equal at bit i).  Adjacent ranges are merged level by level, range 2k+1 as
+    the high part H and range 2k as the low part L (a last unpaired range is carried up unchanged):
+    G = MUX(H.E, L.G, H.G) -- equal on the high part: the low part decides, else the high part does --
+    and E = AND(H.E, L.E).  Every E is computed here (the product builds only the ones a G uses; unused gates
+    do not change any output)."""
+    G = [B.AND(ct1[i], B.NOT(ct2[i])) for i in range(l)]
+    E = [B.XNOR(ct1[i], ct2[i]) for i in range(l)]
+    while len(G) > 1:
+        nG, nE = [], []
+        for k in range(0, len(G), 2):
+            if k + 1 < len(G):
+                nG.append(B.MUX(E[k + 1], G[k], G[k + 1]))
+                nE.append(B.AND(E[k + 1], E[k]))
+            else:
+                nG.append(G[k])
+                nE.append(E[k])
+        G, E = nG, nE
+    return G[0]
+
+
+def hom_comp_le_prefix(B, ct1, ct2, l, unsigned=True):
+    """[z1 <= z2] = NOT [z1 > z2] (free negation)."""
+    assert unsigned, "the prefix comparator is unsigned only"
+    return B.NOT(hom_comp_gt_prefix(B, ct1, ct2, l))
+
+
+def hom_comp_l_prefix(B, ct1, ct2, l, unsigned=True):
+    """[z1 < z2] = [z2 > z1]."""
+    assert unsigned, "the prefix comparator is unsigned only"
+    return hom_comp_gt_prefix(B, ct2, ct1, l)
+
+
 # ------------------------------------------------------------------------------- equality (P:473-502, 730-752)
 def hom_eq_serial(B, ct1, ct2, l):
     """alg:HomEQ: r = trivial Enc(1); r <- AND(r, XNOR(ct1[i], ct2[i])) for every bit."""
@@ -129,12 +165,13 @@ def intv(B, q, rec, l, d, flags):
     (+ [Enc(y_left), Enc(y_right)] for d = 2).  CLOSED_UPPER (R12): the right bound uses
     HomCompLE(x, x_right) (lo <= x <= hi) instead of the paper's HomCompL (x < x_right)."""
     uns = bool(flags & F_UNSIGNED)
-    right = hom_comp_le if flags & F_CLOSED_UPPER else hom_comp_l
-    v_xl = hom_comp_le(B, rec[0], q[0], l, uns)
+    le, lt = (hom_comp_le_prefix, hom_comp_l_prefix) if flags & F_PREFIX_COMP else (hom_comp_le, hom_comp_l)
+    right = le if flags & F_CLOSED_UPPER else lt
+    v_xl = le(B, rec[0], q[0], l, uns)
     v_xr = right(B, q[0], rec[1], l, uns)
     if d == 1:
         return B.AND(v_xl, v_xr)
-    v_yl = hom_comp_le(B, rec[2], q[1], l, uns)
+    v_yl = le(B, rec[2], q[1], l, uns)
     v_yr = right(B, q[1], rec[3], l, uns)
     v_x = B.AND(v_xl, v_xr)
     v_y = B.AND(v_yl, v_yr)

@@ -24,6 +24,11 @@ namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr size_t kMaxRows = size_t{1} << 28;  // rows addressable by a slot id (region << 28 | row)
+// A reference to a node may carry NOT (free: the negated ciphertext, O11): bit 31.  A gate folds it into
+// its linear form (the input's coefficient changes sign), so no ciphertext is ever materialised for it.
+constexpr uint32_t kNeg = 0x80000000u;
+inline uint32_t node_of(uint32_t ref) { return ref & ~kNeg; }
+inline int sgn(uint32_t ref) { return (ref & kNeg) ? -1 : 1; }
 
 struct LinForm {
   uint32_t k0;
@@ -61,18 +66,20 @@ class Builder {
     if (c == kNone) c = leaf(slot(kRegMid, bit ? 1 : 0));
     return c;
   }
+  uint32_t lvl(uint32_t ref) const { return nodes[node_of(ref)].level; }
   uint32_t gate(int op, uint32_t x, uint32_t y) {
-    const uint32_t l = std::max(nodes[x].level, nodes[y].level) + 1;
+    const uint32_t l = std::max(lvl(x), lvl(y)) + 1;
     nodes.push_back(Node{1, static_cast<uint8_t>(op), {x, y, kNone}, l, 0, 0, kNone});
     return static_cast<uint32_t>(nodes.size() - 1);
   }
   // MUX(c, a, b) = c ? a : b (R10)
   uint32_t mux(uint32_t c, uint32_t a, uint32_t b) {
-    const uint32_t h1 = std::max(nodes[c].level, nodes[a].level) + 1;
-    const uint32_t h2 = std::max(nodes[c].level, nodes[b].level) + 1;
+    const uint32_t h1 = std::max(lvl(c), lvl(a)) + 1;
+    const uint32_t h2 = std::max(lvl(c), lvl(b)) + 1;
     nodes.push_back(Node{2, VLP_MUX, {c, a, b}, std::max(h1, h2), h1, h2, kNone});
     return static_cast<uint32_t>(nodes.size() - 1);
   }
+  static uint32_t NOT(uint32_t ref) { return ref ^ kNeg; }
   uint32_t AND(uint32_t x, uint32_t y) { return gate(VLP_AND, x, y); }
   uint32_t OR(uint32_t x, uint32_t y) { return gate(VLP_OR, x, y); }
   uint32_t XOR(uint32_t x, uint32_t y) { return gate(VLP_XOR, x, y); }
@@ -86,8 +93,10 @@ class Builder {
     if (gates + 2 > kMaxRows || outs.size() > kMaxRows)
       return fail(VLP_EINVAL, "schedule too large: more than 2^28 ciphertext rows in one region");
     std::vector<uint32_t> out_index(nodes.size(), kNone);
-    for (size_t j = 0; j < outs.size(); j++)
+    for (size_t j = 0; j < outs.size(); j++) {
+      if (outs[j] & kNeg) return fail(VLP_EINVAL, "internal: a negated reference as a circuit output");
       if (nodes[outs[j]].kind != 0) out_index[outs[j]] = static_cast<uint32_t>(j);
+    }
     uint32_t mid = 2, nl = 0, maxl = 0;
     for (size_t i = 0; i < nodes.size(); i++) {
       Node& nd = nodes[i];
@@ -96,21 +105,25 @@ class Builder {
       maxl = std::max(maxl, nd.level);
     }
     s->levels.assign(maxl, Level{});
+    auto sl = [&](uint32_t ref) { return nodes[node_of(ref)].slot; };
     for (auto& nd : nodes) {
       if (nd.kind == 1) {
         const LinForm f = form(nd.op);
         const uint32_t row = nl++;
-        s->levels[nd.level - 1].br.push_back(BrJob{nodes[nd.in[0]].slot, nodes[nd.in[1]].slot, f.k0, f.ax, f.ay, 0, row});
+        s->levels[nd.level - 1].br.push_back(BrJob{sl(nd.in[0]), sl(nd.in[1]), f.k0,
+                                                   static_cast<int8_t>(f.ax * sgn(nd.in[0])),
+                                                   static_cast<int8_t>(f.ay * sgn(nd.in[1])), 0, row});
         s->levels[nd.level - 1].ks.push_back(KsJob{row, kNone, 0u, nd.slot});
         s->gates++;
         s->br++;
         s->ks++;
       } else if (nd.kind == 2) {
         const uint32_t r1 = nl++, r2 = nl++;
-        const uint32_t c = nodes[nd.in[0]].slot, a = nodes[nd.in[1]].slot, b = nodes[nd.in[2]].slot;
+        const uint32_t c = sl(nd.in[0]), a = sl(nd.in[1]), b = sl(nd.in[2]);
+        const int sc = sgn(nd.in[0]), sa = sgn(nd.in[1]), sb = sgn(nd.in[2]);
         // BR_N((0,-1/8) + c + a) and BR_N((0,-1/8) - c + b); KS((0,1/8) + u1 + u2)
-        s->levels[nd.h1 - 1].br.push_back(BrJob{c, a, 0xE0000000u, 1, 1, 0, r1});
-        s->levels[nd.h2 - 1].br.push_back(BrJob{c, b, 0xE0000000u, -1, 1, 0, r2});
+        s->levels[nd.h1 - 1].br.push_back(BrJob{c, a, 0xE0000000u, static_cast<int8_t>(sc), static_cast<int8_t>(sa), 0, r1});
+        s->levels[nd.h2 - 1].br.push_back(BrJob{c, b, 0xE0000000u, static_cast<int8_t>(-sc), static_cast<int8_t>(sb), 0, r2});
         s->levels[nd.level - 1].ks.push_back(KsJob{r1, r2, kMu, nd.slot});
         s->gates++;
         s->br += 2;
@@ -120,7 +133,7 @@ class Builder {
     s->mid_rows = mid;
     s->nlwe_rows = nl;
     s->out_cts = outs.size();
-    for (uint32_t o : outs) s->out_slots.push_back(nodes[o].slot);
+    for (uint32_t o : outs) s->out_slots.push_back(nodes[node_of(o)].slot);  // outputs are never negated refs
     return VLP_OK;
   }
 
@@ -141,6 +154,58 @@ uint32_t comp(Builder& B, const Word& c1, const Word& c2, int l, bool le, bool u
   return B.mux(t0, uns ? c2[l - 1] : c1[l - 1], t2);
 }
 
+// Log-depth (parallel-prefix) comparator, VLP_F_PREFIX_COMP (NOT in the paper -- reading
+// R23 in DESIGN.md): returns a reference to [c1 > c2] (unsigned).  Bit ranges r = (G, E) with G = [c1 > c2 on
+// the range] and E = [c1 == c2 on the range]; leaves G_i = AND(c1_i, NOT c2_i), E_i = XNOR(c1_i, c2_i);
+// ranges are paired (r[2k+1] high, r[2k] low) level by level, an unpaired top range passing through:
+// G = MUX(H.E, L.G, H.G) (H.G and H.E are exclusive), E = AND(H.E, L.E).  Only the E gates some G needs are
+// built.  Depth 1 + ceil(log2 l) instead of l + 1.
+uint32_t comp_gt_prefix(Builder& B, const Word& c1, const Word& c2, int l) {
+  // tree shape: idx[level] = ranges of that level as (hi child, lo child) indices into the level below
+  std::vector<std::vector<std::pair<int, int>>> lev;
+  for (int m = l; m > 1; m = (m + 1) / 2) {
+    std::vector<std::pair<int, int>> nx;
+    for (int k = 0; 2 * k < m; k++) nx.push_back(2 * k + 1 < m ? std::make_pair(2 * k + 1, 2 * k) : std::make_pair(-1, 2 * k));
+    lev.push_back(nx);
+  }
+  // which ranges need E (top-down): a high child always (for its parent's G), a low child iff its parent's E
+  std::vector<std::vector<char>> needE(lev.size() + 1);
+  needE[0].assign(l, 0);
+  for (size_t L = 0; L < lev.size(); L++) needE[L + 1].assign(lev[L].size(), 0);
+  for (size_t L = lev.size(); L-- > 0;) {
+    for (size_t k = 0; k < lev[L].size(); k++) {
+      const auto [hi, lo] = lev[L][k];
+      if (hi < 0) {
+        needE[L][lo] |= needE[L + 1][k];  // pass-through
+      } else {
+        needE[L][hi] = 1;
+        needE[L][lo] |= needE[L + 1][k];
+      }
+    }
+  }
+  std::vector<uint32_t> G(l), E(l, kNone);
+  for (int i = 0; i < l; i++) {
+    G[i] = B.AND(c1[i], Builder::NOT(c2[i]));
+    if (needE[0][i]) E[i] = B.XNOR(c1[i], c2[i]);
+  }
+  for (size_t L = 0; L < lev.size(); L++) {
+    std::vector<uint32_t> g2(lev[L].size()), e2(lev[L].size(), kNone);
+    for (size_t k = 0; k < lev[L].size(); k++) {
+      const auto [hi, lo] = lev[L][k];
+      if (hi < 0) {
+        g2[k] = G[lo];
+        e2[k] = E[lo];
+        continue;
+      }
+      g2[k] = B.mux(E[hi], G[lo], G[hi]);
+      if (needE[L + 1][k]) e2[k] = B.AND(E[hi], E[lo]);
+    }
+    G.swap(g2);
+    E.swap(e2);
+  }
+  return G[0];
+}
+
 // alg:HomEQ and alg:HomEquiOPT.
 uint32_t eq(Builder& B, const Word& c1, const Word& c2, int l, bool tree) {
   if (!tree) {
@@ -159,12 +224,18 @@ uint32_t eq(Builder& B, const Word& c1, const Word& c2, int l, bool tree) {
 uint32_t validate(Builder& B, const vlp_meta& m, const std::vector<Word>& q, const std::vector<Word>& rec) {
   const int l = static_cast<int>(m.l_I);
   const bool uns = m.flags & VLP_F_UNSIGNED, closed = m.flags & VLP_F_CLOSED_UPPER, tree = m.flags & VLP_F_EQ_TREE;
+  const bool prefix = m.flags & VLP_F_PREFIX_COMP;
+  // CompLE(a, b) = [a <= b] = NOT [a > b]; CompL(a, b) = [a < b] = [b > a] (prefix form)
+  auto cmp = [&](const Word& a, const Word& b, bool le) {
+    if (!prefix) return comp(B, a, b, l, le, uns);
+    return le ? Builder::NOT(comp_gt_prefix(B, a, b, l)) : comp_gt_prefix(B, b, a, l);
+  };
   if (m.mode == VLP_MODE_INTV) {  // alg:InterValid, operand order of P:342-346
-    const uint32_t v_xl = comp(B, rec[0], q[0], l, true, uns);
-    const uint32_t v_xr = comp(B, q[0], rec[1], l, closed, uns);
+    const uint32_t v_xl = cmp(rec[0], q[0], true);
+    const uint32_t v_xr = cmp(q[0], rec[1], closed);
     if (m.d == 1) return B.AND(v_xl, v_xr);
-    const uint32_t v_yl = comp(B, rec[2], q[1], l, true, uns);
-    const uint32_t v_yr = comp(B, q[1], rec[3], l, closed, uns);
+    const uint32_t v_yl = cmp(rec[2], q[1], true);
+    const uint32_t v_yr = cmp(q[1], rec[3], closed);
     const uint32_t v_x = B.AND(v_xl, v_xr);
     const uint32_t v_y = B.AND(v_yl, v_yr);
     return B.AND(v_x, v_y);
@@ -201,6 +272,8 @@ int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, 
   if (int rc = check_meta(&m)) return rc;
   if (count == 0 || first + count > m.M) return fail(VLP_EINVAL, "bad record range");
   if (nq < 1 || nq > 4096) return fail(VLP_EINVAL, "query count must be in [1, 4096]");
+  if ((m.flags & VLP_F_PREFIX_COMP) && !(m.flags & VLP_F_UNSIGNED))
+    return fail(VLP_EINVAL, "the prefix comparator is unsigned only (VLP_F_UNSIGNED)");
   Builder B;
   const size_t l = m.l_I, W = record_words(m), QW = query_words(m), per = W * l + m.l_S;
   if (count * per > kMaxRows || static_cast<size_t>(nq) * QW * l > kMaxRows)

@@ -158,10 +158,12 @@ def _run_config(server, wl, query_seed=7, pk_seed=None):
     return prog, q, db, A.to_host(out)
 
 
-def test_config1_full_parity(server):
+@pytest.mark.parametrize("prefix", [False, True])
+def test_config1_full_parity(server, prefix):
     """Config 1 (IntV 1D tiny): the final aggregate, every record's validation bit and masked payload are
-    byte-equal to the oracle's alg:VeLoPIR, and decrypt to the plain predicate."""
-    wl = make_workload(1, key_seed=SEED)
+    byte-equal to the oracle's alg:VeLoPIR, and decrypt to the plain predicate; also with the R23 prefix
+    comparators (8 levels instead of 13)."""
+    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | (OC.F_PREFIX_COMP if prefix else 0))
     okeys = O.OracleKeys(SEED)
     prog, q, db, out = _run_config(server, wl)
     per = A.record_cts(A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags))
@@ -266,7 +268,8 @@ def _trivial_run(server, mode, d, l_I, l_S, flags, records, payloads, query):
     return A.to_host(out)
 
 
-@pytest.mark.parametrize("case", ["idm32x64", "rect32x64", "cov32", "intv2x1_single", "idm_or_serial"])
+@pytest.mark.parametrize("case", ["idm32x64", "rect32x64", "rect32x64_prefix", "intv32_prefix_halfopen", "cov32",
+                                  "intv2x1_single", "idm_or_serial"])
 def test_all_trivial_extreme_widths(server, case):
     """P11 at the width limits of the ABI (l_I = 32, l_S = 64), a single record (no aggregation tree), the
     minimum comparator width l_I = 2, non-power-of-two M, and the paper-literal serial/OR variants: the
@@ -277,11 +280,16 @@ def test_all_trivial_extreme_widths(server, case):
         mode, d, l_I, l_S, flags = OC.MODE_IDM, 1, 32, 64, OC.CONFIG_FLAGS
         q = [full(32)]
         recs = [(full(32),), (q[0],), (full(32),)]
-    elif case == "rect32x64":
-        mode, d, l_I, l_S, flags = OC.MODE_INTV, 2, 32, 64, OC.CONFIG_FLAGS
+    elif case in ("rect32x64", "rect32x64_prefix"):
+        mode, d, l_I, l_S, flags = OC.MODE_INTV, 2, 32, 64, OC.CONFIG_FLAGS | (OC.F_PREFIX_COMP if "prefix" in case else 0)
         q = [full(31), full(31)]
         recs = [(q[0] - 5, q[0] + 9, q[1] - 1, q[1]), (q[0], q[0], q[1] + 1, q[1] + 2), (0, 2 ** 32 - 1, 0, 2 ** 32 - 1),
                 (q[0] + 1, q[0] + 3, 0, 7), (0, q[0], q[1], 2 ** 32 - 1)]
+    elif case == "intv32_prefix_halfopen":
+        mode, d, l_I, l_S, flags = OC.MODE_INTV, 1, 32, 33, OC.F_UNSIGNED | OC.F_SUM_TREE | OC.F_PREFIX_COMP
+        q = [full(32)]
+        recs = [(q[0], q[0] + 1), (q[0] - 3, q[0]), (0, 2 ** 32 - 1), (q[0] ^ 1, q[0] ^ 1), (0, q[0])]
+        recs = [(lo % 2 ** 32, hi % 2 ** 32) for lo, hi in recs]
     elif case == "cov32":
         mode, d, l_I, l_S, flags = OC.MODE_COV, 2, 32, 40, OC.CONFIG_FLAGS
         q = [full(32), full(32)]
@@ -356,6 +364,13 @@ def test_paper_cov_mode_full_parity(server):
     recs = [(3, 9), (5, 12), (3, 12)]
     want = _full_parity_small(server, OC.MODE_COV, 2, 4, 3, OC.CONFIG_FLAGS, recs, [5, 2, 6], [5, 12])
     assert want == 2
+
+
+def test_prefix_rectangle_half_open_full_parity(server):
+    """R23 prefix comparators on the rectangle circuit with half-open upper bounds (CompL(x, hi) = [hi > x])
+    and the serial HomSum: every record's v and the result byte-equal to the oracle."""
+    recs = [(2, 9, 0, 15), (5, 6, 3, 4), (0, 15, 7, 8), (6, 7, 3, 5)]
+    _full_parity_small(server, OC.MODE_INTV, 2, 4, 3, OC.F_UNSIGNED | OC.F_PREFIX_COMP, recs, [5, 2, 6, 1], [6, 3])
 
 
 def test_paper_literal_intv_serial_full_parity(server):
@@ -503,8 +518,11 @@ def test_device_encrypt_db_equals_host(server, cfg, count):
 
 
 # ------------------------------------------------------------------ pure-function parity of every gate
-_FORMS = {(0xE0000000, 1, 1): O.AND, (0x20000000, -1, -1): O.NAND, (0x20000000, 1, 1): O.OR,
-          (0x40000000, 2, 2): O.XOR, (0xC0000000, -2, -2): O.XNOR}
+# linear form (k0, ax, ay) -> (oracle gate, negate x, negate y); the sign-flipped ANDs are AND gates with
+# NOT (free negation, O11) on an input: the R23 prefix comparator's leaves and the AND of two CompLE results
+_FORMS = {(0xE0000000, 1, 1): (O.AND, 0, 0), (0x20000000, -1, -1): (O.NAND, 0, 0), (0x20000000, 1, 1): (O.OR, 0, 0),
+          (0x40000000, 2, 2): (O.XOR, 0, 0), (0xC0000000, -2, -2): (O.XNOR, 0, 0),
+          (0xE0000000, 1, -1): (O.AND, 0, 1), (0xE0000000, -1, 1): (O.AND, 1, 0), (0xE0000000, -1, -1): (O.AND, 1, 1)}
 
 
 def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
@@ -540,7 +558,9 @@ def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
 
     def one(t):
         if t[1] == "gate":
-            return okeys.gate(t[2], ct(t[3]), ct(t[4]))
+            op, nx, ny = t[2]
+            x, y = ct(t[3]), ct(t[4])
+            return okeys.gate(op, O.OracleKeys.not_(x) if nx else x, O.OracleKeys.not_(y) if ny else y)
         return okeys.mux(ct(t[2]), ct(t[3]), ct(t[4]))
 
     for t, want in zip(todo, POOL.map(one, todo)):
@@ -548,14 +568,20 @@ def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
     return len(todo)
 
 
-def test_config1_every_gate_pure_function(server):
+@pytest.mark.parametrize("prefix", [False, True])
+def test_config1_every_gate_pure_function(server, prefix):
     """SURVEY 4 layer 3: every one of config 1's 188 gate outputs (every level) is byte-equal to the oracle's
-    gate recomputed from the GPU's own inputs."""
-    wl = make_workload(1, key_seed=SEED)
+    gate recomputed from the GPU's own inputs; with the R23 prefix comparators, every one of its gates."""
+    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | (OC.F_PREFIX_COMP if prefix else 0))
     prog, q, db, out = _run_config(server, wl)
     okeys = O.OracleKeys(SEED)
     regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
-    assert _gate_checks(prog, regions, okeys) == 188
+    assert _gate_checks(prog, regions, okeys) == prog.info.gates
+    assert prog.info.levels == (8 if prefix else 13)
+    if not prefix:
+        assert prog.info.gates == 188
+    want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
+    assert server.keys.decrypt_value(out) == want
 
 
 def test_config2_sampled_gates_pure_function(server):

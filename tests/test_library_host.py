@@ -117,6 +117,19 @@ def test_schedule_closed_forms(cfg, br, ks, levels):
     assert (info.br, info.ks, info.levels) == (br, ks, levels)
 
 
+@pytest.mark.parametrize("c,levels", [((0, 4, 8, 8, 1), 8), ((0, 1024, 16, 16, 1), 17), ((0, 4096, 16, 32, 2), 20)])
+def test_prefix_schedule_depth(c, levels):
+    """R23 prefix comparators (VLP_F_PREFIX_COMP): comparator depth 1 + log2 l instead of l + 1, so config 1
+    needs 8 levels (13 ripple), config 2 17 (29), config 3 20 (32); more gates than the ripple form."""
+    m = A.meta(c[0], c[1], c[2], c[3], c[4], L.CONFIG_FLAGS | L.F_PREFIX_COMP)
+    info = _info(m)
+    ripple = _info(A.meta(*c))
+    assert info.levels == levels and info.br > ripple.br
+    bad = A.meta(c[0], c[1], c[2], c[3], c[4], L.F_PREFIX_COMP)  # signed comparators: not supported
+    h = ctypes.c_void_p()
+    assert L.lib().vlp_program_create(None, ctypes.byref(bad), 0, c[1], ctypes.byref(h)) == L.VLP_EINVAL
+
+
 def test_schedule_level_widths_config2():
     """SURVEY 8(d) config 2 widths: L1 32,768; L2 34,816; L3-L17 2,048; L18 1,024; L19 16,384; tree 8,192 -> 16."""
     h = ctypes.c_void_p()

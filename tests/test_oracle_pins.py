@@ -263,6 +263,21 @@ def test_comparators_exhaustive_plain(l):
     assert (B.br, B.ks, r[1]) == (3 * l, 2 * l, l + 1)
 
 
+@pytest.mark.parametrize("l", [1, 2, 3, 4, 5, 6, 7])
+def test_prefix_comparators_exhaustive_plain(l):
+    """R23 (NOT in the paper): the log-depth prefix comparator on the PlainOracle, every
+    pair at width l: [z1 > z2], [z1 <= z2], [z1 < z2] in unsigned order, depth 1 + ceil(log2 l)."""
+    depth = 1 + (math.ceil(math.log2(l)) if l > 1 else 0)
+    for z1, z2 in itertools.product(range(2 ** l), repeat=2):
+        B = C.PlainBackend()
+        a = [B.const(b) for b in P.bits_of(z1, l)]
+        b = [B.const(bb) for bb in P.bits_of(z2, l)]
+        g = C.hom_comp_gt_prefix(B, a, b, l)
+        assert g == (z1 > z2, depth), (z1, z2)
+        assert C.hom_comp_le_prefix(B, a, b, l)[0] == (z1 <= z2)
+        assert C.hom_comp_l_prefix(B, a, b, l)[0] == (z1 < z2)
+
+
 @pytest.mark.parametrize("l", [1, 2, 3, 5, 8, 16, 20])
 def test_equality_plain(l):
     """lem:EQ for the serial and the OPT tree; tree gate count l XNOR +
@@ -286,7 +301,7 @@ def test_velopir_plain_configs():
     rnd = random.Random(17)
     for mode, d, l in [(C.MODE_INTV, 1, 6), (C.MODE_INTV, 2, 4), (C.MODE_COV, 2, 4), (C.MODE_IDM, 1, 5)]:
         for flags in [C.CONFIG_FLAGS, C.CONFIG_FLAGS | C.F_OR_REDUCE, C.F_UNSIGNED,
-                      C.F_CLOSED_UPPER | C.F_UNSIGNED]:
+                      C.F_CLOSED_UPPER | C.F_UNSIGNED, C.CONFIG_FLAGS | C.F_PREFIX_COMP, C.F_UNSIGNED | C.F_PREFIX_COMP]:
             for M in [1, 3, 4, 7]:
                 W = P.record_words(mode, d)
                 recs = []
@@ -321,6 +336,24 @@ def test_tfhe_comparator_small(okeys):
         a = [k.encrypt(b, 31, 10 * z1 + 100 * z2 + j) for j, b in enumerate(P.bits_of(z1, 3))]
         b = [k.encrypt(bb, 32, 10 * z1 + 100 * z2 + j) for j, bb in enumerate(P.bits_of(z2, 3))]
         return k.decrypt(C.hom_comp_le(B, a, b, 3)), int(z1 <= z2)
+
+    for got, want in POOL.map(run, pairs):
+        assert got == want
+
+
+def test_tfhe_prefix_comparator_small(okeys):
+    """R23 on real ciphertexts at l = 3 (AND-with-NOT leaves, XNORs, MUX / AND merges; the result negated
+    for <=): decrypts to the unsigned predicate for a few pairs, threaded."""
+    k = okeys
+    B = C.TfheBackend(k)
+    pairs = [(0, 0), (3, 5), (5, 3), (7, 6), (6, 7), (4, 4)]
+
+    def run(pq):
+        z1, z2 = pq
+        a = [k.encrypt(b, 33, 10 * z1 + 100 * z2 + j) for j, b in enumerate(P.bits_of(z1, 3))]
+        b = [k.encrypt(bb, 34, 10 * z1 + 100 * z2 + j) for j, bb in enumerate(P.bits_of(z2, 3))]
+        return (k.decrypt(C.hom_comp_le_prefix(B, a, b, 3)), k.decrypt(C.hom_comp_l_prefix(B, a, b, 3))), \
+            (int(z1 <= z2), int(z1 < z2))
 
     for got, want in POOL.map(run, pairs):
         assert got == want
