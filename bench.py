@@ -239,6 +239,8 @@ def main():
                     help="queries per step (multi-query packing on one GPU: every level launch carries all of them)")
     ap.add_argument("--prefix-comparator", action="store_true",
                     help="R23 (not in the paper): log-depth prefix comparators (VLP_F_PREFIX_COMP) for IntV configs")
+    ap.add_argument("--linear-sum", action="store_true",
+                    help="R24 (not in the paper): linear XOR aggregation (VLP_F_LINEAR_SUM) instead of the XOR tree")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -267,9 +269,10 @@ def main():
     if args.config == 5:
         return run_nand(args, rank, world, local, dev, stream, A, L, dist)
     wl = make_workload(args.config)
-    if args.prefix_comparator:
-        wl = make_workload(args.config, flags=wl.flags | L.F_PREFIX_COMP)
-    wname = wl.name + ("_prefix" if args.prefix_comparator else "")
+    extra = (L.F_PREFIX_COMP if args.prefix_comparator else 0) | (L.F_LINEAR_SUM if args.linear_sum else 0)
+    if extra:
+        wl = make_workload(args.config, flags=wl.flags | extra)
+    wname = wl.name + ("_prefix" if args.prefix_comparator else "") + ("_linsum" if args.linear_sum else "")
     m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
     first, shard = shard_range(wl.M, world, rank)
     t_setup = time.time()
@@ -347,7 +350,8 @@ def main():
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms = float(tot.item())
     ms_per_step = total_ms / args.steps
-    br_per_query = CONFIG_BR.get(args.config) or prog.info.br // nq * world + (comb.info.br if comb else 0)
+    br_per_query = (CONFIG_BR.get(args.config) if not extra else None) or \
+        prog.info.br // nq * world + (comb.info.br if comb else 0)
     value = nq * br_per_query / (ms_per_step / 1e3)
     records_per_s = nq * wl.M / (ms_per_step / 1e3)
 

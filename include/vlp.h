@@ -57,8 +57,11 @@ enum {
   VLP_F_EQ_TREE = 4,      /* R14: alg:HomEqOPT pairwise AND tree instead of the serial HomEQ */
   VLP_F_SUM_TREE = 8,     /* R15: outermost XOR tree instead of the serial HomSum */
   VLP_F_OR_REDUCE = 16,   /* R19: OR instead of XOR in the aggregation */
-  VLP_F_PREFIX_COMP = 32  /* R23 (NOT in the paper): log-depth parallel-prefix unsigned
+  VLP_F_PREFIX_COMP = 32, /* R23 (NOT in the paper): log-depth parallel-prefix unsigned
                              comparators (depth 1 + ceil(log2 l) instead of l + 1; more gates; needs UNSIGNED) */
+  VLP_F_LINEAR_SUM = 64   /* R24 (NOT in the paper): linear XOR aggregation -- masked bits
+                             in the {0, 1/2} encoding summed without bootstrapping in groups of 64, one refresh
+                             bootstrap per group and bit (XOR only: not with OR_REDUCE) */
 };
 #define VLP_CONFIG_FLAGS (VLP_F_CLOSED_UPPER | VLP_F_UNSIGNED | VLP_F_EQ_TREE | VLP_F_SUM_TREE)
 
@@ -187,7 +190,7 @@ int vlp_program_node_row(const vlp_program* prog, int kind, size_t record, uint3
 typedef struct {
   uint32_t x, y, k0;
   int8_t ax, ay;
-  uint16_t pad;
+  uint16_t tv; /* test vector of the bootstrap: 0 -> 1/8 (R8), 1 -> 1/4 (R24 linear aggregation) */
   uint32_t row;
 } vlp_br_job;
 typedef struct {
@@ -195,6 +198,10 @@ typedef struct {
 } vlp_ks_job;
 int vlp_program_level_jobs(const vlp_program* prog, uint32_t level, vlp_br_job* br, uint64_t* nbr, vlp_ks_job* ks,
                            uint64_t* nks);
+/* R24 linear jobs of level `level` (run after its key switches): jobs [n][4] = (out slot, first, count, 0),
+ * out = sum of the input slots inputs[first .. first + count) mod 2^32.  NULL arrays: counts only. */
+int vlp_program_level_linear(const vlp_program* prog, uint32_t level, uint32_t* jobs, uint64_t* njobs,
+                             uint32_t* inputs, uint64_t* ninputs);
 /* Pointer to the intermediate region inside `scratch_dev` (rows of 632 words). */
 int vlp_program_intermediate_offset(const vlp_program* prog, uint64_t* byte_offset);
 

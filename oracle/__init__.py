@@ -83,6 +83,7 @@ def lib():
                 "oracle_keyswitch": (None, [vp, u32p, u32p]),
                 "oracle_bootstrap_nlwe": (None, [vp, u32p, u32p]),
                 "oracle_bootstrap": (None, [vp, u32p, u32p]),
+                "oracle_bootstrap_mu": (None, [vp, u32p, ctypes.c_uint32, u32p]),
                 "oracle_gate": (None, [vp, ctypes.c_int, u32p, u32p, u32p]),
                 "oracle_mux": (None, [vp, u32p, u32p, u32p, u32p]),
             }
@@ -229,6 +230,12 @@ class OracleKeys:
     def bootstrap(self, c) -> np.ndarray:
         out = np.zeros(n + 1, np.uint32)
         lib().oracle_bootstrap(self._h, _p(u32(c)), _p(out))
+        return out
+
+    def bootstrap_mu(self, c, mu: int) -> np.ndarray:
+        """R24 (not in the paper): bootstrap with test vector mu in every coefficient (R8 uses 1/8)."""
+        out = np.zeros(n + 1, np.uint32)
+        lib().oracle_bootstrap_mu(self._h, _p(u32(c)), mu, _p(out))
         return out
 
     # -- gates (P:162, R10) --

@@ -10,18 +10,21 @@ a gate backend.  Backends:
 
 Readings: R11 (``unsigned``), R12 (``closed_upper``), R13 (rectangle = IntV d=2),
 R14 (``eq_tree``), R15/R19 (``sum_tree``, ``or_reduce``), R16 (mask S_i with its own v_i), R20 (LSB first);
-R23 (``F_PREFIX_COMP``, the log-depth comparator of SURVEY 8(f) NEXT 4 -- not in the paper).
+R23 (``F_PREFIX_COMP``, the log-depth comparator of SURVEY 8(f) NEXT 4 -- not in the paper); R24
+(``F_LINEAR_SUM``, linear XOR aggregation in the {0, 1/2} encoding -- not in the paper).
 """
 from __future__ import annotations
 
 from concurrent.futures import ThreadPoolExecutor
 import os
 
+import numpy as np
+
 from . import AND, NAND, OR, XOR, XNOR, OracleKeys, trivial
 
 # Modes and flags (same values as the product's header, defined independently here).
 MODE_INTV, MODE_COV, MODE_IDM = 0, 1, 2
-F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP = 1, 2, 4, 8, 16, 32
+F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP, F_LINEAR_SUM = 1, 2, 4, 8, 16, 32, 64
 CONFIG_FLAGS = F_CLOSED_UPPER | F_UNSIGNED | F_EQ_TREE | F_SUM_TREE
 
 
@@ -58,6 +61,18 @@ class PlainBackend:
     @staticmethod
     def NOT(x): return (not x[0], x[1])
 
+    # R24 (not in the paper): the {0, 1/2} encoding -- a bit value plus a depth, like every other node
+    def AND_Q(self, x, y): return self._g(x[0] and y[0], x, y)
+
+    @staticmethod
+    def LIN(xs):  # sum of {0, 1/2}-encoded bits = their XOR; no bootstrap, no level
+        v = False
+        for x in xs:
+            v = v != x[0]
+        return (v, max(x[1] for x in xs))
+
+    def REFRESH(self, x, final): return self._g(x[0], x)
+
 
 class TfheBackend:
     """Bootstrapped TFHE gates of the C oracle; trivial constants per R21."""
@@ -76,6 +91,34 @@ class TfheBackend:
     def XNOR(self, x, y): return self.k.gate(XNOR, x, y)
     def MUX(self, c, a, b): return self.k.mux(c, a, b)
     def NOT(self, x): return OracleKeys.not_(x)
+
+    # R24 (not in the paper): bits in the {0, 1/2} encoding (phase b/2), whose sums are XORs
+    def AND_Q(self, x, y):
+        """AND(x, y) into the {0, 1/2} encoding: Bootstrap_{testv 1/4}((0, -1/8) + x + y) + (0, 1/4)."""
+        c = (x.astype(np.uint64) + y.astype(np.uint64)).astype(np.uint32)
+        c[-1] = np.uint32((int(c[-1]) + 0xE0000000) & 0xFFFFFFFF)
+        o = self.k.bootstrap_mu(c, 0x40000000)
+        o[-1] = np.uint32((int(o[-1]) + 0x40000000) & 0xFFFFFFFF)
+        return o
+
+    @staticmethod
+    def LIN(xs):
+        """Sum mod 2^32 of {0, 1/2}-encoded ciphertexts (exact, no bootstrap)."""
+        acc = np.zeros_like(xs[0], dtype=np.uint64)
+        for x in xs:
+            acc = (acc + x.astype(np.uint64)) & 0xFFFFFFFF
+        return acc.astype(np.uint32)
+
+    def REFRESH(self, x, final):
+        """Bootstrap x - (0, 1/4): phase +-1/4 -> the standard +-1/8 encoding (final), or -- test vector 1/4,
+        then + (0, 1/4) -- back into the {0, 1/2} encoding."""
+        c = x.copy()
+        c[-1] = np.uint32((int(c[-1]) + 0xC0000000) & 0xFFFFFFFF)
+        if final:
+            return self.k.bootstrap_mu(c, 0x20000000)
+        o = self.k.bootstrap_mu(c, 0x40000000)
+        o[-1] = np.uint32((int(o[-1]) + 0x40000000) & 0xFFFFFFFF)
+        return o
 
 
 # ------------------------------------------------------------------------------- comparators (P:369-443)
@@ -235,9 +278,26 @@ def hom_sum_tree(B, Ss, l_S, or_reduce=False, pool=None):
     return Ss[0]
 
 
+LIN_GROUP = 64
+
+
+def hom_sum_linear(B, Ss, l_S):
+    """R24 (NOT in the paper): XOR aggregation by sums.  Ss are masked payload bits in the
+    {0, 1/2} encoding.  While more than LIN_GROUP rows remain, each group of LIN_GROUP consecutive rows is
+    summed and refreshed back into the {0, 1/2} encoding; the last sum is refreshed into the standard encoding."""
+    Ss = [list(s) for s in Ss]
+    while len(Ss) > LIN_GROUP:
+        Ss = [[B.REFRESH(B.LIN([Ss[i][j] for i in range(g0, min(len(Ss), g0 + LIN_GROUP))]), False)
+               for j in range(l_S)] for g0 in range(0, len(Ss), LIN_GROUP)]
+    return [B.REFRESH(B.LIN([S[j] for S in Ss]), True) for j in range(l_S)]
+
+
 def record_outputs(B, mode, q, rec, S, l, d, flags):
-    """One iteration of alg:VeLoPIR's record loop: v, then S_i <- HomBitwiseAND(v, S_i)."""
+    """One iteration of alg:VeLoPIR's record loop: v, then S_i <- HomBitwiseAND(v, S_i)
+    (R24: into the {0, 1/2} encoding)."""
     v = validate(B, mode, q, rec, l, d, flags)
+    if flags & F_LINEAR_SUM:
+        return v, [B.AND_Q(v, s) for s in S]
     return v, hom_bitwise_and(B, v, S)
 
 
@@ -254,7 +314,10 @@ def velopir(B, mode, q, records, payloads, l, d, l_S, flags, threads=None):
         vs = [o[0] for o in outs]
         masked = [o[1] for o in outs]
         orr = bool(flags & F_OR_REDUCE)
-        if flags & F_SUM_TREE:
+        if flags & F_LINEAR_SUM:
+            assert not orr, "linear aggregation computes XOR only"
+            R = hom_sum_linear(B, masked, l_S)
+        elif flags & F_SUM_TREE:
             R = hom_sum_tree(B, masked, l_S, orr, pool)
         else:
             R = hom_sum_serial(B, masked, l_S, orr)

@@ -445,15 +445,16 @@ void oracle_external_product(const oracle_keys* k, int i, const uint32_t* D /* [
   free(acc);
 }
 
-/* BlindRotate (O9): acc = (0, X^{-bbar} testv), testv = mu = 1/8 in every coefficient (R8);
+/* BlindRotate (O9): acc = (0, X^{-bbar} testv), testv = mu in every coefficient -- mu = 1/8 for
+ * every gate of the paper (R8); mu = 1/4 only for the R24 linear-aggregation bootstraps (not in the paper);
  * for i = 0..n-1: if abar_i != 0: acc += ExtProd(bsk_i, X^{abar_i} acc - acc).  Works on an
  * already-formed TLWE input c (gate linear form applied by the caller). Output: the TRLWE acc. */
-void oracle_blind_rotate(const oracle_keys* k, const uint32_t* c /* [n+1] */, int steps,
-                         uint32_t* acc /* [2][N] */) {
+void oracle_blind_rotate_mu(const oracle_keys* k, const uint32_t* c /* [n+1] */, int steps, uint32_t mu,
+                            uint32_t* acc /* [2][N] */) {
   uint32_t* testv = malloc(sizeof(uint32_t) * ONR);
   uint32_t* rot = malloc(sizeof(uint32_t) * 2 * ONR);
   uint32_t* ep = malloc(sizeof(uint32_t) * 2 * ONR);
-  for (int j = 0; j < ONR; j++) testv[j] = 0x20000000u;
+  for (int j = 0; j < ONR; j++) testv[j] = mu;
   int bbar = oracle_modswitch(c[ON]);
   memset(acc, 0, sizeof(uint32_t) * ONR);
   poly_mul_monomial(testv, (2 * ONR - bbar) % (2 * ONR), acc + ONR);
@@ -470,6 +471,10 @@ void oracle_blind_rotate(const oracle_keys* k, const uint32_t* c /* [n+1] */, in
   free(testv);
   free(rot);
   free(ep);
+}
+
+void oracle_blind_rotate(const oracle_keys* k, const uint32_t* c, int steps, uint32_t* acc) {
+  oracle_blind_rotate_mu(k, c, steps, 0x20000000u, acc);
 }
 
 /* SampleExtract (S6): a'_0 = a_0, a'_j = -a_{N-j} (j >= 1), b' = b_0. */
@@ -500,6 +505,17 @@ void oracle_bootstrap_nlwe(const oracle_keys* k, const uint32_t* c, uint32_t* nl
   oracle_blind_rotate(k, c, ON, acc);
   oracle_sample_extract(acc, nlwe);
   free(acc);
+}
+
+/* R24: BlindRotate with test vector mu -> SampleExtract -> KeySwitch. */
+void oracle_bootstrap_mu(const oracle_keys* k, const uint32_t* c, uint32_t mu, uint32_t* out) {
+  uint32_t* acc = malloc(sizeof(uint32_t) * 2 * ONR);
+  uint32_t* nlwe = malloc(sizeof(uint32_t) * (ONR + 1));
+  oracle_blind_rotate_mu(k, c, ON, mu, acc);
+  oracle_sample_extract(acc, nlwe);
+  oracle_keyswitch(k, nlwe, out);
+  free(acc);
+  free(nlwe);
 }
 
 /* Bootstrap = BlindRotate -> SampleExtract -> KeySwitch. */

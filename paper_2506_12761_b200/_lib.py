@@ -16,7 +16,7 @@ N = 1024
 VLP_OK, VLP_EINVAL, VLP_EMODE, VLP_EWIDTH, VLP_ERANGE, VLP_EPKUSED, VLP_ECUDA, VLP_ENOMEM, VLP_ENODEV = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)
 MODE_INTV, MODE_COV, MODE_IDM = 0, 1, 2
-F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP = 1, 2, 4, 8, 16, 32
+F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP, F_LINEAR_SUM = 1, 2, 4, 8, 16, 32, 64
 CONFIG_FLAGS = F_CLOSED_UPPER | F_UNSIGNED | F_EQ_TREE | F_SUM_TREE
 AND, NAND, OR, XOR, XNOR, MUX = 0, 1, 2, 3, 4, 5
 
@@ -43,7 +43,7 @@ class VlpProgramInfo(ctypes.Structure):
 
 class VlpBrJob(ctypes.Structure):
     _fields_ = [("x", ctypes.c_uint32), ("y", ctypes.c_uint32), ("k0", ctypes.c_uint32), ("ax", ctypes.c_int8),
-                ("ay", ctypes.c_int8), ("pad", ctypes.c_uint16), ("row", ctypes.c_uint32)]
+                ("ay", ctypes.c_int8), ("tv", ctypes.c_uint16), ("row", ctypes.c_uint32)]
 
 
 class VlpKsJob(ctypes.Structure):
@@ -78,6 +78,8 @@ SIGNATURES = {
     "vlp_program_get_info": (_i, [_vp, ctypes.POINTER(VlpProgramInfo)]),
     "vlp_program_node_row": (_i, [_vp, _i, _sz, ctypes.c_uint32, _u64p]),
     "vlp_program_intermediate_offset": (_i, [_vp, _u64p]),
+    "vlp_program_level_linear": (_i, [_vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32), _u64p,
+                                     ctypes.POINTER(ctypes.c_uint32), _u64p]),
     "vlp_program_level_jobs": (_i, [_vp, ctypes.c_uint32, ctypes.POINTER(VlpBrJob), _u64p, ctypes.POINTER(VlpKsJob),
                                     _u64p]),
     "vlp_program_eval": (_i, [_vp, _vp, _sz, _vp, _vp, _vp, _u64]),

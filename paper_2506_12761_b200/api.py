@@ -313,10 +313,10 @@ class Program:
 
     def level_jobs(self, level: int):
         """(br jobs, ks jobs) of one level of the compiled schedule as numpy structured arrays with the fields
-        of vlp_br_job (x, y, k0, ax, ay, pad, row) and vlp_ks_job (n0, n1, add, out)."""
+        of vlp_br_job (x, y, k0, ax, ay, tv, row) and vlp_ks_job (n0, n1, add, out)."""
         nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
         check(lib().vlp_program_level_jobs(self.h, level, None, ctypes.byref(nb), None, ctypes.byref(nk)))
-        br_t = np.dtype([("x", "<u4"), ("y", "<u4"), ("k0", "<u4"), ("ax", "i1"), ("ay", "i1"), ("pad", "<u2"),
+        br_t = np.dtype([("x", "<u4"), ("y", "<u4"), ("k0", "<u4"), ("ax", "i1"), ("ay", "i1"), ("tv", "<u2"),
                          ("row", "<u4")])
         ks_t = np.dtype([("n0", "<u4"), ("n1", "<u4"), ("add", "<u4"), ("out", "<u4")])
         br = np.zeros(max(1, nb.value), br_t)
@@ -325,6 +325,17 @@ class Program:
                                            ctypes.byref(nb), ks.ctypes.data_as(ctypes.POINTER(L.VlpKsJob)),
                                            ctypes.byref(nk)))
         return br[:nb.value], ks[:nk.value]
+
+    def level_linear(self, level: int):
+        """R24 linear jobs of one level: (jobs uint32 [n, 4] = (out slot, first, count, 0), input slots)."""
+        nj, ni = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib().vlp_program_level_linear(self.h, level, None, ctypes.byref(nj), None, ctypes.byref(ni)))
+        jobs = np.zeros((max(1, nj.value), 4), np.uint32)
+        ins = np.zeros(max(1, ni.value), np.uint32)
+        check(lib().vlp_program_level_linear(self.h, level, jobs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                             ctypes.byref(nj), ins.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                             ctypes.byref(ni)))
+        return jobs[:nj.value], ins[:ni.value]
 
     def intermediate(self):
         """The intermediate-row region of the scratch as an int32 [rows, 632] view (parity dumps)."""

@@ -39,10 +39,11 @@ struct vlp_program {
   vlp_server* server = nullptr;
   vlp::Schedule sched;
   // scratch layout (byte offsets)
-  size_t off_br = 0, off_ks = 0, off_outslots = 0, off_mid = 0, off_nlwe = 0, bytes = 0;
+  size_t off_br = 0, off_ks = 0, off_lin = 0, off_lin_in = 0, off_outslots = 0, off_mid = 0, off_nlwe = 0, bytes = 0;
   size_t off_ks_ws = 0;  // tensor-core key switch staging (ks_stage_bytes)
   uint32_t ks_chunk = 0;
   std::vector<size_t> br_first, ks_first;  // per level, index of the level's first job
+  std::vector<size_t> lin_first, lin_in_first;  // per level (R24 linear jobs and their input slots)
   std::vector<uint32_t> copy_slots;        // outputs that are not written in place
   // host image of the scratch's job-table region [0, off_mid) in pinned memory (allocated on the first
   // evaluation), copied into the caller's scratch by every evaluation: nothing is assumed about what a
@@ -232,18 +233,24 @@ Regions regions(const vlp_program* p, void* scratch, const uint32_t* in0, const 
 
 int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
   Schedule& s = p->sched;
-  size_t nbr = 0, nks = 0;
+  size_t nbr = 0, nks = 0, nlin = 0, nlin_in = 0;
   for (auto& L : s.levels) {
     p->br_first.push_back(nbr);
     p->ks_first.push_back(nks);
+    p->lin_first.push_back(nlin);
+    p->lin_in_first.push_back(nlin_in);
     nbr += L.br.size();
     nks += L.ks.size();
+    nlin += L.lin.size();
+    nlin_in += L.lin_in.size();
   }
   for (uint32_t sl : s.out_slots)
     if ((sl >> 28) != kRegOut) p->copy_slots.push_back(sl);
   p->off_br = 0;
   p->off_ks = align256(p->off_br + nbr * sizeof(BrJob));
-  p->off_outslots = align256(p->off_ks + nks * sizeof(KsJob));
+  p->off_lin = align256(p->off_ks + nks * sizeof(KsJob));
+  p->off_lin_in = align256(p->off_lin + nlin * sizeof(LinJob));
+  p->off_outslots = align256(p->off_lin_in + nlin_in * 4);
   p->off_mid = align256(p->off_outslots + p->copy_slots.size() * 4 + 4);
   p->off_nlwe = align256(p->off_mid + s.mid_rows * kCt * 4);
   size_t max_ks = 0;
@@ -255,7 +262,7 @@ int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
   p->launches = 1 + (p->copy_slots.empty() ? 0 : 1);
   for (auto& L : s.levels) {  // our kernels: BR waves + (indicator, combine) per key-switch GEMM chunk
     p->launches += br_launch_count(static_cast<uint32_t>(L.br.size()), server ? server->sm_count : 148) +
-                   2 * static_cast<uint32_t>((L.ks.size() + p->ks_chunk - 1) / p->ks_chunk);
+                   2 * static_cast<uint32_t>((L.ks.size() + p->ks_chunk - 1) / p->ks_chunk) + (L.lin.empty() ? 0 : 1);
   }
   return VLP_OK;
 }
@@ -450,6 +457,18 @@ int vlp_program_level_jobs(const vlp_program* p, uint32_t level, vlp_br_job* br,
   return VLP_OK;
 }
 
+int vlp_program_level_linear(const vlp_program* p, uint32_t level, uint32_t* jobs, uint64_t* njobs, uint32_t* inputs,
+                             uint64_t* ninputs) {
+  if (!p || !njobs || !ninputs) return fail(VLP_EINVAL, "null argument");
+  if (level >= p->sched.levels.size()) return fail(VLP_EINVAL, "no such level");
+  const Level& lv = p->sched.levels[level];
+  *njobs = lv.lin.size();
+  *ninputs = lv.lin_in.size();
+  if (jobs) std::memcpy(jobs, lv.lin.data(), lv.lin.size() * sizeof(LinJob));
+  if (inputs) std::memcpy(inputs, lv.lin_in.data(), lv.lin_in.size() * 4);
+  return VLP_OK;
+}
+
 int vlp_program_intermediate_offset(const vlp_program* p, uint64_t* off) {
   if (!p || !off) return fail(VLP_EINVAL, "null argument");
   *off = p->off_mid;
@@ -468,6 +487,10 @@ static int stage_tables(vlp_program* p) {
     const Level& lv = p->sched.levels[L];
     if (!lv.br.empty()) std::memcpy(h + p->off_br + p->br_first[L] * sizeof(BrJob), lv.br.data(), lv.br.size() * sizeof(BrJob));
     if (!lv.ks.empty()) std::memcpy(h + p->off_ks + p->ks_first[L] * sizeof(KsJob), lv.ks.data(), lv.ks.size() * sizeof(KsJob));
+    if (!lv.lin.empty()) {
+      std::memcpy(h + p->off_lin + p->lin_first[L] * sizeof(LinJob), lv.lin.data(), lv.lin.size() * sizeof(LinJob));
+      std::memcpy(h + p->off_lin_in + p->lin_in_first[L] * 4, lv.lin_in.data(), lv.lin_in.size() * 4);
+    }
   }
   if (!p->copy_slots.empty()) std::memcpy(h + p->off_outslots, p->copy_slots.data(), p->copy_slots.size() * 4);
   p->tables = h;
@@ -531,6 +554,11 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
       if (int rc = run_keyswitch(s, ka, sc + p->off_ks_ws, p->ks_chunk, st)) return rc;
       p->end(1, st);
     }
+    if (!lv.lin.empty() &&
+        (e = launch_linear(reinterpret_cast<const LinJob*>(sc + p->off_lin) + p->lin_first[L],
+                           reinterpret_cast<const uint32_t*>(sc + p->off_lin_in) + p->lin_in_first[L],
+                           static_cast<uint32_t>(lv.lin.size()), reg, st)))
+      return cuda_fail(e, "linear sums");
   }
   if (!p->copy_slots.empty() &&
       (e = launch_copy_rows(reinterpret_cast<const uint32_t*>(sc + p->off_outslots),

@@ -363,16 +363,17 @@ __global__ void __launch_bounds__(B * kBT, 1) vlp_blind_rotate_kernel(const BrAr
         if (w == static_cast<uint32_t>(n)) c += job.k0;
         abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
       }
+      if (t == 0) abar[n + 1] = job.tv;  // test vector select (R8 / R24)
     } else {
-      for (uint32_t w = t; w <= static_cast<uint32_t>(n); w += kBT) abar[w] = 0;
+      for (uint32_t w = t; w <= static_cast<uint32_t>(n) + 1u; w += kBT) abar[w] = 0;
     }
     __syncthreads();
-    // ---- S4 accumulator init: (0, X^{-bbar} testv), testv = 1/8 everywhere (R8)
+    // ---- S4 accumulator init: (0, X^{-bbar} testv), testv = 1/8 everywhere (R8; 1/4 for R24 jobs)
     {
-      const uint32_t bbar = abar[n];
+      const uint32_t bbar = abar[n], mu = abar[n + 1] ? 2u * kMu : kMu;
       for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT) {
         acc[k] = 0;
-        acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu);
+        acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? mu : (0u - mu);
       }
     }
     __syncthreads();
@@ -616,14 +617,15 @@ __global__ void __launch_bounds__(kLatThreads, 1) vlp_blind_rotate_lat_kernel(co
         if (w == static_cast<uint32_t>(n)) c += job.k0;
         abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
       }
+      if (tid == 0) abar[n + 1] = job.tv;  // test vector select (R8 / R24)
     }
     __syncthreads();
     // ---- S4 accumulator init (R8)
     {
-      const uint32_t bbar = abar[n];
+      const uint32_t bbar = abar[n], mu = abar[n + 1] ? 2u * kMu : kMu;
       for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kLatThreads) {
         acc[k] = 0;
-        acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu);
+        acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? mu : (0u - mu);
       }
     }
     __syncthreads();
@@ -866,12 +868,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kClatThreads, 1)
         if (w == static_cast<uint32_t>(n)) c += job.k0;
         abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
       }
+      if (tid == 0) abar[n + 1] = job.tv;  // test vector select (R8 / R24)
     }
     __syncthreads();
     {  // S4 for component rk: acc_0 = 0, acc_1 = X^{-bbar} testv (R8)
-      const uint32_t bbar = abar[n];
+      const uint32_t bbar = abar[n], mu = abar[n + 1] ? 2u * kMu : kMu;
       for (uint32_t k = tid; k < static_cast<uint32_t>(N); k += kClatThreads)
-        acc[k] = rk == 0 ? 0u : ((((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu));
+        acc[k] = rk == 0 ? 0u : ((((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? mu : (0u - mu));
     }
     __syncthreads();
 
@@ -1101,12 +1104,13 @@ __global__ void __cluster_dims__(kC6, 1, 1) __launch_bounds__(kBT, 1) vlp_blind_
         if (w == static_cast<uint32_t>(n)) c += job.k0;
         abar[w] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
       }
+      if (t == 0) abar[n + 1] = job.tv;  // test vector select (R8 / R24)
     }
     __syncthreads();
     {  // S4 for component u: acc_0 = 0, acc_1 = X^{-bbar} testv (R8)
-      const uint32_t bbar = abar[n];
+      const uint32_t bbar = abar[n], mu = abar[n + 1] ? 2u * kMu : kMu;
       for (uint32_t k = t; k < static_cast<uint32_t>(N); k += kBT)
-        acc[k] = u == 0 ? 0u : ((((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? kMu : (0u - kMu));
+        acc[k] = u == 0 ? 0u : ((((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? mu : (0u - mu));
     }
     __syncthreads();
 
@@ -1395,6 +1399,18 @@ __global__ void vlp_init_constants_kernel(uint32_t* mid) {
   }
 }
 
+// R24 linear aggregation: out slot = sum of the job's input slots mod 2^32 (all 632 words; pad words stay 0).
+__global__ void __launch_bounds__(128) vlp_linear_kernel(const LinJob* __restrict__ jobs, const uint32_t* __restrict__ ins,
+                                                         Regions reg) {
+  const LinJob j = jobs[blockIdx.x];
+  uint32_t* o = slot_wptr(reg, j.out);
+  for (uint32_t w = threadIdx.x; w < static_cast<uint32_t>(kCt); w += blockDim.x) {
+    uint32_t acc = 0;
+    for (uint32_t i = 0; i < j.count; i++) acc += slot_ptr(reg, ins[j.first + i])[w];
+    o[w] = acc;
+  }
+}
+
 __global__ void vlp_copy_rows_kernel(const uint32_t* __restrict__ slots, Regions reg, uint32_t* out) {
   const uint32_t* src = slot_ptr(reg, slots[blockIdx.x]);
   for (uint32_t k = threadIdx.x; k < static_cast<uint32_t>(kCt); k += blockDim.x)
@@ -1613,6 +1629,12 @@ cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const 
 
 cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st) {
   vlp_init_constants_kernel<<<1, 256, 0, st>>>(mid);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_linear(const LinJob* jobs, const uint32_t* inputs, uint32_t count, Regions reg, cudaStream_t st) {
+  if (!count) return cudaSuccess;
+  vlp_linear_kernel<<<count, 128, 0, st>>>(jobs, inputs, reg);
   return cudaGetLastError();
 }
 

@@ -83,5 +83,6 @@ cudaError_t launch_ks_indicator(const KsArgs& a, uint32_t c0, uint32_t cnt, int8
 cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const int32_t* d, cudaStream_t st);
 cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st);
 cudaError_t launch_copy_rows(const uint32_t* slots, uint32_t count, Regions reg, uint32_t* out, cudaStream_t st);
+cudaError_t launch_linear(const LinJob* jobs, const uint32_t* inputs, uint32_t count, Regions reg, cudaStream_t st);
 
 }  // namespace vlp

@@ -34,9 +34,11 @@ struct LinForm {
   uint32_t k0;
   int8_t ax, ay;
 };
+constexpr int kOpRefresh = 100;  // R24 refresh bootstrap of a {0, 1/2}-encoded sum: c = x - 1/4
 // S2 / R10 linear forms: c = (0, k0) + ax*x + ay*y.
 LinForm form(int op) {
   switch (op) {
+    case kOpRefresh: return {0xC0000000u, 1, 0};
     case VLP_AND: return {0xE0000000u, 1, 1};
     case VLP_NAND: return {0x20000000u, -1, -1};
     case VLP_OR: return {0x20000000u, 1, 1};
@@ -46,12 +48,14 @@ LinForm form(int op) {
 }
 
 struct Node {
-  uint8_t kind;  // 0 leaf, 1 gate, 2 mux
+  uint8_t kind;  // 0 leaf, 1 gate, 2 mux, 3 linear sum (R24; in[0] = index into Builder::lin_inputs)
   uint8_t op;
   uint32_t in[3];
-  uint32_t level;      // level at which the output exists (0 for leaves)
+  uint32_t level;      // level at which the output exists (0 for leaves; a linear sum: its inputs' level)
   uint32_t h1, h2;     // MUX half levels
   uint32_t slot;       // leaf: fixed slot id; gate: assigned at finalize
+  uint8_t tv = 0;      // gate: test vector (0: 1/8, 1: 1/4)
+  uint32_t add = 0;    // gate: constant added to b' before the key switch
 };
 
 class Builder {
@@ -80,6 +84,22 @@ class Builder {
     return static_cast<uint32_t>(nodes.size() - 1);
   }
   static uint32_t NOT(uint32_t ref) { return ref ^ kNeg; }
+  // a gate with a non-default test vector / post-bootstrap constant (R24)
+  uint32_t gate_tv(int op, uint32_t x, uint32_t y, uint8_t tv, uint32_t add) {
+    const uint32_t g = gate(op, x, y);
+    nodes[g].tv = tv;
+    nodes[g].add = add;
+    return g;
+  }
+  // R24: sum of {0, 1/2}-encoded ciphertexts (exact, no bootstrap), available in its inputs' level
+  uint32_t lin(const std::vector<uint32_t>& refs) {
+    uint32_t l = 0;
+    for (uint32_t r : refs) l = std::max(l, lvl(r));
+    lin_inputs.push_back(refs);
+    nodes.push_back(Node{3, 0, {static_cast<uint32_t>(lin_inputs.size() - 1), kNone, kNone}, l, 0, 0, kNone});
+    return static_cast<uint32_t>(nodes.size() - 1);
+  }
+  std::vector<std::vector<uint32_t>> lin_inputs;
   uint32_t AND(uint32_t x, uint32_t y) { return gate(VLP_AND, x, y); }
   uint32_t OR(uint32_t x, uint32_t y) { return gate(VLP_OR, x, y); }
   uint32_t XOR(uint32_t x, uint32_t y) { return gate(VLP_XOR, x, y); }
@@ -89,7 +109,7 @@ class Builder {
   // hold a 28-bit row (slot()): a schedule with more intermediate rows is refused.
   int finalize(const std::vector<uint32_t>& outs, Schedule* s) {
     size_t gates = 0;
-    for (auto& nd : nodes) gates += nd.kind != 0;
+    for (auto& nd : nodes) gates += nd.kind != 0;  // every non-leaf node owns an intermediate row
     if (gates + 2 > kMaxRows || outs.size() > kMaxRows)
       return fail(VLP_EINVAL, "schedule too large: more than 2^28 ciphertext rows in one region");
     std::vector<uint32_t> out_index(nodes.size(), kNone);
@@ -112,8 +132,8 @@ class Builder {
         const uint32_t row = nl++;
         s->levels[nd.level - 1].br.push_back(BrJob{sl(nd.in[0]), sl(nd.in[1]), f.k0,
                                                    static_cast<int8_t>(f.ax * sgn(nd.in[0])),
-                                                   static_cast<int8_t>(f.ay * sgn(nd.in[1])), 0, row});
-        s->levels[nd.level - 1].ks.push_back(KsJob{row, kNone, 0u, nd.slot});
+                                                   static_cast<int8_t>(f.ay * sgn(nd.in[1])), nd.tv, row});
+        s->levels[nd.level - 1].ks.push_back(KsJob{row, kNone, nd.add, nd.slot});
         s->gates++;
         s->br++;
         s->ks++;
@@ -128,6 +148,14 @@ class Builder {
         s->gates++;
         s->br += 2;
         s->ks++;
+      } else if (nd.kind == 3) {
+        Level& L = s->levels[nd.level - 1];
+        const auto& ins = lin_inputs[nd.in[0]];
+        L.lin.push_back(LinJob{nd.slot, static_cast<uint32_t>(L.lin_in.size()), static_cast<uint32_t>(ins.size()), 0});
+        for (uint32_t r : ins) {
+          if (r & kNeg) return fail(VLP_EINVAL, "internal: negated input of a linear sum");
+          L.lin_in.push_back(sl(r));
+        }
       }
     }
     s->mid_rows = mid;
@@ -248,6 +276,38 @@ uint32_t validate(Builder& B, const vlp_meta& m, const std::vector<Word>& q, con
   return eq(B, q[0], rec[0], l, tree);  // IdM
 }
 
+// R24 (NOT in the paper): linear XOR aggregation.  The masked bits arrive in the {0, 1/2}
+// encoding (mask bootstraps with test vector 1/4, then + 1/4), so a sum of ciphertexts is the XOR of their
+// bits; groups of kLinGroup consecutive records are summed without bootstrapping (noise grows by
+// sqrt(kLinGroup): 8 sigma of margin at 64) and each group sum is refreshed by one bootstrap of x - 1/4 --
+// test vector 1/4 (+ 1/4 again) while groups remain, test vector 1/8 for the final result (the standard
+// encoding decrypt_result expects).
+constexpr size_t kLinGroup = 64;
+Word aggregate_linear(Builder& B, std::vector<Word> S, size_t l_S) {
+  while (S.size() > kLinGroup) {
+    std::vector<Word> up;
+    for (size_t g0 = 0; g0 < S.size(); g0 += kLinGroup) {
+      Word w(l_S);
+      for (size_t j = 0; j < l_S; j++) {
+        std::vector<uint32_t> ins;
+        for (size_t i = g0; i < std::min(S.size(), g0 + kLinGroup); i++) ins.push_back(S[i][j]);
+        const uint32_t t = B.lin(ins);
+        w[j] = B.gate_tv(kOpRefresh, t, t, 1, 0x40000000u);
+      }
+      up.push_back(w);
+    }
+    S.swap(up);
+  }
+  Word R(l_S);
+  for (size_t j = 0; j < l_S; j++) {
+    std::vector<uint32_t> ins;
+    for (auto& w : S) ins.push_back(w[j]);
+    const uint32_t t = B.lin(ins);
+    R[j] = B.gate_tv(kOpRefresh, t, t, 0, 0u);
+  }
+  return R;
+}
+
 // HomSum tree (R15) or serial alg:HomSum; XOR or OR (R19).  Returns the root word.
 Word aggregate(Builder& B, std::vector<Word> S, size_t l_S, uint32_t flags) {
   const int op = (flags & VLP_F_OR_REDUCE) ? VLP_OR : VLP_XOR;
@@ -274,6 +334,8 @@ int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, 
   if (nq < 1 || nq > 4096) return fail(VLP_EINVAL, "query count must be in [1, 4096]");
   if ((m.flags & VLP_F_PREFIX_COMP) && !(m.flags & VLP_F_UNSIGNED))
     return fail(VLP_EINVAL, "the prefix comparator is unsigned only (VLP_F_UNSIGNED)");
+  const bool linear = m.flags & VLP_F_LINEAR_SUM;
+  if (linear && (m.flags & VLP_F_OR_REDUCE)) return fail(VLP_EINVAL, "linear aggregation computes XOR only");
   Builder B;
   const size_t l = m.l_I, W = record_words(m), QW = query_words(m), per = W * l + m.l_S;
   if (count * per > kMaxRows || static_cast<size_t>(nq) * QW * l > kMaxRows)
@@ -300,9 +362,10 @@ int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, 
       const uint32_t v = validate(B, m, q, recs[r]);
       if (qi == 0) vs[r] = v;
       masked[r].resize(m.l_S);
-      for (size_t j = 0; j < m.l_S; j++) masked[r][j] = B.AND(v, pays[r][j]);  // alg:HomBitwiseAND (R16)
+      for (size_t j = 0; j < m.l_S; j++)  // alg:HomBitwiseAND (R16); R24: into the {0, 1/2} encoding
+        masked[r][j] = linear ? B.gate_tv(VLP_AND, v, pays[r][j], 1, 0x40000000u) : B.AND(v, pays[r][j]);
     }
-    const Word root = aggregate(B, masked, m.l_S, m.flags);
+    const Word root = linear ? aggregate_linear(B, masked, m.l_S) : aggregate(B, masked, m.l_S, m.flags);
     outs.insert(outs.end(), root.begin(), root.end());
     if (qi == 0) masked0 = masked;
   }

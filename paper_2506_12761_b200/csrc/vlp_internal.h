@@ -71,7 +71,7 @@ struct BrJob {       // one blind rotation: input c = k0 + ax*x + ay*y (linear f
   uint32_t x, y;     // slot ids (region << 28 | row)
   uint32_t k0;       // constant added to b
   int8_t ax, ay;     // coefficients
-  uint16_t pad;
+  uint16_t tv;       // test vector: 0 -> mu = 1/8 (R8); 1 -> mu = 1/4 (R24 linear aggregation)
   uint32_t out;      // N-LWE row
 };
 struct KsJob {       // one key switch of nlwe[n0] (+ nlwe[n1] + (0, add) for MUX, S7)
@@ -85,9 +85,16 @@ static_assert(sizeof(KsJob) == 16, "KsJob layout");
 enum Region : uint32_t { kRegIn0 = 0, kRegIn1 = 1, kRegMid = 2, kRegOut = 3 };
 inline uint32_t slot(uint32_t region, uint32_t row) { return (region << 28) | row; }
 
+struct LinJob {      // R24: out slot = sum of `count` input slots (mod 2^32, no bootstrap), after the level's KS
+  uint32_t out, first, count, pad;  // first: index into the level's lin_in
+};
+static_assert(sizeof(LinJob) == 16, "LinJob layout");
+
 struct Level {
   std::vector<BrJob> br;
   std::vector<KsJob> ks;
+  std::vector<LinJob> lin;
+  std::vector<uint32_t> lin_in;  // input slot ids of the level's linear jobs
 };
 
 // Circuit compiler output (sched.cpp)

@@ -20,6 +20,7 @@ from oracle import protocol as OP  # noqa: E402
 from paper_2506_12761_b200 import _lib as L  # noqa: E402
 from paper_2506_12761_b200 import api as A  # noqa: E402
 from synth import make_workload, nand_inputs  # noqa: E402
+from synth.workloads import expected_result  # noqa: E402
 
 POOL = ThreadPoolExecutor(max_workers=max(4, os.cpu_count() or 4))
 SEED = 123
@@ -158,12 +159,16 @@ def _run_config(server, wl, query_seed=7, pk_seed=None):
     return prog, q, db, A.to_host(out)
 
 
-@pytest.mark.parametrize("prefix", [False, True])
-def test_config1_full_parity(server, prefix):
+_VARIANT_FLAGS = {"paper": 0, "prefix": OC.F_PREFIX_COMP, "linear": OC.F_LINEAR_SUM,
+                  "prefix+linear": OC.F_PREFIX_COMP | OC.F_LINEAR_SUM}
+
+
+@pytest.mark.parametrize("variant", list(_VARIANT_FLAGS))
+def test_config1_full_parity(server, variant):
     """Config 1 (IntV 1D tiny): the final aggregate, every record's validation bit and masked payload are
     byte-equal to the oracle's alg:VeLoPIR, and decrypt to the plain predicate; also with the R23 prefix
-    comparators (8 levels instead of 13)."""
-    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | (OC.F_PREFIX_COMP if prefix else 0))
+    comparators (8 levels instead of 13) and / or the R24 linear aggregation (masks in the {0, 1/2} encoding)."""
+    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | _VARIANT_FLAGS[variant])
     okeys = O.OracleKeys(SEED)
     prog, q, db, out = _run_config(server, wl)
     per = A.record_cts(A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags))
@@ -547,8 +552,12 @@ def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
             k = ks[i]
             if int(k["n1"]) == 0xFFFFFFFF:
                 j = by_row[int(k["n0"])]
-                op = _FORMS[(int(j["k0"]), int(j["ax"]), int(j["ay"]))]
-                todo.append((int(k["out"]), "gate", op, int(j["x"]), int(j["y"])))
+                form = (int(j["k0"]), int(j["ax"]), int(j["ay"]))
+                if int(j["tv"]) == 0 and int(k["add"]) == 0 and form in _FORMS:
+                    todo.append((int(k["out"]), "gate", _FORMS[form], int(j["x"]), int(j["y"])))
+                else:  # R24 bootstraps: test vector 1/4 and / or a constant after the key switch
+                    assert int(k["add"]) in (0, 0x40000000) and int(j["tv"]) in (0, 1), (form, k)
+                    todo.append((int(k["out"]), "lin-form", form + (int(j["tv"]), int(k["add"])), int(j["x"]), int(j["y"])))
             else:
                 j1, j2 = by_row[int(k["n0"])], by_row[int(k["n1"])]
                 assert (int(j1["k0"]), int(j1["ax"]), int(j1["ay"])) == (0xE0000000, 1, 1)
@@ -561,6 +570,13 @@ def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
             op, nx, ny = t[2]
             x, y = ct(t[3]), ct(t[4])
             return okeys.gate(op, O.OracleKeys.not_(x) if nx else x, O.OracleKeys.not_(y) if ny else y)
+        if t[1] == "lin-form":  # c = (0, k0) + ax x + ay y; bootstrap with test vector 1/8 or 1/4; + (0, add)
+            k0, ax, ay, tv, add = t[2]
+            c = (ax * ct(t[3]).astype(np.int64) + ay * ct(t[4]).astype(np.int64)) % 2 ** 32
+            c[-1] = (c[-1] + k0) % 2 ** 32
+            o = okeys.bootstrap_mu(c.astype(np.uint32), 0x40000000 if tv else 0x20000000)
+            o[-1] = np.uint32((int(o[-1]) + add) % 2 ** 32)
+            return o
         return okeys.mux(ct(t[2]), ct(t[3]), ct(t[4]))
 
     for t, want in zip(todo, POOL.map(one, todo)):
@@ -568,20 +584,54 @@ def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
     return len(todo)
 
 
-@pytest.mark.parametrize("prefix", [False, True])
-def test_config1_every_gate_pure_function(server, prefix):
+@pytest.mark.parametrize("variant", list(_VARIANT_FLAGS))
+def _linear_checks(prog, regions):
+    """R24: every linear job's output row equals the sum of its input rows mod 2^32.  Returns the count."""
+    def ct(slot):
+        return regions[slot >> 28][slot & 0x0FFFFFFF, :632].astype(np.uint64)
+
+    n = 0
+    for lvl in range(prog.info.levels):
+        jobs, ins = prog.level_linear(lvl)
+        for out, first, count, _ in jobs:
+            want = sum(ct(int(ins[first + i])) for i in range(count)) % 2 ** 32
+            assert np.array_equal(ct(int(out)), want), (lvl, out)
+            n += 1
+    return n
+
+
+@pytest.mark.parametrize("variant", list(_VARIANT_FLAGS))
+def test_config1_every_gate_pure_function(server, variant):
     """SURVEY 4 layer 3: every one of config 1's 188 gate outputs (every level) is byte-equal to the oracle's
-    gate recomputed from the GPU's own inputs; with the R23 prefix comparators, every one of its gates."""
-    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | (OC.F_PREFIX_COMP if prefix else 0))
+    gate recomputed from the GPU's own inputs; with the R23 / R24 variants, every one of their gates and every
+    linear sum."""
+    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | _VARIANT_FLAGS[variant])
     prog, q, db, out = _run_config(server, wl)
     okeys = O.OracleKeys(SEED)
     regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
     assert _gate_checks(prog, regions, okeys) == prog.info.gates
-    assert prog.info.levels == (8 if prefix else 13)
-    if not prefix:
+    nlin = _linear_checks(prog, regions)
+    assert prog.info.levels == {"paper": 13, "prefix": 8, "linear": 12, "prefix+linear": 7}[variant]
+    assert (nlin > 0) == ("linear" in variant)
+    if variant == "paper":
         assert prog.info.gates == 188
     want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
     assert server.keys.decrypt_value(out) == want
+
+
+def test_config2_linear_aggregation(server):
+    """R24 at config 2's full size (1024 records = 16 groups of 64): 115,984 BR in 21 levels instead of 132,080
+    in 29; the result decrypts to the predicate; the refresh levels' gates (all of them), 8 masks and every
+    linear sum are byte-equal to the oracle's recomputation from the GPU's own inputs."""
+    wl = make_workload(2, key_seed=SEED, flags=OC.CONFIG_FLAGS | OC.F_LINEAR_SUM)
+    prog, q, db, out = _run_config(server, wl)
+    assert (prog.info.br, prog.info.levels) == (115984, 21)
+    assert server.keys.decrypt_value(out) == expected_result(wl)
+    okeys = O.OracleKeys(SEED)
+    regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
+    assert _gate_checks(prog, regions, okeys, levels=[19, 20]) == 16 * 16 + 16
+    assert _gate_checks(prog, regions, okeys, levels=[18], per_level=8, seed=3) == 8
+    assert _linear_checks(prog, regions) == 16 * 16 + 16
 
 
 def test_config2_sampled_gates_pure_function(server):

@@ -130,6 +130,19 @@ def test_prefix_schedule_depth(c, levels):
     assert L.lib().vlp_program_create(None, ctypes.byref(bad), 0, c[1], ctypes.byref(h)) == L.VLP_EINVAL
 
 
+def test_linear_aggregation_schedule():
+    """R24 (VLP_F_LINEAR_SUM): config 2's (M-1) l_S = 16,368 tree bootstraps become 16 x 16 group refreshes +
+    16 final ones (levels 29 -> 21); XOR only (OR_REDUCE refused)."""
+    m = A.meta(0, 1024, 16, 16, 1, L.CONFIG_FLAGS | L.F_LINEAR_SUM)
+    info = _info(m)
+    assert (info.br, info.ks, info.levels) == (132080 - 16368 + 272, 99312 - 16368 + 272, 21)
+    small = _info(A.meta(0, 4, 8, 8, 1, L.CONFIG_FLAGS | L.F_LINEAR_SUM))
+    assert (small.br, small.levels) == (252 - 24 + 8, 12)
+    bad = A.meta(0, 4, 8, 8, 1, L.CONFIG_FLAGS | L.F_LINEAR_SUM | L.F_OR_REDUCE)
+    h = ctypes.c_void_p()
+    assert L.lib().vlp_program_create(None, ctypes.byref(bad), 0, 4, ctypes.byref(h)) == L.VLP_EINVAL
+
+
 def test_schedule_level_widths_config2():
     """SURVEY 8(d) config 2 widths: L1 32,768; L2 34,816; L3-L17 2,048; L18 1,024; L19 16,384; tree 8,192 -> 16."""
     h = ctypes.c_void_p()

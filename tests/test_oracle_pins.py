@@ -136,6 +136,20 @@ def test_trivial_bootstrap_closed_form(okeys):
         assert int(out[O.n]) == w, (hex(b), hex(int(out[O.n])), hex(w))
 
 
+def test_trivial_bootstrap_mu_closed_form(okeys):
+    """R24 (not in the paper): the same closed form with test vector 1/4 -- output (0, +-2^30) exactly, with
+    the sign of P3; so the R24 mask (+ 1/4) lands on (0, 1/2) or (0, 0) and the refresh of x - 1/4 reads it."""
+    bs = [0, 0x20000000, 0xE0000000, 0x80000000, 0xFFF00000, 0xFFEFFFFF, 0x7FEFFFFF, 0x7FF00000]
+    bs += [random.Random(9).randrange(2 ** 32) for _ in range(4)]
+    outs = list(POOL.map(lambda b: okeys.bootstrap_mu(O.trivial_mu(b), 0x40000000), bs))
+    for b, out in zip(bs, outs):
+        want = 0x40000000 if (((b + 2 ** 20) >> 21) % 2048) < 1024 else 0xC0000000
+        assert not out[:O.n].any(), hex(b)
+        assert int(out[O.n]) == want, (hex(b), hex(int(out[O.n])))
+    # mu = 1/8 through the same entry point is the P3 bootstrap itself
+    assert np.array_equal(okeys.bootstrap_mu(O.trivial_mu(0x12345678), 0x20000000), okeys.bootstrap(O.trivial_mu(0x12345678)))
+
+
 # ----------------------------------------------------------------------------------- P4: external product
 def test_external_product_invariant(okeys_noiseless):
     """P4, sigma = 0 keys: phase(ExtProd(bsk_i, D)) = 0 exactly if s_i = 0, and phase(D) + eps with
@@ -293,6 +307,25 @@ def test_equality_plain(l):
         r = C.hom_eq_tree(B2, a, b, l)
         assert r[0] == (z1 == z2)
         assert B2.br == 2 * l - 1 and r[1] == math.ceil(math.log2(l)) + 1
+
+
+@pytest.mark.parametrize("M", [1, 2, 63, 64, 65, 200, 4100])
+def test_linear_aggregation_plain(M):
+    """R24 on the PlainOracle: XOR of the matching records' payloads for record counts around the group size
+    (64) and past two group levels (4100); depth = mask level + one refresh level per group level."""
+    rnd = random.Random(M)
+    l, l_S = 4, 3
+    recs = [sorted((rnd.randrange(16), rnd.randrange(16))) for _ in range(M)]
+    q = [rnd.randrange(16)]
+    pays = [rnd.randrange(8) for _ in range(M)]
+    B = C.PlainBackend()
+    qc = [[B.const(b) for b in P.bits_of(v, l)] for v in q]
+    rc = [[[B.const(b) for b in P.bits_of(v, l)] for v in r] for r in recs]
+    pc = [[B.const(b) for b in P.bits_of(v, l_S)] for v in pays]
+    R, vs, _ = C.velopir(B, C.MODE_INTV, qc, rc, pc, l, 1, l_S, C.CONFIG_FLAGS | C.F_LINEAR_SUM, threads=1)
+    assert sum(int(b[0]) << j for j, b in enumerate(R)) == C.plain_result(C.MODE_INTV, q, recs, pays, 1, C.CONFIG_FLAGS)
+    groups = 1 + (M > 64) + (M > 4096)
+    assert max(b[1] for b in R) == max(v[1] for v in vs) + 1 + groups
 
 
 def test_velopir_plain_configs():
