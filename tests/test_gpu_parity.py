@@ -436,6 +436,33 @@ def test_problem_statement_calls(server, okeys):
     assert np.array_equal(k.decrypt_bits(got), np.where(bits3[0] == 1, bits3[1], bits3[2]))
 
 
+def test_linear_aggregation_sharded_decrypts(server):
+    """R24 with sharding: every shard refreshes its own sum into the standard encoding and the roots combine
+    through the XOR tree (vlp_server_combine), so 2- and 4-shard results decrypt to the same predicate as the
+    single-shot result (decrypt-equal; R24 bytes depend on the shard count)."""
+    wl = make_workload(6, key_seed=SEED)
+    wl = make_workload(6, key_seed=SEED, M=8, flags=wl.flags | OC.F_LINEAR_SUM)
+    k = server.keys
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    q = A.to_device(k.encrypt_query(m, wl.query, 7))
+    db = A.to_device(k.encrypt_db(m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1))
+    want = expected_result(wl)
+    one = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    server.eval(m, q, db, one)
+    torch.cuda.synchronize()
+    assert k.decrypt_value(A.to_host(one)) == want
+    per = A.record_cts(m)
+    for G in (2, 4):
+        sh = wl.M // G
+        roots = torch.zeros((G, wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+        for r in range(G):
+            server.eval(m, q, db[r * sh * per:(r + 1) * sh * per], roots[r], first=r * sh, count=sh)
+        comb = torch.zeros_like(one)
+        server.combine(m, G, roots, comb)
+        torch.cuda.synchronize()
+        assert k.decrypt_value(A.to_host(comb)) == want, G
+
+
 def test_single_record_min_width_full_parity(server):
     """Degenerate instance on real encryptions: one record (no aggregation tree, the masked payload is the
     result), the minimum comparator width l_I = 2 and a 1-bit payload."""
@@ -458,14 +485,21 @@ def test_dataset_shapes_predicate(server, cfg):
     assert server.keys.decrypt_value(out) == want
 
 
-def test_multi_query_batch_equals_single(server):
-    """Multi-query packing (vlp_server_eval_batch): 3 queries against the gdacs-shaped DB in one schedule; each
-    result is byte-equal to its own single-query vlp_server_eval and decrypts to its plain predicate."""
-    wl = make_workload(8, key_seed=SEED)
+@pytest.mark.parametrize("cfg,extra", [(8, 0), (6, OC.F_PREFIX_COMP | OC.F_LINEAR_SUM)])
+def test_multi_query_batch_equals_single(server, cfg, extra):
+    """Multi-query packing (vlp_server_eval_batch): 3 queries against the gdacs-shaped DB (and the covid-kor
+    shape with the R23 + R24 options) in one schedule; each result is byte-equal to its own single-query
+    vlp_server_eval and decrypts to its plain predicate."""
+    wl = make_workload(cfg, key_seed=SEED)
+    if extra:
+        wl = make_workload(cfg, key_seed=SEED, flags=wl.flags | extra)
     k = server.keys
     m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
     db = A.to_device(k.encrypt_db(m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1))
-    qvals = [[int(v) for v in wl.records[0]], [int(v) for v in wl.records[5]], [123, 456]]
+    if wl.mode == OC.MODE_INTV:  # points inside record 0's box, record 5's box, and an arbitrary point
+        qvals = [[int(wl.records[r][2 * a]) for a in range(wl.d)] for r in (0, 5)] + [[123, 456][:wl.d]]
+    else:
+        qvals = [[int(v) for v in wl.records[0]], [int(v) for v in wl.records[5]], [123, 456]]
     qs = [k.encrypt_query(m, qv, 40 + i) for i, qv in enumerate(qvals)]
     out = torch.zeros((3 * wl.l_S, 632), dtype=torch.int32, device="cuda:0")
     server.eval_batch(m, A.to_device(np.concatenate(qs)), db, out, 3)
