@@ -164,9 +164,12 @@ class Server:
 
     # ---- the problem-statement calls (vlp_server_eval / vlp_server_combine / vlp_gate_batch): schedules are
     # compiled and cached inside the library; the scratch buffers are torch tensors owned here
-    def _scratch(self, key, nbytes):
+    def _scratch(self, key, nbytes, stream_handle):
+        """One scratch tensor per (call shape, stream): evaluations on one stream are ordered (each reloads its
+        job tables first), evaluations on different streams may run concurrently and get separate buffers."""
         import torch
         cache = self.__dict__.setdefault("_scratch_cache", {})
+        key = key + (stream_handle,)
         t = cache.get(key)
         if t is None or t.numel() < nbytes:
             t = torch.empty(max(256, nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
@@ -181,10 +184,11 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_server_workspace_bytes(ctypes.byref(m), count, None, None, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sc = self._scratch(key, self._ws[key])
+        sh = _stream_handle(stream)
+        sc = self._scratch(key, self._ws[key], sh)
         check(lib().vlp_server_eval(self.h, ctypes.byref(m), first, count, ctypes.c_void_p(query_dev.data_ptr()),
                                     ctypes.c_void_p(db_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
-                                    ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream)))
+                                    ctypes.c_void_p(sc.data_ptr()), sc.numel(), sh))
 
     def eval_batch(self, m: VlpMeta, queries_dev, db_dev, out_dev, nq: int, first: int = 0,
                    count: int | None = None, stream=None):
@@ -195,11 +199,12 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_server_batch_workspace_bytes(ctypes.byref(m), count, nq, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sc = self._scratch(key, self._ws[key])
+        sh = _stream_handle(stream)
+        sc = self._scratch(key, self._ws[key], sh)
         check(lib().vlp_server_eval_batch(self.h, ctypes.byref(m), nq, first, count,
                                           ctypes.c_void_p(queries_dev.data_ptr()), ctypes.c_void_p(db_dev.data_ptr()),
                                           ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(sc.data_ptr()),
-                                          sc.numel(), _stream_handle(stream)))
+                                          sc.numel(), sh))
 
     def combine(self, m: VlpMeta, G: int, partials_dev, out_dev, stream=None):
         key = ("combine", bytes(m), G)
@@ -207,10 +212,11 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_server_combine_workspace_bytes(ctypes.byref(m), G, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sc = self._scratch(key, self._ws[key])
+        sh = _stream_handle(stream)
+        sc = self._scratch(key, self._ws[key], sh)
         check(lib().vlp_server_combine(self.h, ctypes.byref(m), G, ctypes.c_void_p(partials_dev.data_ptr()),
                                        ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(sc.data_ptr()),
-                                       sc.numel(), _stream_handle(stream)))
+                                       sc.numel(), sh))
 
     def gate_batch(self, op: int, a_dev, b_dev, out_dev, c_dev=None, stream=None):
         """A batch of independent gates (config 5): out = op(a, b), or MUX(a, b, c) = a ? b : c."""
@@ -220,10 +226,11 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_gate_batch_workspace_bytes(op, count, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sc = self._scratch(key, self._ws[key])
+        sh = _stream_handle(stream)
+        sc = self._scratch(key, self._ws[key], sh)
         p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
         check(lib().vlp_gate_batch(self.h, op, p(a_dev), p(b_dev), p(c_dev), p(out_dev), count,
-                                   ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream)))
+                                   ctypes.c_void_p(sc.data_ptr()), sc.numel(), sh))
 
     def debug_blind_rotate(self, in_dev, steps: int, stream=None):
         import torch

@@ -773,3 +773,39 @@ def test_shared_scratch_between_programs(server):
         torch.cuda.synchronize()
         assert np.array_equal(k.decrypt_bits(A.to_host(out)), want[op]), op
         shared.random_(0, 256)  # whatever the buffer holds next time must not matter
+
+
+@pytest.mark.gpu
+def test_concurrent_evals_on_two_streams(server):
+    """Two host threads run vlp_server_eval on the same compiled schedule on two CUDA streams at once (separate
+    scratch buffers per stream, shared cached program and key): both results decrypt to the predicate and are
+    byte-equal to a serial evaluation."""
+    import threading
+    wl = make_workload(1, key_seed=SEED)
+    k = server.keys
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    q = A.to_device(k.encrypt_query(m, wl.query, 7))
+    db = A.to_device(k.encrypt_db(m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1))
+    ref = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    server.eval(m, q, db, ref)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.zeros_like(ref) for _ in streams]
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                server.eval(m, q, db, outs[i], stream=streams[i])
+            streams[i].synchronize()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for o in outs:
+        assert np.array_equal(A.to_host(o), A.to_host(ref))
