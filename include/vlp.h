@@ -59,9 +59,12 @@ enum {
   VLP_F_OR_REDUCE = 16,   /* R19: OR instead of XOR in the aggregation */
   VLP_F_PREFIX_COMP = 32, /* R23 (NOT in the paper): log-depth parallel-prefix unsigned
                              comparators (depth 1 + ceil(log2 l) instead of l + 1; more gates; needs UNSIGNED) */
-  VLP_F_LINEAR_SUM = 64   /* R24 (NOT in the paper): linear XOR aggregation -- masked bits
+  VLP_F_LINEAR_SUM = 64,  /* R24 (NOT in the paper): linear XOR aggregation -- masked bits
                              in the {0, 1/2} encoding summed without bootstrapping in groups of 64, one refresh
                              bootstrap per group and bit (XOR only: not with OR_REDUCE) */
+  VLP_F_KEEP_ALL = 128    /* debug: every intermediate keeps its own scratch row for the whole evaluation (for
+                             pure-function parity dumps); by default rows are recycled by liveness, and only
+                             the validation bits and masked payloads (vlp_program_node_row) are kept */
 };
 #define VLP_CONFIG_FLAGS (VLP_F_CLOSED_UPPER | VLP_F_UNSIGNED | VLP_F_EQ_TREE | VLP_F_SUM_TREE)
 

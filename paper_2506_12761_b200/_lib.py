@@ -16,7 +16,7 @@ N = 1024
 VLP_OK, VLP_EINVAL, VLP_EMODE, VLP_EWIDTH, VLP_ERANGE, VLP_EPKUSED, VLP_ECUDA, VLP_ENOMEM, VLP_ENODEV = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)
 MODE_INTV, MODE_COV, MODE_IDM = 0, 1, 2
-F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP, F_LINEAR_SUM = 1, 2, 4, 8, 16, 32, 64
+F_CLOSED_UPPER, F_UNSIGNED, F_EQ_TREE, F_SUM_TREE, F_OR_REDUCE, F_PREFIX_COMP, F_LINEAR_SUM, F_KEEP_ALL = 1, 2, 4, 8, 16, 32, 64, 128
 CONFIG_FLAGS = F_CLOSED_UPPER | F_UNSIGNED | F_EQ_TREE | F_SUM_TREE
 AND, NAND, OR, XOR, XNOR, MUX = 0, 1, 2, 3, 4, 5
 

@@ -107,7 +107,12 @@ class Builder {
 
   // Assign slots (outputs listed in `outs` go to the out region, in order) and emit the levels.  Slot ids
   // hold a 28-bit row (slot()): a schedule with more intermediate rows is refused.
-  int finalize(const std::vector<uint32_t>& outs, Schedule* s) {
+  // Rows are recycled by liveness (unless keep_all): an intermediate is read by the blind rotations of the
+  // levels that consume it (a linear sum's inputs right after its level's key switch), so its row is free
+  // again from the level after its last reader on; an N-LWE row from the level after its key switch on.
+  // `pinned` nodes (the parity-dump rows v_i and the masked payloads) keep their rows.
+  int finalize(const std::vector<uint32_t>& outs, Schedule* s, const std::vector<uint32_t>& pinned = {},
+               bool keep_all = true) {
     size_t gates = 0;
     for (auto& nd : nodes) gates += nd.kind != 0;  // every non-leaf node owns an intermediate row
     if (gates + 2 > kMaxRows || outs.size() > kMaxRows)
@@ -117,19 +122,81 @@ class Builder {
       if (outs[j] & kNeg) return fail(VLP_EINVAL, "internal: a negated reference as a circuit output");
       if (nodes[outs[j]].kind != 0) out_index[outs[j]] = static_cast<uint32_t>(j);
     }
-    uint32_t mid = 2, nl = 0, maxl = 0;
-    for (size_t i = 0; i < nodes.size(); i++) {
-      Node& nd = nodes[i];
-      if (nd.kind == 0) continue;
-      nd.slot = out_index[i] != kNone ? slot(kRegOut, out_index[i]) : slot(kRegMid, mid++);
-      maxl = std::max(maxl, nd.level);
-    }
-    s->levels.assign(maxl, Level{});
-    auto sl = [&](uint32_t ref) { return nodes[node_of(ref)].slot; };
+    uint32_t maxl = 0;
+    for (auto& nd : nodes)
+      if (nd.kind != 0) maxl = std::max(maxl, nd.level);
+    // last level reading each node
+    constexpr uint32_t kForever = 0xFFFFFFFFu;
+    std::vector<uint32_t> death(nodes.size(), 0);
+    auto use = [&](uint32_t ref, uint32_t L) {
+      uint32_t& d = death[node_of(ref)];
+      d = std::max(d, L);
+    };
     for (auto& nd : nodes) {
       if (nd.kind == 1) {
+        use(nd.in[0], nd.level);
+        use(nd.in[1], nd.level);
+      } else if (nd.kind == 2) {
+        use(nd.in[0], std::max(nd.h1, nd.h2));
+        use(nd.in[1], nd.h1);
+        use(nd.in[2], nd.h2);
+      } else if (nd.kind == 3) {
+        for (uint32_t r : lin_inputs[nd.in[0]]) use(r, nd.level);
+      }
+    }
+    for (uint32_t pnode : pinned) death[node_of(pnode)] = kForever;
+    // intermediate rows (0, 1 = the trivial constants) and N-LWE rows, level by level
+    std::vector<std::vector<uint32_t>> born(maxl + 1), mid_free_at(maxl + 2), nl_free_at(maxl + 2);
+    std::vector<std::vector<std::pair<uint32_t, int>>> brs(maxl + 1);  // (node, half) per BR level
+    for (uint32_t i = 0; i < nodes.size(); i++) {
+      const Node& nd = nodes[i];
+      if (nd.kind == 0) continue;
+      if (out_index[i] == kNone) born[nd.level].push_back(i);
+      if (nd.kind == 1) brs[nd.level].push_back({i, 1});
+      if (nd.kind == 2) {
+        brs[nd.h1].push_back({i, 1});
+        brs[nd.h2].push_back({i, 2});
+      }
+    }
+    std::vector<uint32_t> row1(nodes.size(), kNone), row2(nodes.size(), kNone);
+    std::vector<uint32_t> free_mid, free_nl;
+    uint32_t mid = 2, nl = 0;
+    for (uint32_t L = 1; L <= maxl; L++) {
+      for (uint32_t r : mid_free_at[L]) free_mid.push_back(r);
+      for (uint32_t r : nl_free_at[L]) free_nl.push_back(r);
+      for (auto [i, h] : brs[L]) {
+        uint32_t r;
+        if (!keep_all && !free_nl.empty()) {
+          r = free_nl.back();
+          free_nl.pop_back();
+        } else {
+          r = nl++;
+        }
+        (h == 2 ? row2 : row1)[i] = r;
+        if (nodes[i].level + 1 <= maxl) nl_free_at[nodes[i].level + 1].push_back(r);
+      }
+      for (uint32_t i : born[L]) {
+        uint32_t r;
+        if (!keep_all && !free_mid.empty()) {
+          r = free_mid.back();
+          free_mid.pop_back();
+        } else {
+          r = mid++;
+        }
+        nodes[i].slot = slot(kRegMid, r);
+        const uint32_t d = std::max(death[i], nodes[i].level);
+        if (d != kForever && d + 1 <= maxl) mid_free_at[d + 1].push_back(r);
+      }
+    }
+    for (uint32_t i = 0; i < nodes.size(); i++)
+      if (nodes[i].kind != 0 && out_index[i] != kNone) nodes[i].slot = slot(kRegOut, out_index[i]);
+    s->levels.assign(maxl, Level{});
+    auto sl = [&](uint32_t ref) { return nodes[node_of(ref)].slot; };
+    for (uint32_t i = 0; i < nodes.size(); i++) {
+      Node& nd = nodes[i];
+      if (nd.kind == 1) {
         const LinForm f = form(nd.op);
-        const uint32_t row = nl++;
+        const uint32_t row = row1[i];
         s->levels[nd.level - 1].br.push_back(BrJob{sl(nd.in[0]), sl(nd.in[1]), f.k0,
                                                    static_cast<int8_t>(f.ax * sgn(nd.in[0])),
                                                    static_cast<int8_t>(f.ay * sgn(nd.in[1])), nd.tv, row});
@@ -138,7 +205,7 @@ class Builder {
         s->br++;
         s->ks++;
       } else if (nd.kind == 2) {
-        const uint32_t r1 = nl++, r2 = nl++;
+        const uint32_t r1 = row1[i], r2 = row2[i];
         const uint32_t c = sl(nd.in[0]), a = sl(nd.in[1]), b = sl(nd.in[2]);
         const int sc = sgn(nd.in[0]), sa = sgn(nd.in[1]), sb = sgn(nd.in[2]);
         // BR_N((0,-1/8) + c + a) and BR_N((0,-1/8) - c + b); KS((0,1/8) + u1 + u2)
@@ -369,7 +436,9 @@ int compile_velopir(const vlp_meta& m, size_t first, size_t count, Schedule* s, 
     outs.insert(outs.end(), root.begin(), root.end());
     if (qi == 0) masked0 = masked;
   }
-  if (int rc = B.finalize(outs, s)) return rc;
+  std::vector<uint32_t> pinned(vs.begin(), vs.end());  // parity-dump rows of the first query
+  for (auto& w : masked0) pinned.insert(pinned.end(), w.begin(), w.end());
+  if (int rc = B.finalize(outs, s, pinned, m.flags & VLP_F_KEEP_ALL)) return rc;
   s->in0_cts = static_cast<uint64_t>(nq) * QW * l;
   s->in1_cts = count * per;
   s->l_S = m.l_S;

@@ -228,10 +228,14 @@ def test_all_trivial_closed_form_full_size(server, cfg):
     assert [int(x) for x in out[:, 630]] == [0x20000000 if (want >> j) & 1 else 0xE0000000 for j in range(wl.l_S)]
 
 
-def _full_size_sampled(server, cfg, sample):
+def _full_size_sampled(server, cfg, sample, keep_all=True):
     """A config at full size: decrypted result == plain predicate; the sampled records' validation bits and
-    masked payloads are recomputed by the oracle (from the same seeded inputs) and byte-equal."""
+    masked payloads are recomputed by the oracle (from the same seeded inputs) and byte-equal.  keep_all:
+    every intermediate keeps its row (VLP_F_KEEP_ALL), so 4 random gates of every level are rechecked too;
+    otherwise rows are recycled by liveness (the production layout) and only the kept rows are compared."""
     wl = make_workload(cfg, key_seed=SEED)
+    if keep_all:
+        wl = make_workload(cfg, key_seed=SEED, flags=wl.flags | L.F_KEEP_ALL)
     prog, q, db, out = _run_config(server, wl)
     want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
     assert server.keys.decrypt_value(out) == want
@@ -248,9 +252,9 @@ def _full_size_sampled(server, cfg, sample):
         assert np.array_equal(mid[prog.node_row(0, i), :631], v), ("v", i)
         for j in range(wl.l_S):
             assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j]), ("mask", i, j)
-    # plus pure-function parity of 4 random gates of every level (SURVEY 4 layer 3)
-    regions = {0: q, 1: db, 2: mid, 3: out}
-    assert _gate_checks(prog, regions, okeys, per_level=4, seed=cfg) >= 4 * (prog.info.levels - 6)
+    if keep_all:  # plus pure-function parity of 4 random gates of every level (SURVEY 4 layer 3)
+        regions = {0: q, 1: db, 2: mid, 3: out}
+        assert _gate_checks(prog, regions, okeys, per_level=4, seed=cfg) >= 4 * (prog.info.levels - 6)
     return wl, want
 
 
@@ -315,8 +319,9 @@ def test_all_trivial_extreme_widths(server, case):
 
 
 def test_config2_full_size_sampled(server):
-    """Config 2 at full size (IntV 1D, 1024 records, 132,080 BR): predicate + records 3 and 1023 byte-equal."""
-    _full_size_sampled(server, 2, [3, 1023])
+    """Config 2 at full size (IntV 1D, 1024 records, 132,080 BR) in the production layout (rows recycled by
+    liveness, as bench.py runs it): predicate + records 3 and 1023 byte-equal."""
+    _full_size_sampled(server, 2, [3, 1023], keep_all=False)
 
 
 def test_config3_full_size_sampled(server):
@@ -478,7 +483,7 @@ def test_dataset_shapes_predicate(server, cfg):
     sample = [0] if cfg == 8 else []
     wl = make_workload(cfg, key_seed=SEED)
     if sample:
-        _full_size_sampled(server, cfg, sample)
+        _full_size_sampled(server, cfg, sample, keep_all=False)
         return
     prog, q, db, out = _run_config(server, wl)
     want = OC.plain_result(wl.mode, wl.query, [list(map(int, r)) for r in wl.records], wl.payloads, wl.d, wl.flags)
@@ -639,7 +644,7 @@ def test_config1_every_gate_pure_function(server, variant):
     """SURVEY 4 layer 3: every one of config 1's 188 gate outputs (every level) is byte-equal to the oracle's
     gate recomputed from the GPU's own inputs; with the R23 / R24 variants, every one of their gates and every
     linear sum."""
-    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | _VARIANT_FLAGS[variant])
+    wl = make_workload(1, key_seed=SEED, flags=OC.CONFIG_FLAGS | _VARIANT_FLAGS[variant] | L.F_KEEP_ALL)
     prog, q, db, out = _run_config(server, wl)
     okeys = O.OracleKeys(SEED)
     regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}
@@ -657,7 +662,7 @@ def test_config2_linear_aggregation(server):
     """R24 at config 2's full size (1024 records = 16 groups of 64): 115,984 BR in 21 levels instead of 132,080
     in 29; the result decrypts to the predicate; the refresh levels' gates (all of them), 8 masks and every
     linear sum are byte-equal to the oracle's recomputation from the GPU's own inputs."""
-    wl = make_workload(2, key_seed=SEED, flags=OC.CONFIG_FLAGS | OC.F_LINEAR_SUM)
+    wl = make_workload(2, key_seed=SEED, flags=OC.CONFIG_FLAGS | OC.F_LINEAR_SUM | L.F_KEEP_ALL)
     prog, q, db, out = _run_config(server, wl)
     assert (prog.info.br, prog.info.levels) == (115984, 21)
     assert server.keys.decrypt_value(out) == expected_result(wl)
@@ -671,7 +676,7 @@ def test_config2_linear_aggregation(server):
 def test_config2_sampled_gates_pure_function(server):
     """SURVEY 4 layer 3 at full size: 16 random gates of each of config 2's 29 levels (all of the narrow
     tree levels) are recomputed by the oracle from the GPU's own input ciphertexts and byte-equal."""
-    wl = make_workload(2, key_seed=SEED)
+    wl = make_workload(2, key_seed=SEED, flags=OC.CONFIG_FLAGS | L.F_KEEP_ALL)
     prog, q, db, out = _run_config(server, wl)
     okeys = O.OracleKeys(SEED)
     regions = {0: q, 1: db, 2: A.to_host(prog.intermediate()), 3: out}

@@ -143,6 +143,15 @@ def test_linear_aggregation_schedule():
     assert L.lib().vlp_program_create(None, ctypes.byref(bad), 0, 4, ctypes.byref(h)) == L.VLP_EINVAL
 
 
+@pytest.mark.parametrize("c", [(2, 65536, 20, 32, 1), (0, 4096, 16, 32, 2), (0, 1024, 16, 16, 1)])
+def test_liveness_recycles_scratch_rows(c):
+    """Intermediate and N-LWE rows are recycled by liveness (default) instead of one row per gate
+    (VLP_F_KEEP_ALL): the same schedule in well under half the scratch for configs 2-4 (config 4: 45 -> 19 GB)."""
+    a, b = _info(A.meta(*c)), _info(A.meta(*c, L.CONFIG_FLAGS | L.F_KEEP_ALL))
+    assert (a.br, a.ks, a.levels) == (b.br, b.ks, b.levels)
+    assert a.scratch_bytes < 0.55 * b.scratch_bytes
+
+
 def test_schedule_level_widths_config2():
     """SURVEY 8(d) config 2 widths: L1 32,768; L2 34,816; L3-L17 2,048; L18 1,024; L19 16,384; tree 8,192 -> 16."""
     h = ctypes.c_void_p()
