@@ -49,7 +49,7 @@ enum {
   VLP_ENODEV = -8    /* no CUDA device / kernel image for this device */
 };
 
-/* Modes and flags (readings R11, R12, R14, R15, R19). */
+/* Modes and flags (readings R11, R12, R14, R15, R19; R23 / R24 are options outside the paper). */
 enum { VLP_MODE_INTV = 0, VLP_MODE_COV = 1, VLP_MODE_IDM = 2 };
 enum {
   VLP_F_CLOSED_UPPER = 1, /* R12: lo <= x <= hi (CompLE on the right bound) instead of x < hi */
