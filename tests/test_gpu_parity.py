@@ -814,3 +814,54 @@ def test_concurrent_evals_on_two_streams(server):
     assert not errs, errs
     for o in outs:
         assert np.array_equal(A.to_host(o), A.to_host(ref))
+
+
+@pytest.mark.gpu
+def test_linear_aggregation_noise_and_three_group_levels(server):
+    """R24 noise budget and grouping, measured: an IdM database of 4,160 records (65 groups -> 2 -> 1: three
+    refresh levels) with colliding 4-bit ids, so many masks are 1.  Every linear sum's phase is within the
+    refresh margin 1/4 of its exact XOR (bit / 2), the error of the 64-term sums has the predicted spread
+    (sigma ~ 0.028 = sqrt(64) x the gate output sigma), and the result decrypts to the predicate."""
+    M, l_I, l_S = 4160, 4, 8
+    rng = np.random.default_rng(29)
+    recs = rng.integers(0, 16, (M, 1), dtype=np.uint64)
+    pays = rng.integers(0, 256, M, dtype=np.uint64)
+    qv = 5
+    flags = OC.CONFIG_FLAGS | OC.F_LINEAR_SUM | L.F_KEEP_ALL
+    k = server.keys
+    m = A.meta(OC.MODE_IDM, M, l_I, l_S, 1, flags)
+    q = k.encrypt_query(m, [qv], 7)
+    db = k.encrypt_db(m, recs, pays, pk_seed=31)
+    prog = A.Program.velopir(server, m)
+    out = torch.zeros((l_S, 632), dtype=torch.int32, device="cuda:0")
+    prog.eval(A.to_device(q), A.to_device(db), out)
+    torch.cuda.synchronize()
+    want = 0
+    for r, p in zip(recs[:, 0], pays):
+        if int(r) == qv:
+            want ^= int(p)
+    assert k.decrypt_value(A.to_host(out)) == want
+    s = k.export()[0].astype(np.uint64)
+    mid = A.to_host(prog.intermediate())
+
+    def phase(row):  # b - <a, s> mod 2^32, centered
+        ph = (int(row[630]) - int((row[:630].astype(np.uint64) * s).sum() % 2 ** 32)) % 2 ** 32
+        return ph
+
+    errs, levels_with_sums = [], 0
+    for lvl in range(prog.info.levels):
+        jobs, ins = prog.level_linear(lvl)
+        if len(jobs) == 0:
+            continue
+        levels_with_sums += 1
+        for out_slot, first, count, _ in jobs[:64]:
+            bit = 0
+            for i in range(count):  # inputs are {0, 1/2}-encoded: the bit is the phase rounded to 0 or 1/2
+                bit ^= int(round(phase(mid[int(ins[first + i]) & 0x0FFFFFFF]) / 2 ** 31)) & 1
+            e = (phase(mid[int(out_slot) & 0x0FFFFFFF]) - bit * 2 ** 31 + 2 ** 31) % 2 ** 32 - 2 ** 31
+            errs.append(e / 2 ** 32)
+    errs = np.array(errs)
+    print(f"R24 linear sums: {len(errs)} checked, |error| max {np.abs(errs).max():.4f}, std {errs.std():.4f}")
+    assert levels_with_sums == 3
+    assert np.abs(errs).max() < 0.15, np.abs(errs).max()   # margin 1/4
+    assert 0.01 < errs.std() < 0.045, errs.std()            # predicted ~0.028 for 64-term sums
