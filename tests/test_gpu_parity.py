@@ -4,6 +4,7 @@ Bit-exact everywhere (all arithmetic is integer: torus32 and the NTT primes).  S
 (5 bootstraps each in whole waves, 1-4 in the narrower tail wave of a level) with ragged tails; full-size configs are checked on sampled outputs the oracle
 recomputes one by one plus properties that hold at any size (decrypted predicate, all-trivial closed
 form P11)."""
+import ctypes
 import os
 import random
 from concurrent.futures import ThreadPoolExecutor
@@ -865,3 +866,23 @@ def test_linear_aggregation_noise_and_three_group_levels(server):
     assert levels_with_sums == 3
     assert np.abs(errs).max() < 0.15, np.abs(errs).max()   # margin 1/4
     assert 0.01 < errs.std() < 0.045, errs.std()            # predicted ~0.028 for 64-term sums
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [6, 7, 8, 9])
+def test_dataset_shapes_with_options_predicate(server, cfg):
+    """The paper-dataset shapes with both options outside the paper (R23 prefix comparators where there are
+    comparators, R24 linear aggregation; weather-usa shape: 128-bit payloads, 304 records = 5 groups):
+    the decrypted answer equals the plain predicate, with fewer levels than the paper's circuit."""
+    wl0 = make_workload(cfg, key_seed=SEED)
+    wl = make_workload(cfg, key_seed=SEED, flags=wl0.flags | OC.F_LINEAR_SUM |
+                       (OC.F_PREFIX_COMP if wl0.mode == OC.MODE_INTV else 0))
+    prog, q, db, out = _run_config(server, wl)
+    assert server.keys.decrypt_value(out) == expected_result(wl)
+    m0 = A.meta(wl0.mode, wl0.M, wl0.l_I, wl0.l_S, wl0.d, wl0.flags)
+    h = ctypes.c_void_p()
+    L.check(L.lib().vlp_program_create(None, ctypes.byref(m0), 0, wl0.M, ctypes.byref(h)))
+    info = L.VlpProgramInfo()
+    L.check(L.lib().vlp_program_get_info(h, ctypes.byref(info)))
+    L.lib().vlp_free_program(h)
+    assert prog.info.levels < info.levels
