@@ -109,7 +109,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def cpu_baseline_oracle(seconds_target=5.0, nand_gates=None):
+def cpu_baseline_oracle(seconds_target=5.0, nand_gates=None, extended=False):
     """The oracle as it stands, on this host's cores (threads over independent gates), on a bounded
     sample: NAND gates on fresh encryptions (one BR + one KS each)."""
     import oracle as O
@@ -127,9 +127,34 @@ def cpu_baseline_oracle(seconds_target=5.0, nand_gates=None):
         t0 = time.time()
         list(pool.map(lambda i: k.gate(O.NAND, xs[i], ys[i]), range(count)))
         dt = time.time() - t0
-    return {"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    line = {"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{count} NAND gate bootstraps (BR+extract+KS) on fresh encryptions, {cores} threads, "
                       f"{dt:.1f} s wall"}
+    if extended:  # the oracle's key switches per second and config 1 in full
+        from oracle import circuits as OC
+        from oracle import protocol as OP
+        rows = [k.bootstrap_nlwe(xs[i]) for i in range(min(cores, count))]
+        ks_n = 4 * cores
+        with ThreadPoolExecutor(max_workers=cores) as pool:
+            t0 = time.time()
+            list(pool.map(lambda i: k.keyswitch(rows[i % len(rows)]), range(ks_n)))
+            line["ks_per_s"] = ks_n / (time.time() - t0)
+        wl = make_workload(1)
+        k1 = O.OracleKeys(wl.key_seed)
+        q = OP.encrypt_query(k1, wl.query, wl.l_I, 7)
+        recs, pays = [], []
+        for i in range(wl.M):
+            r, pl = OP.server_enc_record(k1, wl.key_seed + 1, i, [int(v) for v in wl.records[i]],
+                                         int(wl.payloads[i]), wl.l_I, wl.l_S)
+            recs.append(r)
+            pays.append(pl)
+        t0 = time.time()
+        R, _, _ = OC.velopir(OC.TfheBackend(k1), wl.mode, q, recs, pays, wl.l_I, wl.d, wl.l_S, wl.flags, threads=cores)
+        line["config1_query_s"] = time.time() - t0
+        assert OP.decrypt_bits(k1, R) == expected_result(wl), "oracle config 1 result"
+        line["sample"] += (f"; {ks_n} key switches ({line['ks_per_s']:.0f}/s); config 1 in full (252 BR, "
+                           f"records in parallel) {line['config1_query_s']:.1f} s")
+    return line
 
 
 def run_reference(args, rank, world):
@@ -409,7 +434,7 @@ def main():
         # achieved over the dominant kernel: algorithmic integer ops of all BRs / total BR kernel time
         br_in_shard = prog.info.br
         achieved = ops_per_br() * br_in_shard * args.steps / (br_ms / 1e3) / 1e9 if br_ms > 0 else None
-        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline_oracle()
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline_oracle(extended=True)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
