@@ -12,6 +12,8 @@
 //  K3 vlp_ks_indicator_kernel + cuBLASLt int8 GEMM + vlp_ks_combine_kernel : MUX combine (S7) + key
 //                               switch (S8) as a one-hot-indicator x byte-limb-ksk GEMM on the tensor cores
 //  K4 vlp_bsk_convert_kernel  : bsk -> 3-limb NTT domain (setup)
+//  K5 vlp_linear_kernel       : R24 linear aggregation (exact ciphertext sums; option outside the paper)
+//  vlp_encrypt_db_kernel      : device PubKeyGen + ServerEnc (setup)
 //
 // Exact arithmetic: NTT prime p = 0x3fff7801 (p = 1 mod 2048, 4p < 2^32); the
 // bootstrapping key is split into three signed limbs (11, 11, 10 bits) so every limb product sum is
