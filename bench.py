@@ -451,7 +451,11 @@ def main():
                          "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
                          "br_share_of_step": br_ms / args.steps / ms_per_step,
                          "br_launch_avg_ms": br_launch_ms, "traffic": TRAFFIC_BYTES_PER_LAUNCH,
-                         "traffic_source": TRAFFIC_SOURCE},
+                         "traffic_source": TRAFFIC_SOURCE,
+                         # the unit that binds this kernel on sm_100a (IMAD.HI / IMAD.WIDE issue at half rate),
+                         # from the same ncu capture as `traffic`
+                         "binding_unit": {"pipe": "fmaheavy", "active": 0.707,
+                                          "source": "sm__pipe_fmaheavy_cycles_active, profiles/r1_br_v11_ncu_summary.txt"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
