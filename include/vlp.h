@@ -232,6 +232,14 @@ int vlp_debug_blind_rotate(vlp_server* server, const uint32_t* in_dev, size_t co
                            uint32_t* acc_dev, void* scratch_dev, uint64_t stream);
 int vlp_debug_keyswitch(vlp_server* server, const uint32_t* nlwe_dev, size_t count, uint32_t* out_dev,
                         void* scratch_dev, uint64_t stream);
+/* Blind-rotation routing for every later launch in this process (debug / parity tests).
+ * Both engines are exact, so the bytes never depend on the route -- the parity tests use this to run every
+ * kernel against the oracle.  engine: 0 = default (VLP_BR_ENGINE / VLP_BR_BOOT / VLP_FFT_WARPS from the
+ * environment, else the FP64-FFT engine K2F for waves with the NTT latency kernels for narrow tails);
+ * 1 = NTT engine only (K2 waves + NTT tails; param != 0 forces one NTT kernel for whole levels, with the
+ * VLP_BR_BOOT meaning: 1-5 bootstraps per CTA, -1 latency, -2 2-CTA cluster, -3 6-CTA cluster);
+ * 2 = K2F with param warps (1-8) per CTA for whole levels.  Returns VLP_EINVAL on other values. */
+int vlp_debug_route(int engine, int param);
 
 /* ---- The problem-statement calls (the north star's keygen / encrypt_query / server_eval /
  * decrypt_result).  They wrap the program calls above: the schedule for a (meta, first, count) shard, a

@@ -14,9 +14,9 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libvlp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["kernels.cu", "api.cu"]
+CU = ["kernels.cu", "kernels_fft.cu", "api.cu"]
 CXX = ["host.cpp", "sched.cpp"]
-HDR = ["vlp_internal.h", "kernels.cuh", os.path.join("..", "..", "include", "vlp.h")]
+HDR = ["vlp_internal.h", "kernels.cuh", "devcommon.cuh", os.path.join("..", "..", "include", "vlp.h")]
 
 
 def _newer(src_list, target):

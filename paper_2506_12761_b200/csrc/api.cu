@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -24,6 +25,8 @@ struct vlp_server {
   uint2* twl_fwd = nullptr;  // thread-layout tables of the blind-rotate kernel
   uint2* twl_inv = nullptr;
   int8_t* kmat = nullptr;  // ksk as 4 signed byte limbs, [2528][24576] (tensor-core key switch)
+  double2* bsk_fft = nullptr;  // FFT-domain bsk of the K2F engine (2 x 16-bit limbs, scaled 1/512)
+  double2* psi = nullptr;      // psi^e, e < 2048
   cublasLtHandle_t lt = nullptr;
   std::mutex algo_mu;
   std::map<uint32_t, cublasLtMatmulAlgo_t> algos;  // cuBLASLt algorithm per GEMM row count
@@ -85,7 +88,8 @@ constexpr size_t kKskBytes = static_cast<size_t>(N) * kKsT * 3 * kCt * 4;
 constexpr size_t kTwBytes = static_cast<size_t>(N) * sizeof(uint2);
 constexpr size_t kTwlBytes = static_cast<size_t>(kTwSlots) * kBT * sizeof(uint2);
 constexpr size_t kRawBskBytes = static_cast<size_t>(n) * kRows * 2 * N * 4;
-constexpr size_t kEvkBytes = kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes + kKmatBytes;
+constexpr size_t kEvkBytes =
+    kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes + kKmatBytes + kBskFftBytes + kPsiBytes;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -333,6 +337,8 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   srv->twl_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes + kTwlBytes);
   uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes);
   srv->kmat = reinterpret_cast<int8_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes);
+  srv->bsk_fft = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->kmat) + kKmatBytes);
+  srv->psi = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->bsk_fft) + kBskFftBytes);
   if (cublasLtCreate(&srv->lt) != CUBLAS_STATUS_SUCCESS) return fail(VLP_ECUDA, "cublasLtCreate failed");
 
   std::vector<uint2> fwd, inv, lf, li;
@@ -350,6 +356,12 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   // Montgomery factor with N^-1 folded in: c = N^-1 * 2^32 mod p
   const uint32_t c_mont = static_cast<uint32_t>(mulmod(powmod(N, kP - 2), (1ull << 32) % kP));
   launch_bsk_convert(raw, srv->bsk_ntt, srv->tw_fwd, c_mont, st);
+  // K2F: psi^e = exp(i pi e / 1024) in double (host libm), the FFT-domain key by a direct DFT on the device
+  std::vector<double2> psi(2048);
+  for (int k = 0; k < 2048; k++) psi[k] = make_double2(cos(M_PI * k / 1024.0), sin(M_PI * k / 1024.0));
+  set_fft_constants(psi.data());
+  if ((e = cudaMemcpyAsync(srv->psi, psi.data(), kPsiBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "psi");
+  launch_bsk_fft(raw, srv->bsk_fft, srv->psi, st);
   launch_ksk_to_i8(srv->ksk, srv->kmat, st);
   if ((e = cudaGetLastError())) return cuda_fail(e, "bsk convert launch");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server create");
@@ -538,6 +550,8 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
     ba.bsk = s->bsk_ntt;
     ba.twl_fwd = s->twl_fwd;
     ba.twl_inv = s->twl_inv;
+    ba.bskf = s->bsk_fft;
+    ba.psi = s->psi;
     if (ba.njobs) {
       p->begin(0, st);
       if ((e = launch_blind_rotate(ba, s->sm_count, st))) return cuda_fail(e, "blind rotate");
@@ -596,6 +610,10 @@ int vlp_program_profile_read(vlp_program* p, double* br_ms, double* ks_ms, uint6
   return VLP_OK;
 }
 
+int vlp_debug_route(int engine, int param) {
+  return set_br_route(engine, param) == 0 ? VLP_OK : fail(VLP_EINVAL, "vlp_debug_route: bad engine / param");
+}
+
 size_t vlp_debug_scratch_bytes(size_t count) {
   const uint32_t chunk = static_cast<uint32_t>(std::min<size_t>(std::max<size_t>(count, 1), kKsChunk));
   return std::max(align256(count * sizeof(BrJob)), align256(count * sizeof(KsJob)) + ks_stage_bytes(chunk));
@@ -622,6 +640,8 @@ int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, 
   ba.bsk = s->bsk_ntt;
   ba.twl_fwd = s->twl_fwd;
   ba.twl_inv = s->twl_inv;
+  ba.bskf = s->bsk_fft;
+  ba.psi = s->psi;
   if ((e = launch_blind_rotate(ba, s->sm_count, st))) return cuda_fail(e, "blind rotate");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "debug sync");
   return VLP_OK;

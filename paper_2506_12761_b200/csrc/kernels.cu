@@ -31,10 +31,12 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "devcommon.cuh"
 
 namespace vlp {
 namespace cg = cooperative_groups;
 namespace {
+using namespace dev;
 
 constexpr uint32_t P = kP;
 constexpr uint32_t P2 = 2u * kP;
@@ -83,71 +85,10 @@ __device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t w, ui
   y = shoup(d, w, ws);
 }
 
-// ------------------------------------------------------------------------------ TMA bulk + mbarrier
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      " @!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// ------------------------------------------------------------------------------ TMEM as spill space
-// tcgen05.ld / tcgen05.st move registers to and from this warp's 32 TMEM lanes (32x32b shape: lane = thread,
-// one 32-bit column per register).  No MMA is issued; TMEM only extends the register file.
-__device__ __forceinline__ void tmem_st2(uint32_t ta, uint32_t a, uint32_t b) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta), "r"(a), "r"(b) : "memory");
-}
-__device__ __forceinline__ void tmem_st8(uint32_t ta, const uint32_t (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta),
-               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld8(uint32_t ta, uint32_t (&v)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-               : "r"(ta)
-               : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
 // Per-bootstrap named barrier (ids 1..B; 128 threads): the bootstraps of a CTA only meet at the bsk ring.
 __device__ __forceinline__ void bar_boot(uint32_t g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kBT) : "memory");
 }
-
-__device__ __forceinline__ uint32_t* slot_wptr(const Regions& reg, uint32_t id) {
-  const uint32_t r = id >> 28;  // select without dynamic indexing (keeps the params out of local memory)
-  uint32_t* b = r == 0 ? reg.base[0] : (r == 1 ? reg.base[1] : (r == 2 ? reg.base[2] : reg.base[3]));
-  return b + static_cast<size_t>(id & 0x0FFFFFFFu) * kCt;
-}
-__device__ __forceinline__ const uint32_t* slot_ptr(const Regions& reg, uint32_t id) { return slot_wptr(reg, id); }
 
 // ------------------------------------------------------------------------------ layouts / swizzle
 // One bootstrap = 128 threads x 8 registers per polynomial (t in [0,128), r in [0,8)):
@@ -1562,41 +1503,94 @@ static cudaError_t launch_br_width(const BrArgs& a, int B, int sm_count, cudaStr
   }
 }
 
-// One level of blind rotations: whole waves of kBrBoot bootstraps per SM, then the remainder (fewer than
-// kBrBoot x sm_count jobs) as one wave of the smallest CTA size that holds it -- a CTA runs all its
-// bootstrap slots, so a narrow tail on 5-slot CTAs would cost a full-width wave.  VLP_BR_BOOT=b (debug)
-// forces b bootstraps per CTA for the whole level.
-static int forced_boot() {
-  static const int f = [] {
-    const char* e = getenv("VLP_BR_BOOT");
-    return e ? atoi(e) : 0;
-  }();
-  return f;
+// One level of blind rotations.  Engine (VLP_BR_ENGINE, read once): "fft" (default) -- whole waves of
+// kFftMaxWarps bootstraps per SM on K2F (kernels_fft.cu), a remainder wider than one bootstrap per SM on a K2F
+// wave of ceil(rest / SMs) warps per CTA; "ntt" -- whole waves of kBrBoot bootstraps per SM on K2 and a narrower
+// K2 tail.  With either engine a remainder of at most one bootstrap per SM runs on the NTT latency kernels
+// (6-CTA cluster / 2-CTA cluster / warp groups per bootstrap).  Both engines are exact: the bytes do not
+// depend on the choice.  VLP_BR_BOOT=b (debug) forces one NTT kernel for the whole level (1-5: K2 with b
+// bootstraps per CTA, -1 latency, -2 2-CTA cluster, -3 6-CTA cluster); VLP_FFT_WARPS=w forces K2F with w warps.
+// Routing state: initialised once from the environment, replaced by vlp_debug_route (set_br_route).
+struct Route {
+  int engine;     // 0 ntt, 1 fft
+  int boot;       // forced NTT kernel (VLP_BR_BOOT meaning) or 0
+  int fft_warps;  // forced K2F warps per CTA or 0
+};
+static Route env_route() {
+  Route r{1, 0, 0};
+  if (const char* e = getenv("VLP_BR_ENGINE")) r.engine = e[0] == 'n' ? 0 : 1;
+  if (const char* e = getenv("VLP_BR_BOOT")) r.boot = atoi(e);
+  if (const char* e = getenv("VLP_FFT_WARPS")) {
+    const int v = atoi(e);
+    r.fft_warps = v >= 1 && v <= kFftMaxWarps ? v : 0;
+  }
+  return r;
+}
+static std::atomic<int> g_engine{-1}, g_boot{0}, g_fft_warps{0};
+static Route route() {
+  if (g_engine.load() < 0) {
+    const Route r = env_route();
+    g_boot.store(r.boot);
+    g_fft_warps.store(r.fft_warps);
+    int expect = -1;
+    g_engine.compare_exchange_strong(expect, r.engine);
+  }
+  return Route{g_engine.load(), g_boot.load(), g_fft_warps.load()};
+}
+int set_br_route(int engine, int param) {
+  if (engine == 0) {
+    const Route r = env_route();
+    g_boot.store(r.boot);
+    g_fft_warps.store(r.fft_warps);
+    g_engine.store(r.engine);
+  } else if (engine == 1) {
+    if (!((param >= 0 && param <= kBrBoot) || param == -1 || param == -2 || param == -3)) return -1;
+    g_boot.store(param);
+    g_fft_warps.store(0);
+    g_engine.store(0);
+  } else if (engine == 2) {
+    if (param < 1 || param > kFftMaxWarps) return -1;
+    g_boot.store(0);
+    g_fft_warps.store(param);
+    g_engine.store(1);
+  } else {
+    return -1;
+  }
+  return 0;
+}
+static int forced_boot() { return route().boot; }
+static int forced_fft_warps() { return route().fft_warps; }
+static bool fft_engine() { return route().engine == 1; }
+static bool forced_any() {
+  const int f = forced_boot();
+  return (f >= 1 && f <= kBrBoot) || f == -1 || f == -2 || f == -3 || forced_fft_warps() > 0;
 }
 
 int br_launch_count(uint32_t njobs, int sm_count) {
   if (njobs == 0) return 0;
-  if ((forced_boot() >= 1 && forced_boot() <= kBrBoot) || forced_boot() == -1 || forced_boot() == -2 ||
-      forced_boot() == -3)
-    return 1;
-  const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
+  if (forced_any()) return 1;
+  const uint32_t wave = static_cast<uint32_t>(fft_engine() ? kFftMaxWarps : kBrBoot) * static_cast<uint32_t>(sm_count);
   return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
 }
 
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) {
   if (a.njobs == 0) return cudaSuccess;
   const int forced = forced_boot();
+  if (forced_fft_warps()) return launch_blind_rotate_fft(a, forced_fft_warps(), sm_count, st);
   if (forced >= 1 && forced <= kBrBoot) return launch_br_width(a, forced, sm_count, st);
   if (forced == -1) return launch_br_width(a, 0, sm_count, st);   // VLP_BR_BOOT=-1: latency mode
   if (forced == -2) return launch_br_width(a, -1, sm_count, st);  // VLP_BR_BOOT=-2: cluster latency mode
   if (forced == -3) return launch_br_width(a, -2, sm_count, st);  // VLP_BR_BOOT=-3: 6-CTA cluster mode
-  const uint32_t wave = static_cast<uint32_t>(kBrBoot) * static_cast<uint32_t>(sm_count);
+  const bool fft = fft_engine();
+  const uint32_t per_sm = static_cast<uint32_t>(fft ? kFftMaxWarps : kBrBoot);
+  const uint32_t wave = per_sm * static_cast<uint32_t>(sm_count);
   const uint32_t full = a.njobs / wave * wave, tail = a.njobs - full;
   cudaError_t e = cudaSuccess;
   if (full) {
     BrArgs f = a;
     f.njobs = full;
-    if ((e = launch_br_width(f, kBrBoot, sm_count, st)) != cudaSuccess) return e;
+    e = fft ? launch_blind_rotate_fft(f, kFftMaxWarps, sm_count, st) : launch_br_width(f, kBrBoot, sm_count, st);
+    if (e != cudaSuccess) return e;
   }
   if (tail) {
     BrArgs r = a;
@@ -1605,10 +1599,12 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
     if (r.raw_acc) r.raw_acc = a.raw_acc + static_cast<size_t>(full) * 2 * N;
     // a tail of at most one bootstrap per SM runs in latency mode (warp groups per bootstrap); at most one per
     // two SMs, on a 2-CTA cluster per bootstrap; at most one per resident 6-CTA cluster, on a 6-CTA cluster
+    const uint32_t per = (tail + sm_count - 1) / sm_count;
+    if (fft && tail > static_cast<uint32_t>(sm_count)) return launch_blind_rotate_fft(r, static_cast<int>(per), sm_count, st);
     const int b = tail <= c6_max_clusters() ? -2
                   : tail <= static_cast<uint32_t>(sm_count / 2) ? -1
                   : tail <= static_cast<uint32_t>(sm_count) ? 0
-                                                             : static_cast<int>((tail + sm_count - 1) / sm_count);
+                                                             : static_cast<int>(per);
     e = launch_br_width(r, b, sm_count, st);
   }
   return e;

@@ -58,6 +58,8 @@ struct BrArgs {
   const uint32_t* bsk;  // NTT-domain bsk, layout [i][chunk][t][kChunkWords]
   const uint2* twl_fwd;  // [kTwSlots][kBT] (w, floor(w 2^32 / p)) in thread order
   const uint2* twl_inv;
+  const double2* bskf;  // FFT-domain bsk (K2F engine), layout [i][chunk 12][rho' 8][o*2 + l][lane 32] complex
+  const double2* psi;   // psi^e = exp(i pi e / 1024), e < 2048 (K2F per-lane twiddles)
   uint32_t zero;  // always 0 (a runtime zero; see add_alu in kernels.cu)
   uint32_t p2;    // always 2p, set by launch_blind_rotate (a runtime constant; see ct_bfly in kernels.cu)
 };
@@ -70,11 +72,24 @@ struct KsArgs {
   const uint32_t* ksk;   // [N][8][3][kCt] (torus32 key-switching key; the GEMM uses its byte limbs)
 };
 
+// ---- K2F: the blind rotation on an exact FP64 negacyclic FFT (kernels_fft.cu).
+// One warp = one bootstrap (32 lanes x 16 complex points of the folded 512-point transform), up to 8 per CTA;
+// the FFT-domain key holds 2 signed 16-bit limbs per coefficient, scaled by 1/512.
+constexpr int kFftMaxWarps = 8;
+constexpr int kFftChunks = 12;                         // ring chunks per CMux step: 6 digit rows x 2 halves
+constexpr int kFftChunkBytes = 8 * 4 * 32 * 16;        // 16384: [rho' 8][o*2 + l 4][lane 32] complex double
+constexpr size_t kBskFftBytes = static_cast<size_t>(n) * kFftChunks * kFftChunkBytes;  // 123,863,040
+constexpr size_t kPsiBytes = 2048 * sizeof(double2);
+void launch_bsk_fft(const uint32_t* raw, double2* out, const double2* psi, cudaStream_t st);
+void set_fft_constants(const double2* psi_host);
+cudaError_t launch_blind_rotate_fft(const BrArgs& a, int warps, int sm_count, cudaStream_t st);
+
 void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd, uint32_t c_mont,
                         cudaStream_t st);
 void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
 // one level: whole waves of kBrBoot bootstraps per CTA + a narrower tail wave (1 or 2 kernel launches)
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st);
+int set_br_route(int engine, int param);  // vlp_debug_route
 int br_launch_count(uint32_t njobs, int sm_count);
 cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
                               uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st);

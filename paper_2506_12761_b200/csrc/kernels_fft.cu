@@ -1,0 +1,492 @@
+// kernels_fft.cu -- K2F: the blind rotation (S2-S6 of SURVEY 8(a)) on an exact FP64 negacyclic FFT.
+//
+// Same job, same bytes as K2 (kernels.cu): gate linear form (S2) + mod-switch (S3) + accumulator init (S4) +
+// 630 CMux steps (S5) with the accumulator on chip + SampleExtract (S6).  Only the engine of the external
+// product differs ("K2F"):
+//
+//  * negacyclic product mod X^1024 + 1 through the folded 512-point complex FFT: z_j = (x_j + i x_{j+512}) psi^j,
+//    psi = exp(i pi / 1024), A_k = sum_j z_j w^{jk}, w = exp(2 pi i / 512), so A_k = x(psi^{4k+1});
+//  * the bootstrapping key split into two signed 16-bit limbs b = lo + 2^16 hi (R_lo, R_hi each bounded by
+//    6 * 1024 * 64 * 2^15 = 2^33.6); the FFT-domain key (scaled by 1/512) is computed at setup by a direct DFT
+//    (K4F below).  The rounding error of every limb result is far below 1/2 (bound and measured
+//    margin, tools/emulate_br_fft.py), so round(R_lo) + 2^16 round(R_hi) mod 2^32 is the exact torus32 external
+//    product -- bit-identical to the NTT engine and to the oracle.
+//  * one warp = one bootstrap: lane b holds 16 complex points; the 512-point FFT is four-step 16 x 32: a 16-point
+//    DFT in registers, per-lane twiddles psi^{b(1 + 4 k1)}, a transpose through warp-private shared memory, one
+//    radix-2 stage across the lane pair (L, L ^ 16) by shuffles, a second 16-point DFT in registers.  After the
+//    forward transform lane L / register rho holds point k = L + 32 mrev(rho).  No CTA-wide barrier on the step
+//    path: the warps of a CTA meet only at the shared key ring (TMA bulk copies, mbarriers).
+//  * per digit row, the MAC acc[o][l] += X_r * B_r[o][l] runs right after the row's FFT with the four complex
+//    accumulators per point parked in TMEM (tcgen05.ld / st, 256 columns per warp; no MMA).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "devcommon.cuh"
+#include "kernels.cuh"
+
+namespace vlp {
+namespace {
+using namespace dev;
+
+struct cd {
+  double x, y;
+};
+__device__ __forceinline__ cd cadd(cd a, cd b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cd cmul(cd a, cd b) { return {fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x)}; }
+__device__ __forceinline__ cd cmulc(cd a, cd b) { return {fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -(a.x * b.y))}; }  // a conj(b)
+
+__constant__ cd c_twist[16];  // psi^(32 a): the uniform part of the fold twist
+__constant__ cd c_w16[16];    // w16^k = psi^(128 k)
+__constant__ cd c_w32[8];     // w32^r = psi^(64 r)
+
+constexpr int kFSlots = 5;                         // key ring depth (chunks of 16 KB)
+constexpr int kTrStride = 33;                      // complex per transpose row (one pad: conflict-free LDS.128)
+constexpr int kTrBytes = 16 * kTrStride * 16;      // 8448
+constexpr int kFWarpBytes = 2 * N * 4 + kTrBytes + 640 * 2;  // accumulator + transpose buffer + abar: 17,920
+__host__ __device__ constexpr int fft_smem_bytes(int W) {
+  return kFSlots * kFftChunkBytes + W * kFWarpBytes + kFSlots * 8 + kFSlots * 4 + 16;
+}
+static_assert(fft_smem_bytes(kFftMaxWarps) <= 232448, "shared memory per CTA");
+constexpr int kFSmemMin = 120 * 1024;  // every K2F CTA asks for >= this: one CTA per SM (TMEM is allocated whole)
+
+__host__ __device__ constexpr int mrev(int r) { return (r >> 2) | ((r & 3) << 2); }
+
+// 4-point DFT in place, (a, b, c, d) <- (X0, X1, X2, X3), omega_4 = +i (forward) or -i (inverse)
+template <bool INV>
+__device__ __forceinline__ void bfly4(cd& a, cd& b, cd& c, cd& d) {
+  const cd s02 = cadd(a, c), d02 = csub(a, c), s13 = cadd(b, d), d13 = csub(b, d);
+  a = cadd(s02, s13);
+  c = csub(s02, s13);
+  if (!INV) {
+    b = {d02.x - d13.y, d02.y + d13.x};
+    d = {d02.x + d13.y, d02.y - d13.x};
+  } else {
+    b = {d02.x + d13.y, d02.y - d13.x};
+    d = {d02.x - d13.y, d02.y + d13.x};
+  }
+}
+// multiply by w16^e (e compile-time; e = 0 identity, e = 4 is +i)
+template <bool INV>
+__device__ __forceinline__ cd tw16(cd v, int e) {
+  if (e == 0) return v;
+  if (e == 4) return INV ? cd{v.y, -v.x} : cd{-v.y, v.x};
+  return INV ? cmulc(v, c_w16[e]) : cmul(v, c_w16[e]);
+}
+// 16-point DFT, radix 4 x 4.  Forward: natural in -> register rho holds X[mrev(rho)].  Inverse: the exact
+// mirror (register rho holds X[mrev(rho)] -> 16 x natural).
+__device__ __forceinline__ void dft16_fwd(cd (&v)[16]) {
+#pragma unroll
+  for (int a0 = 0; a0 < 4; a0++) {
+    bfly4<false>(v[a0], v[a0 + 4], v[a0 + 8], v[a0 + 12]);
+#pragma unroll
+    for (int k0 = 1; k0 < 4; k0++) v[a0 + 4 * k0] = tw16<false>(v[a0 + 4 * k0], a0 * k0);
+  }
+#pragma unroll
+  for (int k0 = 0; k0 < 4; k0++) bfly4<false>(v[4 * k0], v[4 * k0 + 1], v[4 * k0 + 2], v[4 * k0 + 3]);
+}
+__device__ __forceinline__ void dft16_inv(cd (&v)[16]) {
+#pragma unroll
+  for (int k0 = 0; k0 < 4; k0++) {
+    bfly4<true>(v[4 * k0], v[4 * k0 + 1], v[4 * k0 + 2], v[4 * k0 + 3]);
+#pragma unroll
+    for (int a0 = 1; a0 < 4; a0++) v[4 * k0 + a0] = tw16<true>(v[4 * k0 + a0], a0 * k0);
+  }
+#pragma unroll
+  for (int a0 = 0; a0 < 4; a0++) bfly4<true>(v[a0], v[a0 + 4], v[a0 + 8], v[a0 + 12]);
+}
+
+__device__ __forceinline__ cd shfl16(cd v) {
+  return {__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16)};
+}
+__device__ __forceinline__ cd sel(bool p, cd a, cd b) { return p ? a : b; }
+
+// Gadget digit field f = (w >> s) & 127 (R5: w = D + 0x81020400) as the double f - 64 (exact: 2^52 + f - (2^52 + 64))
+__device__ __forceinline__ double digit_d(uint32_t w, uint32_t s) {
+  return __hiloint2double(0x43300000, static_cast<int>((w >> s) & 127u)) - 4503599627370560.0;
+}
+// round(v) mod 2^32 for |v| < 2^51 (1.5 * 2^52 shifts the integer part into the low mantissa word)
+__device__ __forceinline__ uint32_t round_u32(double v) {
+  return static_cast<uint32_t>(__double2loint(v + 6755399441055744.0));
+}
+
+// Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
+// 32 q + lane, q < 32) -> X[rho] = point lane + 32 mrev(rho).
+// Per-lane twiddle of register rho: psi^{lane (1 + 4 mrev(rho))}; registers rho and rho + 8 differ by the factor
+// psi^{8 lane} (mrev(rho + 8) = mrev(rho) + 2), so only rho < 8 and that factor are kept (tw[8]).
+__device__ __forceinline__ cd twid(const cd (&tw)[9], int r) { return r < 8 ? tw[r] : cmul(tw[r - 8], tw[8]); }
+
+__device__ __forceinline__ void fft_fwd(cd (&v)[16], const uint32_t (&wv)[32], uint32_t s, const cd (&tw)[9],
+                                        cd* tr, uint32_t lane) {
+#pragma unroll
+  for (int a = 0; a < 16; a++) {
+    const cd x{digit_d(wv[a], s), digit_d(wv[16 + a], s)};
+    v[a] = a == 0 ? x : cmul(x, c_twist[a]);
+  }
+  dft16_fwd(v);
+  __syncwarp();  // the previous reader of tr is done
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const cd t = cmul(v[r], twid(tw, r));
+    reinterpret_cast<double2*>(tr)[mrev(r) * kTrStride + lane] = make_double2(t.x, t.y);
+  }
+  __syncwarp();
+  const uint32_t e = lane >> 4, k1 = lane & 15;
+  const bool hi = e != 0;
+  const double2* row = reinterpret_cast<const double2*>(tr) + k1 * kTrStride + 8 * e;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const double2 yi = row[r], yj = row[16 + r];
+    const cd sm{yi.x + yj.x, yi.y + yj.y};
+    cd df{yi.x - yj.x, yi.y - yj.y};
+    if (r) df = cmul(df, c_w32[r]);
+    df = sel(hi, cd{-df.y, df.x}, df);  // w32^(8 e + r) = i^e w32^r
+    // lane e = 0 keeps its sums and gets the partner's sums (i >= 8); e = 1 keeps its differences and gets
+    // the partner's differences (i < 8)
+    const cd recv = shfl16(sel(hi, sm, df));
+    v[r] = sel(hi, recv, sm);
+    v[8 + r] = sel(hi, df, recv);
+  }
+  dft16_fwd(v);
+}
+
+// Inverse transform: v[rho] at point lane + 32 mrev(rho) -> v[a] = 512 * (c_{32a+lane} + i c_{32a+lane+512})
+__device__ __forceinline__ void fft_inv(cd (&v)[16], const cd (&tw)[9], cd* tr, uint32_t lane) {
+  dft16_inv(v);  // 16 V_e[i]
+  const uint32_t e = lane >> 4, k1 = lane & 15;
+  const bool hi = e != 0;
+  __syncwarp();
+  double2* row = reinterpret_cast<double2*>(tr) + k1 * kTrStride + 8 * e;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const cd recv = shfl16(sel(hi, v[r], v[8 + r]));
+    const cd sm = sel(hi, recv, v[r]);
+    cd df = sel(hi, v[8 + r], recv);
+    df = sel(hi, cd{df.y, -df.x}, df);  // conj(i^e)
+    if (r) df = cmulc(df, c_w32[r]);
+    row[r] = make_double2(sm.x + df.x, sm.y + df.y);
+    row[16 + r] = make_double2(sm.x - df.x, sm.y - df.y);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const double2 t = reinterpret_cast<const double2*>(tr)[mrev(r) * kTrStride + lane];
+    v[r] = cmulc(cd{t.x, t.y}, twid(tw, r));
+  }
+  dft16_inv(v);
+#pragma unroll
+  for (int a = 1; a < 16; a++) v[a] = cmulc(v[a], c_twist[a]);
+}
+
+// TMEM (32x32b: lane = thread): one double <-> 2 consecutive columns (lo, hi word).  x2 ops take the double's own
+// aligned register pair, so no register moves are needed to gather operands (an x16 op needs 16 consecutive
+// registers and cost ~2 moves per word).  Loads are asynchronous until tcgen05.wait::ld.
+__device__ __forceinline__ void tm_st_d(uint32_t ta, double v) {
+  asm volatile("{ .reg .b32 lo, hi; mov.b64 {lo, hi}, %1; tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {lo, hi}; }" ::"r"(ta),
+               "d"(v)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld_d(uint32_t ta, double& v) {
+  asm volatile("{ .reg .b32 lo, hi; tcgen05.ld.sync.aligned.32x32b.x2.b32 {lo, hi}, [%1]; mov.b64 %0, {lo, hi}; }"
+               : "=d"(v)
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+}  // namespace
+
+// ================================================================================ K2F blind rotation
+// W warps per CTA, one bootstrap per warp; persistent over groups of W jobs.  Per CMux step and warp:
+//   for u in {0 (mask), 1 (body)}: D = X^abar acc_u - acc_u (offset 0x81020400, R5); for each gadget digit j:
+//     forward FFT of digit j, then acc4[o][l] (+)= X * B[3u + j][o][l] over this lane's 16 points (TMEM);
+//   for o in {0, 1}: inverse FFT of acc4[o][0], acc4[o][1] -> round -> acc_o += R_lo + 2^16 R_hi (mod 2^32).
+// The key of a step is 12 chunks of 16 KB (digit row r, register half h: [rho' 8][o*2 + l][lane 32]) streamed by
+// TMA into a ring shared by the CTA's warps; the last warp to release a chunk refills its slot.
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const BrArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  double2* ring = reinterpret_cast<double2*>(smem);
+  uint8_t* wb = smem + kFSlots * kFftChunkBytes;
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(wb + w * kFWarpBytes);
+  cd* tr = reinterpret_cast<cd*>(wb + w * kFWarpBytes + 2 * N * 4);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(wb + w * kFWarpBytes + 2 * N * 4 + kTrBytes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wb + W * kFWarpBytes);
+  uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kFSlots);
+  uint32_t* tmem_base_sh = rel + kFSlots;
+  constexpr int kCols = W <= 4 ? 256 : 512;
+
+  const uint32_t ngroups = (a.njobs + W - 1) / W;
+  if (blockIdx.x >= ngroups) return;
+  const uint32_t my_groups = (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const uint32_t steps = static_cast<uint32_t>(a.steps);
+  const uint32_t total_chunks = my_groups * steps * kFftChunks;  // < 2^32 (launcher checks)
+
+  if (tid == 0) {
+    for (int s = 0; s < kFSlots; s++) {
+      mbar_init(&mbar[s], 1);
+      rel[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this warp's 256 TMEM columns in its lane quadrant: column rho * 16 + (o * 2 + l) * 4 + {re lo, re hi, im lo, im hi}
+  const uint32_t tm = *tmem_base_sh + ((32u * (w & 3u)) << 16) + (w >> 2) * 256u;
+
+  // per-lane twiddles psi^{lane (1 + 4 k1)}, k1 = mrev(rho) (the psi^lane factor of the fold twist merged in)
+  cd tw[9];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const double2 t = a.psi[(lane * (1u + 4u * mrev(r))) & 2047u];
+    tw[r] = {t.x, t.y};
+  }
+  {
+    const double2 t = a.psi[(8u * lane) & 2047u];
+    tw[8] = {t.x, t.y};
+  }
+
+  auto issue = [&](uint32_t nseq) {
+    const uint32_t step = (nseq / kFftChunks) % steps, c = nseq % kFftChunks, s = nseq % kFSlots;
+    bulk_load(ring + s * (kFftChunkBytes / 16),
+              a.bskf + (static_cast<size_t>(step) * kFftChunks + c) * (kFftChunkBytes / 16), kFftChunkBytes, &mbar[s]);
+  };
+  if (tid == 0)
+    for (uint32_t q = 0; q < kFSlots && q < total_chunks; q++) issue(q);
+  uint32_t nseq = 0, sl = 0, ph = 0;
+  auto release = [&]() {  // this warp is done with ring slot sl
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&rel[sl], 1u) == W - 1) {
+        atomicExch(&rel[sl], 0u);
+        if (nseq + kFSlots < total_chunks) {
+          fence_proxy_async();
+          issue(nseq + kFSlots);
+        }
+      }
+    }
+    nseq++;
+    if (++sl == kFSlots) {
+      sl = 0;
+      ph ^= 1u;
+    }
+  };
+
+  for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const uint32_t jb = grp * W + w;
+    if (jb >= a.njobs) {  // idle warp of the last group: keep the ring moving
+      for (uint32_t c = 0; c < steps * kFftChunks; c++) {
+        mbar_wait(&mbar[sl], ph);
+        release();
+      }
+      continue;
+    }
+    // ---- S2 gate linear form + S3 mod-switch: abar[0..629], bbar at [630], test-vector select at [631]
+    {
+      const BrJob job = a.jobs[jb];
+      const uint32_t* x = slot_ptr(a.reg, job.x);
+      const uint32_t* y = slot_ptr(a.reg, job.y);
+      for (uint32_t wd = lane; wd <= static_cast<uint32_t>(n); wd += 32) {
+        uint32_t c = static_cast<uint32_t>(static_cast<int32_t>(job.ax)) * x[wd];
+        if (job.ay) c += static_cast<uint32_t>(static_cast<int32_t>(job.ay)) * y[wd];
+        if (wd == static_cast<uint32_t>(n)) c += job.k0;
+        abar[wd] = static_cast<uint16_t>(((c + (1u << 20)) >> 21) & (2 * N - 1));
+      }
+      if (lane == 0) abar[n + 1] = job.tv;
+    }
+    __syncwarp();
+    // ---- S4 accumulator init: (0, X^{-bbar} testv), testv = 1/8 (R8; 1/4 for R24 jobs)
+    {
+      const uint32_t bbar = abar[n], mu = abar[n + 1] ? 2u * kMu : kMu;
+      for (uint32_t k = lane; k < static_cast<uint32_t>(N); k += 32) {
+        acc[k] = 0;
+        acc[N + k] = (((k + bbar) & (2 * N - 1)) < static_cast<uint32_t>(N)) ? mu : (0u - mu);
+      }
+    }
+    __syncwarp();
+
+    // ---- S5: CMux steps
+    for (uint32_t i = 0; i < steps; i++) {
+      const uint32_t ab = abar[i];
+#pragma unroll 1
+      for (int u = 0; u < 2; u++) {
+        uint32_t wv[32];
+        const uint32_t* au = acc + u * N;
+#pragma unroll
+        for (int q = 0; q < 32; q++) {
+          const uint32_t j = 32u * q + lane;
+          const uint32_t kk = (j - ab) & (2 * N - 1);
+          uint32_t v = au[kk & (N - 1)];
+          v = kk >= static_cast<uint32_t>(N) ? 0u - v : v;
+          wv[q] = v - au[j] + 0x81020400u;
+        }
+#pragma unroll 1
+        for (int dj = 0; dj < 3; dj++) {
+          cd X[16];
+          fft_fwd(X, wv, 25u - 7u * dj, tw, tr, lane);
+          const bool first = u == 0 && dj == 0;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            mbar_wait(&mbar[sl], ph);
+            const double2* kc = ring + sl * (kFftChunkBytes / 16) + lane;
+#pragma unroll
+            for (int rp = 0; rp < 8; rp++) {
+              const int rho = 8 * h + rp;
+              const uint32_t ta = tm + rho * 16;
+              double ac[8];  // [ol][re, im]
+              if (!first) {
+#pragma unroll
+                for (int q = 0; q < 8; q++) tm_ld_d(ta + 2 * q, ac[q]);
+                tm_wait_ld();
+              } else {
+#pragma unroll
+                for (int q = 0; q < 8; q++) ac[q] = 0.0;
+              }
+#pragma unroll
+              for (int ol = 0; ol < 4; ol++) {
+                const double2 k = kc[(rp * 4 + ol) * 32];
+                ac[2 * ol] = fma(X[rho].x, k.x, fma(-X[rho].y, k.y, ac[2 * ol]));
+                ac[2 * ol + 1] = fma(X[rho].x, k.y, fma(X[rho].y, k.x, ac[2 * ol + 1]));
+              }
+#pragma unroll
+              for (int q = 0; q < 8; q++) tm_st_d(ta + 2 * q, ac[q]);
+            }
+            release();
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+      // inverse transforms, rounding: acc_o += R_lo, acc_o += 2^16 R_hi (mod 2^32), one limb at a time
+#pragma unroll 1
+      for (int ol = 0; ol < 4; ol++) {
+        cd V[16];
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+          tm_ld_d(tm + r * 16 + ol * 4, V[r].x);
+          tm_ld_d(tm + r * 16 + ol * 4 + 2, V[r].y);
+        }
+        tm_wait_ld();
+        fft_inv(V, tw, tr, lane);
+        uint32_t* ao = acc + (ol >> 1) * N + lane;
+        const uint32_t sh = (ol & 1) * 16u;
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          ao[32 * q] += round_u32(V[q].x) << sh;
+          ao[512 + 32 * q] += round_u32(V[q].y) << sh;
+        }
+      }
+      __syncwarp();
+    }
+
+    // ---- S6 SampleExtract: a'_0 = a_0, a'_k = -a_{N-k}, b' = b_0
+    if (a.raw_acc) {
+      uint32_t* o = a.raw_acc + static_cast<size_t>(jb) * 2 * N;
+      for (uint32_t k = lane; k < 2u * N; k += 32) o[k] = acc[k];
+    } else {
+      uint32_t* o = a.nlwe + static_cast<size_t>(a.jobs[jb].out) * kNlwe;
+      for (uint32_t k = lane; k < static_cast<uint32_t>(N); k += 32) o[k] = k == 0 ? acc[0] : 0u - acc[N - k];
+      if (lane == 0) o[N] = acc[N];
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kCols) : "memory");
+}
+
+// ================================================================================ K4F key conversion (setup)
+// One CTA per (i, digit row r): thread k (< 512) computes the four FFT-domain key values of point k (o in {0, 1}
+// output component, l in {lo, hi} limb) by a direct DFT in double: B_k = (1/512) sum_j (p_j + i p_{j+512})
+// psi^{j (1 + 4k)}, and stores them where lane L = k & 31, register rho = mrev(k >> 5) reads them.
+__global__ void __launch_bounds__(512) vlp_bsk_fft_kernel(const uint32_t* __restrict__ raw, double2* __restrict__ out,
+                                                          const double2* __restrict__ psi) {
+  __shared__ int32_t limb[4][N];  // [o * 2 + l][j]
+  const double2* ps = psi;
+  const uint32_t ir = blockIdx.x;  // i * 6 + r
+  for (uint32_t t = threadIdx.x; t < 2u * N; t += blockDim.x) {
+    const uint32_t o = t / N, j = t % N;
+    const int64_t s = static_cast<int32_t>(raw[(static_cast<size_t>(ir) * 2 + o) * N + j]);
+    const int64_t lo = ((s + 32768) & 65535) - 32768;
+    limb[o * 2 + 0][j] = static_cast<int32_t>(lo);
+    limb[o * 2 + 1][j] = static_cast<int32_t>((s - lo) >> 16);
+  }
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  double re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
+  for (uint32_t j = 0; j < 512; j++) {
+    const double2 t = __ldg(ps + ((j * (1u + 4u * k)) & 2047u));
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const double x = static_cast<double>(limb[q][j]), y = static_cast<double>(limb[q][j + 512]);
+      re[q] = fma(x, t.x, fma(-y, t.y, re[q]));
+      im[q] = fma(x, t.y, fma(y, t.x, im[q]));
+    }
+  }
+  const uint32_t L = k & 31, rho = static_cast<uint32_t>(mrev(static_cast<int>(k >> 5)));
+  const uint32_t h = rho >> 3, rp = rho & 7;
+  double2* dst = out + (static_cast<size_t>(ir) * 2 + h) * (kFftChunkBytes / 16);
+#pragma unroll
+  for (int q = 0; q < 4; q++) dst[(rp * 4 + q) * 32 + L] = make_double2(re[q] / 512.0, im[q] / 512.0);
+}
+
+void launch_bsk_fft(const uint32_t* raw, double2* out, const double2* psi, cudaStream_t st) {
+  vlp_bsk_fft_kernel<<<n * kRows, 512, 0, st>>>(raw, out, psi);
+}
+
+void set_fft_constants(const double2* psi) {
+  cd tws[16], w16[16], w32[8];
+  for (int a = 0; a < 16; a++) tws[a] = {psi[32 * a].x, psi[32 * a].y};
+  for (int k = 0; k < 16; k++) w16[k] = {psi[128 * k].x, psi[128 * k].y};
+  for (int r = 0; r < 8; r++) w32[r] = {psi[64 * r].x, psi[64 * r].y};
+  cudaMemcpyToSymbol(c_twist, tws, sizeof(tws));
+  cudaMemcpyToSymbol(c_w16, w16, sizeof(w16));
+  cudaMemcpyToSymbol(c_w32, w32, sizeof(w32));
+}
+
+template <int W>
+static cudaError_t launch_fft_w(const BrArgs& a, int sm_count, cudaStream_t st) {
+  static std::atomic<uint64_t> attr_set{0};
+  const int smem = fft_smem_bytes(W) > kFSmemMin ? fft_smem_bytes(W) : kFSmemMin;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
+    e = cudaFuncSetAttribute(vlp_blind_rotate_fft_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit);
+  }
+  if (a.njobs == 0) return cudaSuccess;
+  const uint64_t groups = (a.njobs + W - 1) / W;
+  const int grid = static_cast<int>(groups < static_cast<uint64_t>(sm_count) ? groups : sm_count);
+  if (grid <= 0 || (groups + grid - 1) / grid * static_cast<uint64_t>(a.steps) * kFftChunks >= (1ull << 32))
+    return cudaErrorInvalidValue;
+  vlp_blind_rotate_fft_kernel<W><<<grid, W * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blind_rotate_fft(const BrArgs& a, int warps, int sm_count, cudaStream_t st) {
+  switch (warps) {
+    case 1: return launch_fft_w<1>(a, sm_count, st);
+    case 2: return launch_fft_w<2>(a, sm_count, st);
+    case 3: return launch_fft_w<3>(a, sm_count, st);
+    case 4: return launch_fft_w<4>(a, sm_count, st);
+    case 5: return launch_fft_w<5>(a, sm_count, st);
+    case 6: return launch_fft_w<6>(a, sm_count, st);
+    case 7: return launch_fft_w<7>(a, sm_count, st);
+    default: return launch_fft_w<8>(a, sm_count, st);
+  }
+}
+
+}  // namespace vlp

@@ -23,15 +23,22 @@ for l in txt.splitlines():
     if ".text." in l and "section" in l: on = kern in l
     if not on: continue
     m = re.search(r"line (\d+)", l)
-    if m and "//##" in l: line = int(m.group(1)); continue
+    if m and "//##" in l:
+        line = int(m.group(1)) if os.path.basename(os.environ.get("SRC", "kernels.cu")) in l else line
+        continue
     m = re.search(r"/\*([0-9a-f]{4,})\*/\s+\S", l)
     if m: addr2line[int(m.group(1), 16)] = line
 inst = collections.Counter(); samp = collections.Counter(); ti = ts = 0
+ops = collections.defaultdict(collections.Counter)
 for a, src, n, s in prof:
     ln = addr2line.get(a - base, -1)
     inst[ln] += n; samp[ln] += s; ti += n; ts += s
-src = open(os.path.join(os.path.dirname(os.path.abspath(obj)), "..", "csrc", "kernels.cu")).read().splitlines()
+    op = src.split()[0] if src else "?"
+    if op.startswith("@"): op = src.split()[1]
+    ops[ln][op.rstrip(";")] += n
+src = open(os.environ.get("SRC", os.path.join(os.path.dirname(os.path.abspath(obj)), "..", "csrc", "kernels.cu"))).read().splitlines()
 print(f"{'line':>5} {'%inst':>6} {'%samp':>6}  source")
 for ln, n in sorted(inst.items(), key=lambda kv: -kv[1])[:top]:
     s = src[ln - 1].strip()[:90] if 0 < ln <= len(src) else "?"
-    print(f"{ln:5d} {n / ti * 100:6.2f} {samp[ln] / ts * 100:6.2f}  {s}")
+    top3 = ", ".join(f"{o} {c / n * 100:.0f}%" for o, c in ops[ln].most_common(3))
+    print(f"{ln:5d} {n / ti * 100:6.2f} {samp[ln] / ts * 100:6.2f}  {s[:70]:70s} | {top3}")
