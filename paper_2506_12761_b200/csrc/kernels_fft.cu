@@ -43,9 +43,9 @@ __constant__ cd c_w16[16];    // w16^k = psi^(128 k)
 __constant__ cd c_w32[8];     // w32^r = psi^(64 r)
 
 constexpr int kFSlots = 5;                         // key ring depth (chunks of 16 KB)
-constexpr int kTrStride = 33;                      // complex per transpose row (one pad: conflict-free LDS.128)
-constexpr int kTrBytes = 16 * kTrStride * 16;      // 8448
-constexpr int kFWarpBytes = 2 * N * 4 + kTrBytes + 640 * 2;  // accumulator + transpose buffer + abar: 17,920
+constexpr int kTrStride = 17;                      // complex per transpose row (one pad: conflict-free LDS.128)
+constexpr int kTrBytes = 2 * 16 * kTrStride * 16;  // T[g 2][k1 16][i 16 + 1]: 8704
+constexpr int kFWarpBytes = 2 * N * 4 + kTrBytes + 640 * 2;  // accumulator + transpose buffer + abar: 18,176
 __host__ __device__ constexpr int fft_smem_bytes(int W) {
   return kFSlots * kFftChunkBytes + W * kFWarpBytes + kFSlots * 8 + kFSlots * 4 + 16;
 }
@@ -103,10 +103,8 @@ __device__ __forceinline__ cd shfl16(cd v) {
 }
 __device__ __forceinline__ cd sel(bool p, cd a, cd b) { return p ? a : b; }
 
-// Gadget digit field f = (w >> s) & 127 (R5: w = D + 0x81020400) as the double f - 64 (exact: 2^52 + f - (2^52 + 64))
-__device__ __forceinline__ double digit_d(uint32_t w, uint32_t s) {
-  return __hiloint2double(0x43300000, static_cast<int>((w >> s) & 127u)) - 4503599627370560.0;
-}
+// Gadget digit field f = (w >> s) & 127 (R5: w = D + 0x81020400) enters the FFT as the double f - 64, exactly:
+// (2^52 + f) - (2^52 + 64), the first term built by putting f into the low mantissa word of 2^52 (fft_fwd).
 // round(v) mod 2^32 for |v| < 2^51 (1.5 * 2^52 shifts the integer part into the low mantissa word)
 __device__ __forceinline__ uint32_t round_u32(double v) {
   return static_cast<uint32_t>(__double2loint(v + 6755399441055744.0));
@@ -114,70 +112,85 @@ __device__ __forceinline__ uint32_t round_u32(double v) {
 
 // Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
 // 32 q + lane, q < 32) -> X[rho] = point lane + 32 mrev(rho).
-// Per-lane twiddle of register rho: psi^{lane (1 + 4 mrev(rho))}; registers rho and rho + 8 differ by the factor
-// psi^{8 lane} (mrev(rho + 8) = mrev(rho) + 2), so only rho < 8 and that factor are kept (tw[8]).
-__device__ __forceinline__ cd twid(const cd (&tw)[9], int r) { return r < 8 ? tw[r] : cmul(tw[r - 8], tw[8]); }
+// Per-lane constants of the transform (lane b = 16 h + bb).
+//  * Lanes with h = 1 negate the odd inputs a of their first 16-point DFT, which shifts its output by 8: register
+//    rho then holds k1 = mrev(rho) ^ 8h.  So the registers rho with mrev(rho) < 8 ("A": rho & 2 == 0) hold each
+//    lane's own 8 k1 values and the lane-pair partner (b ^ 16) holds the matching values in register rho | 2 --
+//    the lane-pair radix-2 stage needs no lane-dependent selects (tools/emulate_br_fft.py --v3).
+//  * tw[r] = psi^{b (1 + 4 k1(rho = r))} for r < 8 (the fold twist's psi^b merged in); registers rho and rho + 8
+//    differ by psi^{8b} (tw[8]).
+//  * tau = (h ? -1 : 1) w32^bb, the twiddle of the pair's difference (the sign makes both lanes use own - partner).
+struct Lane {
+  cd tw[9];
+  cd tau;
+  double sgn, off;  // sgn = h ? -1 : 1; off = -sgn (2^52 + 64) (odd-a digit conversion)
+  uint32_t lane, tbase;  // tbase: this lane's transpose offset (8h * kTrStride + bb) in complex
+};
+__device__ __forceinline__ cd twid(const Lane& c, int r) { return r < 8 ? c.tw[r] : cmul(c.tw[r - 8], c.tw[8]); }
 
-__device__ __forceinline__ void fft_fwd(cd (&v)[16], const uint32_t (&wv)[32], uint32_t s, const cd (&tw)[9],
-                                        cd* tr, uint32_t lane) {
+// Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
+// 32 q + lane, q < 32) -> v[rho] = point lane + 32 mrev(rho).
+__device__ __forceinline__ void fft_fwd(cd (&v)[16], const uint32_t (&wv)[32], uint32_t s, const Lane& c, double2* tr) {
 #pragma unroll
   for (int a = 0; a < 16; a++) {
-    const cd x{digit_d(wv[a], s), digit_d(wv[16 + a], s)};
+    const double rx = __hiloint2double(0x43300000, static_cast<int>((wv[a] >> s) & 127u));
+    const double ry = __hiloint2double(0x43300000, static_cast<int>((wv[16 + a] >> s) & 127u));
+    // (f - 64), times -1 on odd a of the h = 1 lanes (exact: one rounding of a small integer)
+    const cd x = (a & 1) ? cd{fma(c.sgn, rx, c.off), fma(c.sgn, ry, c.off)}
+                         : cd{rx - 4503599627370560.0, ry - 4503599627370560.0};
     v[a] = a == 0 ? x : cmul(x, c_twist[a]);
   }
   dft16_fwd(v);
   __syncwarp();  // the previous reader of tr is done
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
-    const cd t = cmul(v[r], twid(tw, r));
-    reinterpret_cast<double2*>(tr)[mrev(r) * kTrStride + lane] = make_double2(t.x, t.y);
+  for (int q = 0; q < 8; q++) {
+    const int ra = (q & 1) | ((q >> 1) << 2);  // 0, 1, 4, 5, 8, 9, 12, 13
+    const cd own = cmul(v[ra], twid(c, ra));
+    const cd recv = shfl16(cmul(v[ra | 2], twid(c, ra | 2)));
+    const cd sm = cadd(own, recv);
+    const cd df = cmul(csub(own, recv), c.tau);
+    double2* t = tr + c.tbase + mrev(ra) * kTrStride;
+    t[0] = make_double2(sm.x, sm.y);
+    t[16 * kTrStride] = make_double2(df.x, df.y);
   }
   __syncwarp();
-  const uint32_t e = lane >> 4, k1 = lane & 15;
-  const bool hi = e != 0;
-  const double2* row = reinterpret_cast<const double2*>(tr) + k1 * kTrStride + 8 * e;
+  const double2* row = tr + (c.lane >> 4) * 16 * kTrStride + (c.lane & 15) * kTrStride;
 #pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const double2 yi = row[r], yj = row[16 + r];
-    const cd sm{yi.x + yj.x, yi.y + yj.y};
-    cd df{yi.x - yj.x, yi.y - yj.y};
-    if (r) df = cmul(df, c_w32[r]);
-    df = sel(hi, cd{-df.y, df.x}, df);  // w32^(8 e + r) = i^e w32^r
-    // lane e = 0 keeps its sums and gets the partner's sums (i >= 8); e = 1 keeps its differences and gets
-    // the partner's differences (i < 8)
-    const cd recv = shfl16(sel(hi, sm, df));
-    v[r] = sel(hi, recv, sm);
-    v[8 + r] = sel(hi, df, recv);
+  for (int i = 0; i < 16; i++) {
+    const double2 t = row[i];
+    v[i] = {t.x, t.y};
   }
   dft16_fwd(v);
 }
 
-// Inverse transform: v[rho] at point lane + 32 mrev(rho) -> v[a] = 512 * (c_{32a+lane} + i c_{32a+lane+512})
-__device__ __forceinline__ void fft_inv(cd (&v)[16], const cd (&tw)[9], cd* tr, uint32_t lane) {
-  dft16_inv(v);  // 16 V_e[i]
-  const uint32_t e = lane >> 4, k1 = lane & 15;
-  const bool hi = e != 0;
+// Inverse transform: v[rho] at point lane + 32 mrev(rho) -> v[a] = 512 sgn^a (c_{32a+lane} + i c_{32a+lane+512})
+// (sgn^a: the h = 1 lanes' odd a come out negated; round_u32s undoes it)
+__device__ __forceinline__ void fft_inv(cd (&v)[16], const Lane& c, double2* tr) {
+  dft16_inv(v);
   __syncwarp();
-  double2* row = reinterpret_cast<double2*>(tr) + k1 * kTrStride + 8 * e;
+  double2* row = tr + (c.lane >> 4) * 16 * kTrStride + (c.lane & 15) * kTrStride;
 #pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const cd recv = shfl16(sel(hi, v[r], v[8 + r]));
-    const cd sm = sel(hi, recv, v[r]);
-    cd df = sel(hi, v[8 + r], recv);
-    df = sel(hi, cd{df.y, -df.x}, df);  // conj(i^e)
-    if (r) df = cmulc(df, c_w32[r]);
-    row[r] = make_double2(sm.x + df.x, sm.y + df.y);
-    row[16 + r] = make_double2(sm.x - df.x, sm.y - df.y);
-  }
+  for (int i = 0; i < 16; i++) row[i] = make_double2(v[i].x, v[i].y);
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
-    const double2 t = reinterpret_cast<const double2*>(tr)[mrev(r) * kTrStride + lane];
-    v[r] = cmulc(cd{t.x, t.y}, twid(tw, r));
+  for (int q = 0; q < 8; q++) {
+    const int ra = (q & 1) | ((q >> 1) << 2);
+    const double2* t = tr + c.tbase + mrev(ra) * kTrStride;
+    const double2 s2 = t[0], d2 = t[16 * kTrStride];
+    const cd dd = cmulc(cd{d2.x, d2.y}, c.tau);
+    const cd own{s2.x + dd.x, s2.y + dd.y};
+    const cd part = shfl16(cd{s2.x - dd.x, s2.y - dd.y});
+    v[ra] = cmulc(own, twid(c, ra));
+    v[ra | 2] = cmulc(part, twid(c, ra | 2));
   }
   dft16_inv(v);
 #pragma unroll
   for (int a = 1; a < 16; a++) v[a] = cmulc(v[a], c_twist[a]);
+}
+// round(sgn^a v) mod 2^32 (see fft_inv)
+template <int A>
+__device__ __forceinline__ uint32_t round_u32s(double v, const Lane& c) {
+  return static_cast<uint32_t>(__double2loint((A & 1) ? fma(c.sgn, v, 6755399441055744.0) : v + 6755399441055744.0));
 }
 
 // TMEM (32x32b: lane = thread): one double <-> 2 consecutive columns (lo, hi word).  x2 ops take the double's own
@@ -195,6 +208,36 @@ __device__ __forceinline__ void tm_ld_d(uint32_t ta, double& v) {
                : "memory");
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// MAC of one key chunk (digit row r, registers 8h .. 8h + 7): acc[o][l] (+)= X * B_r[o][l] per point, the
+// accumulators (doubles, re/im, ol = o * 2 + l) at TMEM columns rho * 16 + ol * 4 + {0: re, 2: im}.
+template <bool FIRST>
+__device__ __forceinline__ void mac_half(const cd (&X)[16], int h, const double2* kc, uint32_t tm) {
+#pragma unroll
+  for (int rp = 0; rp < 8; rp++) {
+    const int rho = 8 * h + rp;
+    const uint32_t ta = tm + rho * 16;
+    double ac[8];
+    if (!FIRST) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) tm_ld_d(ta + 2 * q, ac[q]);
+      tm_wait_ld();
+    }
+#pragma unroll
+    for (int ol = 0; ol < 4; ol++) {
+      const double2 k = kc[(rp * 4 + ol) * 32];
+      if (FIRST) {
+        ac[2 * ol] = fma(X[rho].x, k.x, -(X[rho].y * k.y));
+        ac[2 * ol + 1] = fma(X[rho].x, k.y, X[rho].y * k.x);
+      } else {
+        ac[2 * ol] = fma(X[rho].x, k.x, fma(-X[rho].y, k.y, ac[2 * ol]));
+        ac[2 * ol + 1] = fma(X[rho].x, k.y, fma(X[rho].y, k.x, ac[2 * ol + 1]));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) tm_st_d(ta + 2 * q, ac[q]);
+  }
+}
+
 }  // namespace
 
 // ================================================================================ K2F blind rotation
@@ -209,9 +252,10 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   extern __shared__ __align__(128) uint8_t smem[];
   double2* ring = reinterpret_cast<double2*>(smem);
   uint8_t* wb = smem + kFSlots * kFftChunkBytes;
-  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t w = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform (lets the TMEM address live in a UR)
   uint32_t* acc = reinterpret_cast<uint32_t*>(wb + w * kFWarpBytes);
-  cd* tr = reinterpret_cast<cd*>(wb + w * kFWarpBytes + 2 * N * 4);
+  double2* tr = reinterpret_cast<double2*>(wb + w * kFWarpBytes + 2 * N * 4);
   uint16_t* abar = reinterpret_cast<uint16_t*>(wb + w * kFWarpBytes + 2 * N * 4 + kTrBytes);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(wb + W * kFWarpBytes);
   uint32_t* rel = reinterpret_cast<uint32_t*>(mbar + kFSlots);
@@ -243,16 +287,23 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   // this warp's 256 TMEM columns in its lane quadrant: column rho * 16 + (o * 2 + l) * 4 + {re lo, re hi, im lo, im hi}
   const uint32_t tm = *tmem_base_sh + ((32u * (w & 3u)) << 16) + (w >> 2) * 256u;
 
-  // per-lane twiddles psi^{lane (1 + 4 k1)}, k1 = mrev(rho) (the psi^lane factor of the fold twist merged in)
-  cd tw[9];
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const double2 t = a.psi[(lane * (1u + 4u * mrev(r))) & 2047u];
-    tw[r] = {t.x, t.y};
-  }
+  // per-lane constants of the transform (see Lane)
+  Lane lc;
   {
-    const double2 t = a.psi[(8u * lane) & 2047u];
-    tw[8] = {t.x, t.y};
+    const uint32_t h = lane >> 4;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const double2 t = a.psi[(lane * (1u + 4u * (static_cast<uint32_t>(mrev(r)) ^ (8u * h)))) & 2047u];
+      lc.tw[r] = {t.x, t.y};
+    }
+    const double2 t8 = a.psi[(8u * lane) & 2047u];
+    lc.tw[8] = {t8.x, t8.y};
+    const double2 w32 = a.psi[(64u * (lane & 15u)) & 2047u];
+    lc.sgn = h ? -1.0 : 1.0;
+    lc.tau = {lc.sgn * w32.x, lc.sgn * w32.y};
+    lc.off = -lc.sgn * 4503599627370560.0;
+    lc.lane = lane;
+    lc.tbase = 8u * h * kTrStride + (lane & 15u);
   }
 
   auto issue = [&](uint32_t nseq) {
@@ -333,35 +384,21 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
 #pragma unroll 1
         for (int dj = 0; dj < 3; dj++) {
           cd X[16];
-          fft_fwd(X, wv, 25u - 7u * dj, tw, tr, lane);
-          const bool first = u == 0 && dj == 0;
+          fft_fwd(X, wv, 25u - 7u * dj, lc, tr);
+          if (u == 0 && dj == 0) {
 #pragma unroll
-          for (int h = 0; h < 2; h++) {
-            mbar_wait(&mbar[sl], ph);
-            const double2* kc = ring + sl * (kFftChunkBytes / 16) + lane;
-#pragma unroll
-            for (int rp = 0; rp < 8; rp++) {
-              const int rho = 8 * h + rp;
-              const uint32_t ta = tm + rho * 16;
-              double ac[8];  // [ol][re, im]
-              if (!first) {
-#pragma unroll
-                for (int q = 0; q < 8; q++) tm_ld_d(ta + 2 * q, ac[q]);
-                tm_wait_ld();
-              } else {
-#pragma unroll
-                for (int q = 0; q < 8; q++) ac[q] = 0.0;
-              }
-#pragma unroll
-              for (int ol = 0; ol < 4; ol++) {
-                const double2 k = kc[(rp * 4 + ol) * 32];
-                ac[2 * ol] = fma(X[rho].x, k.x, fma(-X[rho].y, k.y, ac[2 * ol]));
-                ac[2 * ol + 1] = fma(X[rho].x, k.y, fma(X[rho].y, k.x, ac[2 * ol + 1]));
-              }
-#pragma unroll
-              for (int q = 0; q < 8; q++) tm_st_d(ta + 2 * q, ac[q]);
+            for (int h = 0; h < 2; h++) {
+              mbar_wait(&mbar[sl], ph);
+              mac_half<true>(X, h, ring + sl * (kFftChunkBytes / 16) + lane, tm);
+              release();
             }
-            release();
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              mbar_wait(&mbar[sl], ph);
+              mac_half<false>(X, h, ring + sl * (kFftChunkBytes / 16) + lane, tm);
+              release();
+            }
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
@@ -376,13 +413,15 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
           tm_ld_d(tm + r * 16 + ol * 4 + 2, V[r].y);
         }
         tm_wait_ld();
-        fft_inv(V, tw, tr, lane);
+        fft_inv(V, lc, tr);
         uint32_t* ao = acc + (ol >> 1) * N + lane;
         const uint32_t sh = (ol & 1) * 16u;
 #pragma unroll
         for (int q = 0; q < 16; q++) {
-          ao[32 * q] += round_u32(V[q].x) << sh;
-          ao[512 + 32 * q] += round_u32(V[q].y) << sh;
+          const uint32_t rx = (q & 1) ? round_u32s<1>(V[q].x, lc) : round_u32s<0>(V[q].x, lc);
+          const uint32_t ry = (q & 1) ? round_u32s<1>(V[q].y, lc) : round_u32s<0>(V[q].y, lc);
+          ao[32 * q] += rx << sh;
+          ao[512 + 32 * q] += ry << sh;
         }
       }
       __syncwarp();

@@ -204,5 +204,87 @@ def main():
         print(f"{nl} limb(s): worst |err| over {trials} trials = {worst:.3g}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--v3" not in sys.argv:
     main()
+
+
+# ---------------------------------------------------------------------------- v3: select-free lane pairs
+# Lane b = 16 h + bb.  Lanes h = 1 negate odd inputs a, so their first 16-point DFT comes out shifted by 8:
+# register rho holds k1 = mrev(rho) ^ 8h.  Registers A (mrev(rho) < 8) are a lane's own k1 set; the partner's
+# matching values sit in register rho | 2.  The lane pair (bb, bb + 16) forms s = Y_bb + Y_bb+16 and
+# d = (Y_bb - Y_bb+16) w32^bb for the 8 k1 of each lane; T[g][k1][bb] (g = 0: s, 1: d); lane L = (g, k1) reads
+# 16 values and runs the second 16-point DFT -> point L + 32 mrev(rho), as before.
+A_REGS = [r for r in range(16) if not (r & 2)]
+
+
+def k1_of(b, rho):
+    return MREV[rho] ^ (8 * (b >> 4))
+
+
+TW3 = np.array([[PSI[(b * (1 + 4 * k1_of(b, r))) % 2048] for r in range(16)] for b in range(32)])
+TAU = np.array([(-1 if b >> 4 else 1) * W32[b & 15] for b in range(32)])
+SIG = np.array([[(-1) ** a if b >> 4 else 1 for a in range(16)] for b in range(32)])
+
+
+def fwd3(x):
+    u = np.empty((32, 16), complex)
+    for b in range(32):
+        for a in range(16):
+            u[b, a] = SIG[b, a] * (x[32 * a + b] + 1j * x[32 * a + b + 512]) * TWIST[a]
+    y = dft16_fwd(u) * TW3
+    T = np.zeros((2, 16, 16), complex)
+    for b in range(32):
+        P = b ^ 16
+        for ra in A_REGS:
+            recv = y[P, ra | 2]
+            s = y[b, ra] + recv
+            d = (y[b, ra] - recv) * TAU[b]
+            k1 = k1_of(b, ra)
+            T[0, k1, b & 15], T[1, k1, b & 15] = s, d
+    V = np.empty((32, 16), complex)
+    for L in range(32):
+        V[L] = T[L >> 4, L & 15, :]
+    return dft16_fwd(V)
+
+
+def inv3(C):
+    V = dft16_inv(C)
+    T = np.zeros((2, 16, 16), complex)
+    for L in range(32):
+        T[L >> 4, L & 15, :] = V[L]
+    y = np.empty((32, 16), complex)
+    part = np.empty((32, 16), complex)
+    for b in range(32):
+        for ra in A_REGS:
+            k1 = k1_of(b, ra)
+            s, d = T[0, k1, b & 15], T[1, k1, b & 15]
+            dd = d * np.conj(TAU[b])
+            y[b, ra] = s + dd
+            part[b, ra] = s - dd
+    for b in range(32):
+        for ra in A_REGS:
+            y[b, ra | 2] = part[b ^ 16, ra]
+    u = dft16_inv(y * np.conj(TW3))
+    out = np.empty(1024)
+    for b in range(32):
+        for a in range(16):
+            z = u[b, a] * np.conj(TWIST[a]) * SIG[b, a]
+            out[32 * a + b], out[32 * a + b + 512] = z.real, z.imag
+    return out
+
+
+def check_v3():
+    rng = np.random.default_rng(9)
+    x = rng.integers(-64, 64, N)
+    p = rng.integers(-2 ** 15, 2 ** 15, N)
+    assert np.max(np.abs(fwd3(x.astype(float)) - fwd(x.astype(float)))) < 1e-6, "v3 forward layout"
+    got = inv3(fwd3(x.astype(float)) * key_fft(p.astype(float)))
+    want = np.convolve(x, p)
+    want = want[:N] - np.concatenate([want[N:], [0]])
+    err = np.max(np.abs(got - want))
+    print("v3 single product max |err| =", err)
+    assert err < 1e-3
+
+
+if __name__ == "__main__" and "--v3" in sys.argv:
+    check_v3()

@@ -13,27 +13,34 @@
 
 namespace vlp {
 __global__ void fft_unit_kernel(const int* x, const double2* key, const double2* psi, double2* Xout, double* out) {
-  __shared__ cd trb[16 * 33];
-  const uint32_t lane = threadIdx.x;
-  cd tw[9];
+  __shared__ double2 trb[2 * 16 * kTrStride];
+  const uint32_t lane = threadIdx.x, h = lane >> 4;
+  Lane lc;
   for (int r = 0; r < 8; r++) {
-    const double2 t = psi[(lane * (1u + 4u * mrev(r))) & 2047u];
-    tw[r] = {t.x, t.y};
+    const double2 t = psi[(lane * (1u + 4u * (static_cast<uint32_t>(mrev(r)) ^ (8u * h)))) & 2047u];
+    lc.tw[r] = {t.x, t.y};
   }
-  tw[8] = {psi[(8u * lane) & 2047u].x, psi[(8u * lane) & 2047u].y};
+  lc.tw[8] = {psi[(8u * lane) & 2047u].x, psi[(8u * lane) & 2047u].y};
+  const double2 w32 = psi[(64u * (lane & 15u)) & 2047u];
+  lc.sgn = h ? -1.0 : 1.0;
+  lc.tau = {lc.sgn * w32.x, lc.sgn * w32.y};
+  lc.off = -lc.sgn * 4503599627370560.0;
+  lc.lane = lane;
+  lc.tbase = 8u * h * kTrStride + (lane & 15u);
   uint32_t wv[32];
   for (int q = 0; q < 32; q++) wv[q] = static_cast<uint32_t>(x[32 * q + lane] + 64) << 25;
   cd X[16];
-  fft_fwd(X, wv, 25u, tw, trb, lane);
+  fft_fwd(X, wv, 25u, lc, trb);
   for (int r = 0; r < 16; r++) {
     Xout[lane * 16 + r] = make_double2(X[r].x, X[r].y);
     const double2 k = key[lane * 16 + r];
     X[r] = cmul(X[r], cd{k.x, k.y});
   }
-  fft_inv(X, tw, trb, lane);
+  fft_inv(X, lc, trb);
   for (int a = 0; a < 16; a++) {
-    out[32 * a + lane] = X[a].x;
-    out[32 * a + lane + 512] = X[a].y;
+    const double sg = (a & 1) ? lc.sgn : 1.0;
+    out[32 * a + lane] = sg * X[a].x;
+    out[32 * a + lane + 512] = sg * X[a].y;
   }
 }
 }  // namespace vlp
