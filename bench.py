@@ -1,11 +1,11 @@
 #!/usr/bin/env python
 """bench.py -- VeLoPIR query throughput on B200 (gate bootstraps/s and records/s per query).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
 
-A step is one VeLoPIR query over BASELINE.json config 2 (IntV 1D, 1024 records, l_I = l_S = 16; 132,080
-blind rotations, 99,312 key switches, 29 levels) with the encrypted DB and the query already resident in
-HBM.  With N > 1 (torchrun) the records are sharded contiguously (M/N each, R15): the query is broadcast
+A step is one VeLoPIR query over BASELINE.json config 3 (the largest single-GPU config: "CoV 2D" rectangle
+containment, 4096 records, l_I = 16, l_S = 32; 1,060,832 blind rotations, 798,688 key switches, 32 levels)
+with the encrypted DB and the query already resident in HBM.  With N > 1 (torchrun) the records are sharded contiguously (M/N each, R15): the query is broadcast
 (NCCL), every rank evaluates its shard down to its root, the roots are gathered to rank 0 (NCCL) and rank 0
 runs the top log2 N tree levels: strong scaling of one query.  `e2e` repeats the step through the public API
 with the query copied from pinned host memory and the result copied back every step.  `--impl reference`
@@ -32,18 +32,22 @@ from synth.workloads import expected_result, extra_queries  # noqa: E402
 METRIC = "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
 UNIT = "gate bootstraps/s"
 CONFIG_BR = {1: 252, 2: 132080, 3: 1060832, 4: 6750176}
-# dram__bytes_read.sum + dram__bytes_write.sum of one vlp_blind_rotate_kernel launch from `ncu --set full`
-# (profiles/r1_br_v11_ncu_summary.txt: a one-wave launch of 740 bootstraps, i.e. one bsk pass per CTA; the bsk
-# itself is L2-resident, so DRAM sees about one 92.9 MB bsk read per launch plus the ciphertexts)
-TRAFFIC_BYTES_PER_LAUNCH = (102.260992 + 4.645376) * 1e6
-TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_kernel<5>, 740-bootstrap launch (profiles/r1_br_v11_ncu_summary.txt)"
+# dram__bytes_read.sum + dram__bytes_write.sum of one K2F launch (one whole wave of 8 x 148 = 1184 bootstraps,
+# 630 CMux steps) from `ncu --set full` (profiles/r2_k2f_ncu_summary.txt): ~one pass over the 123.9 MB FFT-domain
+# key per launch (the key stays in the 126 MB L2 across the wave's CTAs) plus the ciphertexts.
+TRAFFIC_BYTES_PER_WAVE = (127.971840 + 4.631040) * 1e6
+TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_fft_kernel<8>, 1184-bootstrap launch (profiles/r2_k2f_ncu_summary.txt)"
+BSK_FFT_BYTES = 630 * 12 * 16384   # FFT-domain key streamed per pass (kernels.cuh kBskFftBytes)
+FP64_PER_BR = 4.375e6 * 32         # FP64 lane-ops per blind rotation in K2F (ncu SASS histogram, profiles/)
 
 
-def ops_per_br():
-    """Integer lane-operations of one blind rotation in the implemented algorithm:
-    per CMux step 12 NTTs x 5120 butterflies x 7 ops + 1024 positions x 72 MAC ops + 2048 x 15 digit ops
-    + 2048 x 19 lift/recombine ops."""
-    per_step = 12 * 5120 * 7 + 1024 * 72 + 2048 * 15 + 2048 * 19
+def alg_ops_per_br():
+    """SURVEY 8(d)'s algorithmic work of one blind rotation (the method's, not the engine's), in int32
+    lane-operations: per CMux step 8 negacyclic transforms of N = 1024 (6 forward digit polynomials, 2 inverse
+    outputs) x 5120 butterflies x 7 ops + 12 products x 1024 positions x 2 MAC ops + 2048 digit coefficients
+    x 15 ops + 2048 lifted coefficients x 19 ops; x 630 steps = 240.0 M (5,040 NTTs = 25.8 M butterflies and
+    7.74 M MACs per BR)."""
+    per_step = 8 * 5120 * 7 + 12 * 1024 * 2 + 2048 * 15 + 2048 * 19
     return 630 * per_step
 
 
@@ -56,15 +60,32 @@ def load_peaks():
 
 
 def int_peak():
-    """Issue-limited integer peak: 148 SMs x 4 SMSPs x 32 lanes x 1 instr/cycle x max SM clock.
-    If profiles/int_peak.json holds a measured IMAD/IADD3 mix rate, that is used instead."""
-    p = os.path.join(ROOT, "profiles", "int_peak.json")
+    """Measured integer peak of this pool's B200s: tools/int_peak.cu (1:1 IMAD / IADD3-LOP3 mix, every SMSP
+    full), profiles/int_peak_r1.json.  Falls back to the issue limit 148 SM x 128 lanes x max clock."""
+    p = os.path.join(ROOT, "profiles", "int_peak_r1.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d["gops"], "measured " + d.get("how", "")
+        return d["gops"], "measured (profiles/int_peak_r1.json): " + d.get("how", "")
     mhz = load_peaks().get("sm_max_mhz", 1965.0)
     return 148 * 128 * mhz * 1e6 / 1e9, "derived: 148 SM x 128 lanes x %.0f MHz" % mhz
+
+
+def fp64_peak():
+    """Measured FP64 pipe peak (tools/fp64_bench.cu: DFMA / DADD / DMUL each 1.97 warp-instr per SM per clock),
+    profiles/fp64_bench_r2.json, at the max SM clock: lane-ops/s in G."""
+    rate = 1.97
+    p = os.path.join(ROOT, "profiles", "fp64_bench_r2.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            for line in f:
+                if not line.startswith("{"):
+                    continue
+                d = json.loads(line)
+                if d.get("op") == "DFMA":
+                    rate = d["warp_instr_per_sm_per_clk_at_1965"]
+    mhz = load_peaks().get("sm_max_mhz", 1965.0)
+    return rate * 32 * 148 * mhz * 1e6 / 1e9
 
 
 class ClockSampler:
@@ -201,6 +222,8 @@ def run_nand(args, rank, world, local, dev, stream, A, L, dist):
     scaling is strong)."""
     import torch
     total = args.nand
+    if total % world:
+        raise SystemExit(f"--nand {total} must be a multiple of the {world} ranks (every counted gate is computed)")
     per = total // world
     a_bits, b_bits = nand_inputs(total, 2005)
     keys = A.Keys(1005)
@@ -238,15 +261,16 @@ def run_nand(args, rank, world, local, dev, stream, A, L, dist):
     ms = float(tot.item()) / args.steps
     if rank == 0:
         peak, how = int_peak()
-        achieved = ops_per_br() * per * args.steps / (br_ms / 1e3) / 1e9
+        achieved = alg_ops_per_br() * per * args.steps / (br_ms / 1e3) / 1e9
         print(json.dumps({
             "metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong",  # the batch (--nand gates in total) is split over the ranks: fixed total work
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"cfg5_nand_{total}", "gates": total, "l2": "flushed between steps (untimed)"},
-            "roofline": {"bound": "alu", "kernel": "vlp_blind_rotate_kernel", "achieved": achieved, "peak": peak,
-                         "unit": "Gop/s (int32 lane ops)", "frac": achieved / peak, "peak_source": how,
+            "roofline": {"bound": "alu", "kernel": "vlp_blind_rotate_fft_kernel", "achieved": achieved, "peak": peak,
+                         "unit": "Gop/s (SURVEY 8(d) algorithmic int32 lane ops)", "frac": achieved / peak,
+                         "peak_source": how,
                          "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
                          "traffic": None},
             "cpu_baseline": None, "e2e": None, "clocks": clocks,
@@ -258,7 +282,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2,
+    ap.add_argument("--config", type=int, default=3,
                     help="1-4: BASELINE.json configs; 5: NAND sweep; 6-9: synthetic stand-ins shaped like the paper's "
                          "datasets (covid-kor, covid-usa, gdacs, weather-usa; synth/workloads.py)")
     ap.add_argument("--nand", type=int, default=1 << 17, help="config 5: NAND gates per step (split over ranks)")
@@ -271,6 +295,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="steps of the end-to-end (host-buffer) measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -409,8 +434,9 @@ def main():
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_steps = max(1, min(args.e2e_steps, args.steps))
         e0.record(stream)
-        for s in range(args.steps):
+        for s in range(e2e_steps):
             if rank == 0:
                 qd.copy_(q_pin, non_blocking=True)
             step(qd)
@@ -421,22 +447,27 @@ def main():
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e_ms = float(et.item()) / args.steps
+        e2e_ms = float(et.item()) / e2e_steps
         if rank == 0:
             check_all(out_pin.numpy().view(np.uint32))
         e2e = {"value": nq * br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": nq * wl.M / (e2e_ms / 1e3),
                # the query, plus the job tables every server_eval / combine copies into its scratch
                "h2d_bytes_per_step": int(q_host.nbytes) + int(prog.info.table_bytes)
                                      + (int(comb.info.table_bytes) if comb else 0),
-               "d2h_bytes_per_step": int(nq * wl.l_S * 632 * 4)}
+               "d2h_bytes_per_step": int(nq * wl.l_S * 632 * 4), "steps": e2e_steps}
 
     if rank == 0:
         peak, peak_how = int_peak()
         br_launch_ms = br_ms / max(1, br_n)
-        # achieved over the dominant kernel: algorithmic integer ops of all BRs / total BR kernel time
+        # achieved over the dominant kernel (the blind rotation, CUDA events on its launch stream): SURVEY 8(d)'s
+        # algorithmic integer ops of all BRs / total BR kernel time
         br_in_shard = prog.info.br
-        achieved = ops_per_br() * br_in_shard * args.steps / (br_ms / 1e3) / 1e9 if br_ms > 0 else None
+        br_s = br_ms / 1e3
+        achieved = alg_ops_per_br() * br_in_shard * args.steps / br_s / 1e9 if br_ms > 0 else None
+        fp64 = FP64_PER_BR * br_in_shard * args.steps / br_s / 1e9 if br_ms > 0 else None
+        waves = br_in_shard / (8 * torch.cuda.get_device_properties(dev).multi_processor_count)
         cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline_oracle(extended=True)
+        hbm_peak = load_peaks().get("hbm_gbs", 6566.4)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -446,18 +477,30 @@ def main():
                        "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels, "queries_per_step": nq,
                        "parallelism": f"records sharded x{world}" if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)",
-                       "params": "TFHE n=630 N=1024 Bg=2^7 l=3 ks 2^2x8 (tab:tfhe_params)"},
-            "roofline": {"bound": "alu", "kernel": "vlp_blind_rotate_kernel", "achieved": achieved,
-                         "peak": peak, "unit": "Gop/s (int32 lane ops)", "frac": (achieved / peak) if achieved else None,
-                         "peak_source": peak_how, "ops_per_br": ops_per_br(),
+                       "params": "TFHE n=630 N=1024 Bg=2^7 l=3 ks 2^2x8 (tab:tfhe_params)",
+                       "engine": "K2F exact FP64 FFT (whole waves) + NTT latency kernels (narrow tails)"},
+            "roofline": {"bound": "alu", "kernel": "vlp_blind_rotate_fft_kernel", "achieved": achieved,
+                         "peak": peak, "unit": "Gop/s (SURVEY 8(d) algorithmic int32 lane ops)",
+                         "frac": (achieved / peak) if achieved else None, "peak_source": peak_how,
+                         "ops_per_br": alg_ops_per_br(),
+                         "ops_per_br_basis": "SURVEY 8(d): per CMux step 8 transforms x 5120 butterflies x 7 + 12 x 1024 "
+                                             "MAC x 2 + 2048 digit coefficients x 15 + 2048 lifts x 19; x 630",
+                         # the engine's own binding pipe: FP64 lane-ops the kernel executes per BR (ncu) / measured
+                         # FP64 peak (tools/fp64_bench.cu)
+                         "frac_impl": (fp64 / fp64_peak()) if fp64 else None, "impl_pipe": "fp64",
+                         "impl_achieved": fp64, "impl_peak": fp64_peak(), "impl_ops_per_br": FP64_PER_BR,
                          "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
                          "br_share_of_step": br_ms / args.steps / ms_per_step,
-                         "br_launch_avg_ms": br_launch_ms, "traffic": TRAFFIC_BYTES_PER_LAUNCH,
-                         "traffic_source": TRAFFIC_SOURCE,
-                         # the unit that binds this kernel on sm_100a (IMAD.HI / IMAD.WIDE issue at half rate),
-                         # from the same ncu capture as `traffic`
-                         "binding_unit": {"pipe": "fmaheavy", "active": 0.707,
-                                          "source": "sm__pipe_fmaheavy_cycles_active, profiles/r1_br_v11_ncu_summary.txt"}},
+                         "br_launch_avg_ms": br_launch_ms,
+                         "traffic": TRAFFIC_BYTES_PER_WAVE, "traffic_source": TRAFFIC_SOURCE,
+                         "traffic_unit": "bytes per whole-wave K2F launch"},
+            # bootstrapping-key streaming against HBM (north star): one FFT-domain key pass per wave of 8 bootstraps
+            # per SM; the key stays L2-resident across the CTAs of a wave, so DRAM sees about one pass per launch
+            "hbm": {"bsk_pass_bytes": BSK_FFT_BYTES, "passes_per_step": waves,
+                    "bsk_gbs": BSK_FFT_BYTES * waves / br_s * args.steps / 1e9 if br_ms > 0 else None,
+                    "peak_gbs": hbm_peak,
+                    "frac": (BSK_FFT_BYTES * waves / br_s * args.steps / 1e9 / hbm_peak) if br_ms > 0 else None,
+                    "note": "algorithmic key bytes (one pass per wave); the kernel is FP64/MIO-bound, not HBM-bound"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,

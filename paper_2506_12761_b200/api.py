@@ -26,10 +26,12 @@ def meta(mode, M, l_I, l_S, d, flags=L.CONFIG_FLAGS) -> VlpMeta:
     return VlpMeta(mode, M, l_I, l_S, d, flags)
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device=None) -> int:
+    """The raw cudaStream_t of `stream`; None -> the current torch stream of `device` (the server's GPU, not the
+    caller's current device)."""
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
@@ -153,7 +155,7 @@ class Server:
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             check(lib().vlp_server_create(device, keys.evk, ctypes.c_void_p(self.evk_dev.data_ptr()), nbytes,
-                                          _stream_handle(stream), ctypes.byref(h)))
+                                          _stream_handle(stream, device), ctypes.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -184,7 +186,7 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_server_workspace_bytes(ctypes.byref(m), count, None, None, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sh = _stream_handle(stream)
+        sh = _stream_handle(stream, self.device)
         sc = self._scratch(key, self._ws[key], sh)
         check(lib().vlp_server_eval(self.h, ctypes.byref(m), first, count, ctypes.c_void_p(query_dev.data_ptr()),
                                     ctypes.c_void_p(db_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
@@ -199,7 +201,7 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_server_batch_workspace_bytes(ctypes.byref(m), count, nq, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sh = _stream_handle(stream)
+        sh = _stream_handle(stream, self.device)
         sc = self._scratch(key, self._ws[key], sh)
         check(lib().vlp_server_eval_batch(self.h, ctypes.byref(m), nq, first, count,
                                           ctypes.c_void_p(queries_dev.data_ptr()), ctypes.c_void_p(db_dev.data_ptr()),
@@ -212,7 +214,7 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_server_combine_workspace_bytes(ctypes.byref(m), G, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sh = _stream_handle(stream)
+        sh = _stream_handle(stream, self.device)
         sc = self._scratch(key, self._ws[key], sh)
         check(lib().vlp_server_combine(self.h, ctypes.byref(m), G, ctypes.c_void_p(partials_dev.data_ptr()),
                                        ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(sc.data_ptr()),
@@ -226,7 +228,7 @@ class Server:
             sb = ctypes.c_size_t()
             check(lib().vlp_gate_batch_workspace_bytes(op, count, ctypes.byref(sb)))
             self._ws[key] = sb.value
-        sh = _stream_handle(stream)
+        sh = _stream_handle(stream, self.device)
         sc = self._scratch(key, self._ws[key], sh)
         p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
         check(lib().vlp_gate_batch(self.h, op, p(a_dev), p(b_dev), p(c_dev), p(out_dev), count,
@@ -239,7 +241,7 @@ class Server:
         scratch = torch.empty(max(256, lib().vlp_debug_scratch_bytes(count)), dtype=torch.uint8, device=in_dev.device)
         check(lib().vlp_debug_blind_rotate(self.h, ctypes.c_void_p(in_dev.data_ptr()), count, steps,
                                            ctypes.c_void_p(acc.data_ptr()), ctypes.c_void_p(scratch.data_ptr()),
-                                           _stream_handle(stream)))
+                                           _stream_handle(stream, self.device)))
         return acc
 
     def debug_keyswitch(self, nlwe_dev, stream=None):
@@ -249,7 +251,7 @@ class Server:
         scratch = torch.empty(max(256, lib().vlp_debug_scratch_bytes(count)), dtype=torch.uint8, device=nlwe_dev.device)
         check(lib().vlp_debug_keyswitch(self.h, ctypes.c_void_p(nlwe_dev.data_ptr()), count,
                                         ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(scratch.data_ptr()),
-                                        _stream_handle(stream)))
+                                        _stream_handle(stream, self.device)))
         return out
 
 
@@ -300,7 +302,7 @@ class Program:
     def eval(self, in0, in1, out, stream=None):
         p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
         check(lib().vlp_program_eval(self.h, ctypes.c_void_p(self.scratch.data_ptr()), self.scratch.numel(),
-                                     p(in0), p(in1), p(out), _stream_handle(stream)))
+                                     p(in0), p(in1), p(out), _stream_handle(stream, self.server.device)))
 
     def profile(self, enable: bool = True):
         check(lib().vlp_program_profile(self.h, 1 if enable else 0))

@@ -14,7 +14,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libvlp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["kernels.cu", "kernels_fft.cu", "api.cu"]
+CU = ["kernels.cu", "kernels_fft.cu", "kernels_ks.cu", "api.cu"]
 CXX = ["host.cpp", "sched.cpp"]
 HDR = ["vlp_internal.h", "kernels.cuh", "devcommon.cuh", os.path.join("..", "..", "include", "vlp.h")]
 
@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-pthread",
-                               "-lcublasLt", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
+                               "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
         os.replace(LIB + ".tmp", LIB)
     return LIB
 

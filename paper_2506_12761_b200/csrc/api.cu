@@ -1,7 +1,6 @@
 // api.cu -- the device half of the C ABI (include/vlp.h): server creation (evk upload + NTT conversion),
 // program compilation / binding / evaluation (one BR launch + one KS launch per circuit level),
 // and the debug entry points used by the parity tests.
-#include <cublasLt.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -24,18 +23,19 @@ struct vlp_server {
   uint2* tw_fwd = nullptr;   // natural order (bsk conversion)
   uint2* twl_fwd = nullptr;  // thread-layout tables of the blind-rotate kernel
   uint2* twl_inv = nullptr;
-  int8_t* kmat = nullptr;  // ksk as 4 signed byte limbs, [2528][24576] (tensor-core key switch)
+  int8_t* kmat = nullptr;  // ksk as 4 signed byte limbs in UMMA order (K3T key switch, kernels_ks.cu)
   double2* bsk_fft = nullptr;  // FFT-domain bsk of the K2F engine (2 x 16-bit limbs, scaled 1/512)
   double2* psi = nullptr;      // psi^e, e < 2048
-  cublasLtHandle_t lt = nullptr;
-  std::mutex algo_mu;
-  std::map<uint32_t, cublasLtMatmulAlgo_t> algos;  // cuBLASLt algorithm per GEMM row count
-  ~vlp_server() {
-    if (lt) cublasLtDestroy(lt);
-  }
   // programs compiled by the problem-statement calls (vlp_server_eval, vlp_server_combine, vlp_gate_batch)
   std::mutex mu;
-  std::map<std::string, std::unique_ptr<vlp_program>> cache;
+  // LRU-bounded (kMaxCachedPrograms): an evicted program (and its pinned job tables) is freed once the last call
+  // using it has returned (shared ownership)
+  struct Cached {
+    std::shared_ptr<vlp_program> prog;
+    uint64_t last_use = 0;
+  };
+  std::map<std::string, Cached> cache;
+  uint64_t use_clock = 0;
 };
 
 struct vlp_program {
@@ -43,7 +43,7 @@ struct vlp_program {
   vlp::Schedule sched;
   // scratch layout (byte offsets)
   size_t off_br = 0, off_ks = 0, off_lin = 0, off_lin_in = 0, off_outslots = 0, off_mid = 0, off_nlwe = 0, bytes = 0;
-  size_t off_ks_ws = 0;  // tensor-core key switch staging (ks_stage_bytes)
+  size_t off_ks_ws = 0;  // key-switch staging (abar + b' per job of a chunk, ks_stage_bytes)
   uint32_t ks_chunk = 0;
   std::vector<size_t> br_first, ks_first;  // per level, index of the level's first job
   std::vector<size_t> lin_first, lin_in_first;  // per level (R24 linear jobs and their input slots)
@@ -89,9 +89,24 @@ constexpr size_t kTwBytes = static_cast<size_t>(N) * sizeof(uint2);
 constexpr size_t kTwlBytes = static_cast<size_t>(kTwSlots) * kBT * sizeof(uint2);
 constexpr size_t kRawBskBytes = static_cast<size_t>(n) * kRows * 2 * N * 4;
 constexpr size_t kEvkBytes =
-    kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes + kKmatBytes + kBskFftBytes + kPsiBytes;
+    kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes + kKmatSwBytes + kBskFftBytes + kPsiBytes;
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+// Makes `device` current for one C call and restores the caller's current device on return (the library never
+// leaves a changed current device behind).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t set(int device) {
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return e;
+    return prev == device ? cudaSuccess : cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(VLP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -158,73 +173,12 @@ void make_layout_twiddles(const std::vector<uint2>& nat, std::vector<uint2>& lay
     }
 }
 
-// K3' key switch on the tensor cores, in chunks of at most `chunk` ciphertexts: one-hot digit indicator
-// (our kernel) -> D = ind x kmat^T as a cuBLASLt int8 GEMM with int32 accumulation (a plain library GEMM;
-// exact, |D| < 2^21) -> combine (our kernel).
-int ks_gemm(vlp_server* s, uint32_t rows, const int8_t* ind, int32_t* dmat, void* ws, cudaStream_t st) {
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, ld = nullptr;
-  int rc = VLP_OK;
-  const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-  const int32_t one = 1, zero = 0;
-  if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, kKsK, kKsNp, kKsK) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, kKsK, rows, kKsK) != CUBLAS_STATUS_SUCCESS ||
-      cublasLtMatrixLayoutCreate(&ld, CUDA_R_32I, kKsNp, rows, kKsNp) != CUBLAS_STATUS_SUCCESS) {
-    rc = fail(VLP_ECUDA, "cuBLASLt descriptor setup failed");
-  }
-  cublasLtMatmulAlgo_t algo{};
-  if (rc == VLP_OK) {
-    std::lock_guard<std::mutex> lock(s->algo_mu);
-    auto it = s->algos.find(rows);
-    if (it == s->algos.end()) {
-      cublasLtMatmulPreference_t pref = nullptr;
-      size_t wsb = kKsWsBytes;
-      cublasLtMatmulHeuristicResult_t h{};
-      int nres = 0;
-      if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS ||
-          cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb)) !=
-              CUBLAS_STATUS_SUCCESS ||
-          cublasLtMatmulAlgoGetHeuristic(s->lt, op, la, lb, ld, ld, pref, 1, &h, &nres) != CUBLAS_STATUS_SUCCESS ||
-          nres == 0)
-        rc = fail(VLP_ECUDA, "no cuBLASLt int8 algorithm for the key-switch GEMM");
-      else
-        it = s->algos.emplace(rows, h.algo).first;
-      if (pref) cublasLtMatmulPreferenceDestroy(pref);
-    }
-    if (rc == VLP_OK) algo = it->second;
-  }
-  if (rc == VLP_OK &&
-      cublasLtMatmul(s->lt, op, &one, s->kmat, la, ind, lb, &zero, dmat, ld, dmat, ld, &algo, ws, kKsWsBytes, st) !=
-          CUBLAS_STATUS_SUCCESS)
-    rc = fail(VLP_ECUDA, "cuBLASLt key-switch GEMM failed");
-  if (ld) cublasLtMatrixLayoutDestroy(ld);
-  if (lb) cublasLtMatrixLayoutDestroy(lb);
-  if (la) cublasLtMatrixLayoutDestroy(la);
-  if (op) cublasLtMatmulDescDestroy(op);
-  return rc;
-}
-
 int run_keyswitch(vlp_server* s, const KsArgs& ka, uint8_t* stage, uint32_t chunk, cudaStream_t st) {
-  // stage: [cuBLASLt workspace][indicator chunk x 24576][D chunk x 2528 int32]
-  void* ws = stage;
-  int8_t* ind = reinterpret_cast<int8_t*>(stage + align256(kKsWsBytes));
-  int32_t* dmat = reinterpret_cast<int32_t*>(stage + align256(kKsWsBytes) + align256(static_cast<size_t>(chunk) * kKsK));
-  cudaError_t e;
-  for (uint32_t c0 = 0; c0 < ka.njobs; c0 += chunk) {
-    const uint32_t cnt = std::min(chunk, ka.njobs - c0);
-    if ((e = launch_ks_indicator(ka, c0, cnt, ind, st))) return cuda_fail(e, "key-switch indicator");
-    if (int rc = ks_gemm(s, cnt, ind, dmat, ws, st)) return rc;
-    if ((e = launch_ks_combine(ka, c0, cnt, dmat, st))) return cuda_fail(e, "key-switch combine");
-  }
+  if (cudaError_t e = launch_keyswitch_t(ka, s->kmat, stage, chunk, s->sm_count, st)) return cuda_fail(e, "key switch");
   return VLP_OK;
 }
 
-size_t ks_stage_bytes(uint32_t chunk) {
-  return align256(kKsWsBytes) + align256(static_cast<size_t>(chunk) * kKsK) + align256(static_cast<size_t>(chunk) * kKsNp * 4);
-}
+size_t ks_stage_bytes(uint32_t chunk) { return ks_stage_bytes_t(chunk); }
 
 Regions regions(const vlp_program* p, void* scratch, const uint32_t* in0, const uint32_t* in1, uint32_t* out) {
   Regions r;
@@ -264,7 +218,7 @@ int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
   p->bytes = p->off_ks_ws + ks_stage_bytes(p->ks_chunk);
   p->server = server;
   p->launches = 1 + (p->copy_slots.empty() ? 0 : 1);
-  for (auto& L : s.levels) {  // our kernels: BR waves + (indicator, combine) per key-switch GEMM chunk
+  for (auto& L : s.levels) {  // our kernels: BR waves + (prologue, tcgen05 GEMM) per key-switch chunk
     p->launches += br_launch_count(static_cast<uint32_t>(L.br.size()), server ? server->sm_count : 148) +
                    2 * static_cast<uint32_t>((L.ks.size() + p->ks_chunk - 1) / p->ks_chunk) + (L.lin.empty() ? 0 : 1);
   }
@@ -323,7 +277,8 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   if (evk_bytes < kEvkBytes) return fail(VLP_ENOMEM, "evk buffer too small");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(VLP_ENODEV, "no CUDA device");
-  if (cudaError_t e = cudaSetDevice(device)) return cuda_fail(e, "cudaSetDevice");
+  DeviceGuard dg;
+  if (cudaError_t e = dg.set(device)) return cuda_fail(e, "cudaSetDevice");
   auto srv = std::make_unique<vlp_server>();
   srv->device = device;
   cudaDeviceGetAttribute(&srv->sm_count, cudaDevAttrMultiProcessorCount, device);
@@ -337,9 +292,8 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   srv->twl_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes + kTwlBytes);
   uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes);
   srv->kmat = reinterpret_cast<int8_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes);
-  srv->bsk_fft = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->kmat) + kKmatBytes);
+  srv->bsk_fft = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->kmat) + kKmatSwBytes);
   srv->psi = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->bsk_fft) + kBskFftBytes);
-  if (cublasLtCreate(&srv->lt) != CUBLAS_STATUS_SUCCESS) return fail(VLP_ECUDA, "cublasLtCreate failed");
 
   std::vector<uint2> fwd, inv, lf, li;
   make_twiddles(fwd, inv);
@@ -362,7 +316,7 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   set_fft_constants(psi.data());
   if ((e = cudaMemcpyAsync(srv->psi, psi.data(), kPsiBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "psi");
   launch_bsk_fft(raw, srv->bsk_fft, srv->psi, st);
-  launch_ksk_to_i8(srv->ksk, srv->kmat, st);
+  launch_kmat_sw(srv->ksk, srv->kmat, st);
   if ((e = cudaGetLastError())) return cuda_fail(e, "bsk convert launch");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server create");
   *out = srv.release();
@@ -519,7 +473,8 @@ int vlp_program_eval(vlp_program* p, void* scratch, size_t scratch_bytes, const 
     return fail(VLP_EINVAL, "missing input / output buffer");
   vlp_server* s = p->server;
   cudaError_t e;
-  if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+  DeviceGuard dg;
+  if ((e = dg.set(s->device))) return cuda_fail(e, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* sc = static_cast<uint8_t*>(scratch);
   if (int rc = stage_tables(p)) return rc;
@@ -625,7 +580,8 @@ int vlp_debug_blind_rotate(vlp_server* s, const uint32_t* in_dev, size_t count, 
   if (count == 0) return VLP_OK;
   if (steps < 0 || steps > n) return fail(VLP_EINVAL, "steps out of range");
   cudaError_t e;
-  if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+  DeviceGuard dg;
+  if ((e = dg.set(s->device))) return cuda_fail(e, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   std::vector<BrJob> jobs(count);
   for (size_t i = 0; i < count; i++) jobs[i] = BrJob{slot(kRegIn0, static_cast<uint32_t>(i)), 0, 0, 1, 0, 0, static_cast<uint32_t>(i)};
@@ -652,7 +608,8 @@ int vlp_debug_keyswitch(vlp_server* s, const uint32_t* nlwe_dev, size_t count, u
   if (!s || !scratch || (count && (!nlwe_dev || !out_dev))) return fail(VLP_EINVAL, "null argument");
   if (count == 0) return VLP_OK;
   cudaError_t e;
-  if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+  DeviceGuard dg;
+  if ((e = dg.set(s->device))) return cuda_fail(e, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   std::vector<KsJob> jobs(count);
   for (size_t i = 0; i < count; i++)
@@ -680,17 +637,25 @@ static std::string meta_key(const char* kind, const vlp_meta& m, size_t a, size_
          std::to_string(m.flags) + "," + std::to_string(a) + "," + std::to_string(b);
 }
 
+constexpr size_t kMaxCachedPrograms = 16;
 template <class Make>
-static int cached_program(vlp_server* s, const std::string& key, Make make, vlp_program** out) {
+static int cached_program(vlp_server* s, const std::string& key, Make make, std::shared_ptr<vlp_program>* out) {
   return no_throw([&] {
     std::lock_guard<std::mutex> lock(s->mu);
     auto it = s->cache.find(key);
     if (it == s->cache.end()) {
       vlp_program* p = nullptr;
       if (int rc = make(&p)) return rc;
-      it = s->cache.emplace(key, std::unique_ptr<vlp_program>(p)).first;
+      if (s->cache.size() >= kMaxCachedPrograms) {  // evict the least recently used schedule
+        auto lru = s->cache.begin();
+        for (auto c = s->cache.begin(); c != s->cache.end(); ++c)
+          if (c->second.last_use < lru->second.last_use) lru = c;
+        s->cache.erase(lru);
+      }
+      it = s->cache.emplace(key, vlp_server::Cached{std::shared_ptr<vlp_program>(p), 0}).first;
     }
-    *out = it->second.get();
+    it->second.last_use = ++s->use_clock;
+    *out = it->second.prog;
     return static_cast<int>(VLP_OK);
   });
 }
@@ -715,11 +680,11 @@ int vlp_server_eval(vlp_server* s, const vlp_meta* meta, size_t first, size_t co
                     const uint32_t* db_dev, uint32_t* out_dev, void* scratch, size_t scratch_bytes,
                     uint64_t stream) {
   if (!s || !meta) return fail(VLP_EINVAL, "null argument");
-  vlp_program* p = nullptr;
+  std::shared_ptr<vlp_program> p;
   if (int rc = cached_program(s, meta_key("eval", *meta, first, count),
                               [&](vlp_program** o) { return vlp_program_create(s, meta, first, count, o); }, &p))
     return rc;
-  return vlp_program_eval(p, scratch, scratch_bytes, query_dev, db_dev, out_dev, stream);
+  return vlp_program_eval(p.get(), scratch, scratch_bytes, query_dev, db_dev, out_dev, stream);
 }
 
 int vlp_server_batch_workspace_bytes(const vlp_meta* meta, size_t count, uint32_t nq, size_t* scratch_bytes) {
@@ -735,12 +700,12 @@ int vlp_server_eval_batch(vlp_server* s, const vlp_meta* meta, uint32_t nq, size
                           const uint32_t* queries_dev, const uint32_t* db_dev, uint32_t* out_dev, void* scratch,
                           size_t scratch_bytes, uint64_t stream) {
   if (!s || !meta) return fail(VLP_EINVAL, "null argument");
-  vlp_program* p = nullptr;
+  std::shared_ptr<vlp_program> p;
   if (int rc = cached_program(s, meta_key("batch", *meta, first, count) + "," + std::to_string(nq),
                               [&](vlp_program** o) { return vlp_program_create_queries(s, meta, first, count, nq, o); },
                               &p))
     return rc;
-  return vlp_program_eval(p, scratch, scratch_bytes, queries_dev, db_dev, out_dev, stream);
+  return vlp_program_eval(p.get(), scratch, scratch_bytes, queries_dev, db_dev, out_dev, stream);
 }
 
 int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t* scratch_bytes) {
@@ -755,11 +720,11 @@ int vlp_server_combine_workspace_bytes(const vlp_meta* meta, uint32_t G, size_t*
 int vlp_server_combine(vlp_server* s, const vlp_meta* meta, uint32_t G, const uint32_t* partials_dev,
                        uint32_t* out_dev, void* scratch, size_t scratch_bytes, uint64_t stream) {
   if (!s || !meta) return fail(VLP_EINVAL, "null argument");
-  vlp_program* p = nullptr;
+  std::shared_ptr<vlp_program> p;
   if (int rc = cached_program(s, meta_key("combine", *meta, G, 0),
                               [&](vlp_program** o) { return vlp_program_create_combine(s, meta, G, o); }, &p))
     return rc;
-  return vlp_program_eval(p, scratch, scratch_bytes, partials_dev, nullptr, out_dev, stream);
+  return vlp_program_eval(p.get(), scratch, scratch_bytes, partials_dev, nullptr, out_dev, stream);
 }
 
 int vlp_gate_batch_workspace_bytes(int op, size_t count, size_t* scratch_bytes) {
@@ -780,7 +745,7 @@ int vlp_gate_batch(vlp_server* s, int op, const uint32_t* a_dev, const uint32_t*
   if (!s || !scratch || (count && (!a_dev || !b_dev || !out_dev || (op == VLP_MUX && !c_dev))))
     return fail(VLP_EINVAL, "null argument");
   if (count == 0) return VLP_OK;
-  vlp_program* p = nullptr;
+  std::shared_ptr<vlp_program> p;
   if (int rc = cached_program(s, "gates:" + std::to_string(op) + "," + std::to_string(count),
                               [&](vlp_program** o) { return vlp_program_create_gates(s, op, count, o); }, &p))
     return rc;
@@ -791,13 +756,14 @@ int vlp_gate_batch(vlp_server* s, int op, const uint32_t* a_dev, const uint32_t*
     uint32_t* st_bc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + prog_bytes);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    if ((e = cudaSetDevice(s->device))) return cuda_fail(e, "cudaSetDevice");
+    DeviceGuard dg;
+  if ((e = dg.set(s->device))) return cuda_fail(e, "cudaSetDevice");
     if ((e = cudaMemcpyAsync(st_bc, b_dev, count * kCt * 4, cudaMemcpyDeviceToDevice, st)) ||
         (e = cudaMemcpyAsync(st_bc + count * kCt, c_dev, count * kCt * 4, cudaMemcpyDeviceToDevice, st)))
       return cuda_fail(e, "stage mux operands");
     in1 = st_bc;
   }
-  return vlp_program_eval(p, scratch, scratch_bytes, a_dev, in1, out_dev, stream);
+  return vlp_program_eval(p.get(), scratch, scratch_bytes, a_dev, in1, out_dev, stream);
 }
 
 void vlp_free_server(vlp_server* s) { delete s; }

@@ -9,8 +9,8 @@
 //                               (one accumulator component per SM, DSMEM exchange of the MAC inputs)
 //  K2 vlp_blind_rotate_c6_kernel : a tail of <= 1 bootstrap per resident 6-CTA cluster, one bootstrap on 6
 //                               SMs (one digit polynomial and one output limb per SM)
-//  K3 vlp_ks_indicator_kernel + cuBLASLt int8 GEMM + vlp_ks_combine_kernel : MUX combine (S7) + key
-//                               switch (S8) as a one-hot-indicator x byte-limb-ksk GEMM on the tensor cores
+//  K3T (kernels_ks.cu)         : MUX combine (S7) + key switch (S8) as a hand-written tcgen05 int8 GEMM
+//  K2F (kernels_fft.cu)        : the blind rotation on an exact FP64 FFT (whole waves)
 //  K4 vlp_bsk_convert_kernel  : bsk -> 3-limb NTT domain (setup)
 //  K5 vlp_linear_kernel       : R24 linear aggregation (exact ciphertext sums; option outside the paper)
 //  vlp_encrypt_db_kernel      : device PubKeyGen + ServerEnc (setup)
@@ -1174,69 +1174,6 @@ __global__ void __cluster_dims__(kC6, 1, 1) __launch_bounds__(kBT, 1) vlp_blind_
   cl.sync();  // peers may still read this CTA's limbs
 }
 
-// ================================================================================ K3' key switch on tensor cores
-// (a) one-hot digit indicator: CTA per ciphertext; coefficient i -> 24 bytes ind[c][i*24 + j*3 + v-1].
-//     MUX combine (S7) and the 16-bit rounding (R6) in the prologue, as in K3.
-__global__ void __launch_bounds__(256) vlp_ks_indicator_kernel(const KsArgs a, uint32_t c0, int8_t* __restrict__ ind) {
-  const uint32_t c = blockIdx.x;
-  const KsJob job = a.jobs[c0 + c];
-  const uint32_t* x0 = a.nlwe + static_cast<size_t>(job.n0) * kNlwe;
-  const uint32_t* x1 = job.n1 != 0xFFFFFFFFu ? a.nlwe + static_cast<size_t>(job.n1) * kNlwe : nullptr;
-  uint2* row = reinterpret_cast<uint2*>(ind + static_cast<size_t>(c) * kKsK);
-  for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(N); i += blockDim.x) {
-    uint32_t v = x0[i];
-    if (x1) v += x1[i];
-    const uint32_t ab = (v + (1u << 15)) >> 16;  // 16-bit rounded mask (R6)
-    uint64_t w[3] = {0, 0, 0};
-#pragma unroll
-    for (int j = 0; j < kKsT; j++) {
-      const uint32_t dg = (ab >> (14 - 2 * j)) & 3u;  // most significant digit first
-      if (dg) {
-        const int byte = j * 3 + static_cast<int>(dg) - 1;
-        w[byte >> 3] |= 1ull << (8 * (byte & 7));
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 3; q++) row[i * 3 + q] = make_uint2(static_cast<uint32_t>(w[q]), static_cast<uint32_t>(w[q] >> 32));
-  }
-}
-
-// (b) combine: out = (0, b' + add) - sum_l D_l << 8l (mod 2^32), pad word 0.  CTA per ciphertext.
-__global__ void __launch_bounds__(256) vlp_ks_combine_kernel(const KsArgs a, uint32_t c0, const int32_t* __restrict__ d) {
-  const uint32_t c = blockIdx.x;
-  const KsJob job = a.jobs[c0 + c];
-  const int32_t* dr = d + static_cast<size_t>(c) * kKsNp;
-  uint32_t* o = slot_wptr(a.reg, job.out);
-  for (uint32_t col = threadIdx.x; col < static_cast<uint32_t>(kCt); col += blockDim.x) {
-    uint32_t v = 0;
-    if (col <= static_cast<uint32_t>(n)) {
-      const uint32_t s = static_cast<uint32_t>(dr[col]) + (static_cast<uint32_t>(dr[kCt + col]) << 8) +
-                         (static_cast<uint32_t>(dr[2 * kCt + col]) << 16) + (static_cast<uint32_t>(dr[3 * kCt + col]) << 24);
-      uint32_t b = 0;
-      if (col == static_cast<uint32_t>(n)) {
-        b = a.nlwe[static_cast<size_t>(job.n0) * kNlwe + N] + job.add;
-        if (job.n1 != 0xFFFFFFFFu) b += a.nlwe[static_cast<size_t>(job.n1) * kNlwe + N];
-      }
-      v = b - s;
-    }
-    o[col] = v;
-  }
-}
-
-// (c) setup: kmat[l*632 + col][k] = signed byte limb l of ksk row k (k = (i*8 + j)*3 + v-1), column col.
-__global__ void vlp_ksk_to_i8_kernel(const uint32_t* __restrict__ ksk, int8_t* __restrict__ kmat) {
-  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<size_t>(kKsK) * kCt) return;
-  const uint32_t k = static_cast<uint32_t>(idx / kCt), col = static_cast<uint32_t>(idx % kCt);
-  int64_t x = static_cast<int64_t>(ksk[idx]);  // row k, column col of the [K][632] ksk
-#pragma unroll
-  for (int l = 0; l < 4; l++) {
-    const int64_t s = ((x + 128) & 255) - 128;  // balanced limb in [-128, 128)
-    kmat[(static_cast<size_t>(l) * kCt + col) * kKsK + k] = static_cast<int8_t>(s);
-    x = (x - s) >> 8;
-  }
-}
-
 // ================================================================================ device PubKeyGen + ServerEnc
 // (setup) one warp per DB ciphertext: the TLWE(0) public-key sample of alg:PubKeyGen
 // (mask words from the counter PRNG of R3, b = <a, s> + e with e computed on the host by the same libm
@@ -1610,20 +1547,8 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
   return e;
 }
 
-void launch_ksk_to_i8(const uint32_t* ksk, int8_t* kmat, cudaStream_t st) {
-  const size_t total = static_cast<size_t>(kKsK) * kCt;
-  vlp_ksk_to_i8_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(ksk, kmat);
-}
 
-cudaError_t launch_ks_indicator(const KsArgs& a, uint32_t c0, uint32_t cnt, int8_t* ind, cudaStream_t st) {
-  if (cnt) vlp_ks_indicator_kernel<<<cnt, 256, 0, st>>>(a, c0, ind);
-  return cudaGetLastError();
-}
 
-cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const int32_t* d, cudaStream_t st) {
-  if (cnt) vlp_ks_combine_kernel<<<cnt, 256, 0, st>>>(a, c0, d);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st) {
   vlp_init_constants_kernel<<<1, 256, 0, st>>>(mid);

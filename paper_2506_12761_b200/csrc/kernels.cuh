@@ -34,15 +34,15 @@ static_assert(kBrBoot * kTmemSlotCols <= 512, "TMEM columns");
 static_assert(kBrSmemBytes <= 232448, "shared memory per CTA");
 
 
-// ---- key switch on the tensor cores (K3'): out = (0, b') - sum_{i,j} ksk[i][j][d_ij] written as a GEMM
-// D[c][l*632 + col] = sum_k ind[c][k] * kmat[l*632 + col][k] with the one-hot digit indicator
-// ind[c][(i*8 + j)*3 + v-1] = [d_ij == v] (int8) and kmat = the ksk split into 4 balanced signed byte limbs
-// (int8, |D| <= 8192 * 128 < 2^31: exact), then out = (0, b') - sum_l D_l 2^(8l) mod 2^32.
+// ---- key switch on the tensor cores (K3T, kernels_ks.cu): out = (0, b') - sum_{i,j} ksk[i][j][d_ij] as a
+// hand-written tcgen05 int8 GEMM D[c][n] = sum_k ind[c][k] * kmat[n][k] with the one-hot digit indicator
+// (generated in shared memory) and kmat = the ksk split into 4 balanced signed byte limbs, n = col * 4 + limb;
+// |D| <= 8192 * 128 < 2^31: exact; out[col] = (col == n ? b' : 0) - sum_l D[c][4 col + l] 2^(8l) mod 2^32.
 constexpr int kKsK = N * kKsT * 3;               // 24576 GEMM depth
-constexpr int kKsNp = 4 * kCt;                   // 2528 GEMM columns (4 limbs x 632)
-constexpr size_t kKmatBytes = static_cast<size_t>(kKsNp) * kKsK;  // 62,128,128
-constexpr int kKsChunk = 8192;                   // ciphertexts per GEMM
-constexpr size_t kKsWsBytes = 32u << 20;         // cuBLASLt workspace
+constexpr int kKsNp = 4 * kCt;                   // 2528 GEMM columns (632 columns x 4 limbs)
+constexpr int kKsNt = (kKsNp + 255) / 256;       // 10 N tiles of 256
+constexpr size_t kKmatSwBytes = static_cast<size_t>(kKsNt) * 256 * kKsK;  // 62,914,560 (UMMA-ordered, zero-padded)
+constexpr int kKsChunk = 32768;                  // jobs per key-switch launch pair (staging 2 KB + 4 B per job)
 
 struct Regions {
   uint32_t* base[4];  // kRegIn0, kRegIn1, kRegMid, kRegOut; rows of kCt words
@@ -93,9 +93,11 @@ int set_br_route(int engine, int param);  // vlp_debug_route
 int br_launch_count(uint32_t njobs, int sm_count);
 cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
                               uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st);
-void launch_ksk_to_i8(const uint32_t* ksk, int8_t* kmat, cudaStream_t st);
-cudaError_t launch_ks_indicator(const KsArgs& a, uint32_t c0, uint32_t cnt, int8_t* ind, cudaStream_t st);
-cudaError_t launch_ks_combine(const KsArgs& a, uint32_t c0, uint32_t cnt, const int32_t* d, cudaStream_t st);
+void launch_kmat_sw(const uint32_t* ksk, int8_t* kmat_sw, cudaStream_t st);
+size_t ks_stage_bytes_t(uint32_t chunk);
+// K3T over all jobs of a level in chunks of `chunk`: prologue (S7 + R6) + tcgen05 GEMM with fused epilogue
+cudaError_t launch_keyswitch_t(const KsArgs& a, const int8_t* kmat_sw, uint8_t* stage, uint32_t chunk, int sm_count,
+                               cudaStream_t st);
 cudaError_t launch_init_constants(uint32_t* mid, cudaStream_t st);
 cudaError_t launch_copy_rows(const uint32_t* slots, uint32_t count, Regions reg, uint32_t* out, cudaStream_t st);
 cudaError_t launch_linear(const LinJob* jobs, const uint32_t* inputs, uint32_t count, Regions reg, cudaStream_t st);

@@ -101,14 +101,9 @@ __device__ __forceinline__ void dft16_inv(cd (&v)[16]) {
 __device__ __forceinline__ cd shfl16(cd v) {
   return {__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16)};
 }
-__device__ __forceinline__ cd sel(bool p, cd a, cd b) { return p ? a : b; }
 
 // Gadget digit field f = (w >> s) & 127 (R5: w = D + 0x81020400) enters the FFT as the double f - 64, exactly:
 // (2^52 + f) - (2^52 + 64), the first term built by putting f into the low mantissa word of 2^52 (fft_fwd).
-// round(v) mod 2^32 for |v| < 2^51 (1.5 * 2^52 shifts the integer part into the low mantissa word)
-__device__ __forceinline__ uint32_t round_u32(double v) {
-  return static_cast<uint32_t>(__double2loint(v + 6755399441055744.0));
-}
 
 // Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
 // 32 q + lane, q < 32) -> X[rho] = point lane + 32 mrev(rho).
@@ -187,7 +182,7 @@ __device__ __forceinline__ void fft_inv(cd (&v)[16], const Lane& c, double2* tr)
 #pragma unroll
   for (int a = 1; a < 16; a++) v[a] = cmulc(v[a], c_twist[a]);
 }
-// round(sgn^a v) mod 2^32 (see fft_inv)
+// round(sgn^a v) mod 2^32 (see fft_inv): 1.5 * 2^52 shifts the integer part of |v| < 2^51 into the low mantissa word
 template <int A>
 __device__ __forceinline__ uint32_t round_u32s(double v, const Lane& c) {
   return static_cast<uint32_t>(__double2loint((A & 1) ? fma(c.sgn, v, 6755399441055744.0) : v + 6755399441055744.0));

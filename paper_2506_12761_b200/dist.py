@@ -2,7 +2,7 @@
 
 Records split into contiguous power-of-two shards [r*M/G, (r+1)*M/G), one per rank (process per GPU).  Per
 query: the query ciphertexts are broadcast from rank 0, every rank evaluates its shard down to the shard's
-aggregation-tree root (l_S ciphertexts), the roots are gathered, and rank 0 runs the top log2 G tree levels
+aggregation-tree root (l_S ciphertexts), the roots are gathered to rank 0 (a gather, not an all-gather: only rank 0 combines), and rank 0 runs the top log2 G tree levels
 (vlp_program_create_combine).  Because the tree pairs (i, i+k) never cross a power-of-two shard boundary
 for k < M/G, the result is byte-identical to the single-GPU evaluation.  torch.distributed is plumbing only
 (NCCL on GPUs; gloo in the CPU tests); the evaluation callbacks are the library's kernels.
@@ -25,8 +25,8 @@ def shard_range(M: int, world: int, rank: int):
 
 
 def sharded_step(q, eval_shard, combine, world: int, rank: int, gathered=None):
-    """One query: broadcast q (rank 0's), eval_shard(q) -> shard root tensor [l_S, 632], gather all roots,
-    rank 0 returns combine(roots [G*l_S, 632]); other ranks return None.  Single rank: eval_shard(q)."""
+    """One query: broadcast q (rank 0's), eval_shard(q) -> shard root tensor [l_S, 632], gather all roots to
+    rank 0, which returns combine(roots [G*l_S, 632]); other ranks return None.  Single rank: eval_shard(q)."""
     if world == 1:
         return eval_shard(q)
     import torch
@@ -35,7 +35,8 @@ def sharded_step(q, eval_shard, combine, world: int, rank: int, gathered=None):
     part = eval_shard(q)
     if gathered is None:  # concatenated along dim 0: [G * l_S, 632] (rank order = shard order)
         gathered = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype, device=part.device)
-    dist.all_gather_into_tensor(gathered, part.contiguous())
     if rank == 0:
+        dist.gather(part.contiguous(), gather_list=list(gathered.chunk(world, dim=0)), dst=0)
         return combine(gathered)
+    dist.gather(part.contiguous(), dst=0)
     return None

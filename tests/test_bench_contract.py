@@ -25,10 +25,24 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["metric"] == "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
-    assert d["config"]["workload"] == "cfg2_intv1d_1024"  # the same config as the GPU arm's default line
+    assert d["config"]["workload"] == "cfg3_rect2d_4096"  # the same config as the GPU arm's default line (config 3)
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
 def test_reference_arm_other_ranks_exit_quietly():
     assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, "--steps", "1", "--warmup", "0") == []
+
+
+def test_algorithmic_ops_per_br_is_survey_8d():
+    """roofline.frac's numerator follows SURVEY 8(d): 5,040 transforms (25.8 M butterflies) + 7.74 M MACs per BR
+    at the stated per-op costs (7 / butterfly, 2 / MAC, 15 / digit coefficient, 19 / lifted coefficient)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    butterflies = 630 * 8 * 5120
+    macs = 630 * 12 * 1024
+    assert butterflies == 25_804_800 and macs == 7_741_440
+    assert bench.alg_ops_per_br() == butterflies * 7 + macs * 2 + 630 * 2048 * (15 + 19) == 239_984_640
+    peak, how = bench.int_peak()
+    assert how.startswith("measured") and 25_000 < peak < 40_000  # profiles/int_peak_r1.json, Gop/s
+    assert 17_000 < bench.fp64_peak() < 19_000  # profiles/fp64_bench_r2.json

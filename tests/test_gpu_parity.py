@@ -1,9 +1,11 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
 
-Bit-exact everywhere (all arithmetic is integer: torus32 and the NTT primes).  Sizes span several CTAs
-(5 bootstraps each in whole waves, 1-4 in the narrower tail wave of a level) with ragged tails; full-size configs are checked on sampled outputs the oracle
-recomputes one by one plus properties that hold at any size (decrypted predicate, all-trivial closed
-form P11)."""
+Bit-exact everywhere: torus32 integer arithmetic, with the external product computed exactly by either engine --
+K2F (FP64 negacyclic FFT, 2 x 16-bit key limbs, rounding error far below 1/2: DESIGN.md section 4) for whole
+waves of 8 bootstraps per SM, the NTT kernels (K2, latency / cluster kernels) for narrow tails and on request
+(vlp_debug_route).  Sizes span several CTAs and tiles with ragged tails; full-size configs are checked on sampled
+outputs the oracle recomputes one by one plus properties that hold at any size (decrypted predicate,
+all-trivial closed form P11)."""
 import ctypes
 import os
 import random
@@ -42,9 +44,72 @@ def rand_tlwe(rng, count):
     return rng.integers(0, 2 ** 32, (count, 632), dtype=np.uint64).astype(np.uint32)
 
 
-def test_blind_rotate_steps_bit_exact(server, okeys):
-    """K2 after 1, 2 and 7 CMux steps (raw TRLWE accumulator) == oracle BlindRotate, 9 inputs (3 CTAs,
+@pytest.fixture
+def route():
+    """Force a blind-rotation route for one test (vlp_debug_route), restore the default afterwards."""
+    def set_route(engine, param=0):
+        assert L.lib().vlp_debug_route(engine, param) == 0
+    yield set_route
+    L.lib().vlp_debug_route(0, 0)
+
+
+@pytest.mark.parametrize("warps", [1, 3, 8])
+def test_fft_engine_steps_bit_exact(server, okeys, route, warps):
+    """K2F (FP64 FFT engine) with 1 / 3 / 8 warps (bootstraps) per CTA after 1, 2 and 7 CMux steps == oracle
+    BlindRotate: 19 inputs (ragged groups; idle warps in the last CTA), uniformly random masks plus one trivial
+    input."""
+    route(2, warps)
+    rng = np.random.default_rng(10 + warps)
+    cts = rand_tlwe(rng, 19)
+    cts[:, 631] = 0
+    cts[6, :630] = 0
+    dev = A.to_device(cts)
+    for steps in (1, 2, 7):
+        got = A.to_host(server.debug_blind_rotate(dev, steps))
+        want = list(POOL.map(lambda c: okeys.blind_rotate(c[:631], steps), cts))
+        for i in range(len(cts)):
+            assert np.array_equal(got[i], want[i]), (warps, steps, i, np.flatnonzero(got[i] != want[i])[:8])
+
+
+def test_fft_engine_full_630_and_extreme_digits(server, okeys, route):
+    """K2F over all 630 steps on fresh encryptions and on inputs whose first steps see extreme gadget digits
+    (accumulator words near +-2^31 give digits of magnitude 64: the largest FFT inputs), byte-equal to the
+    oracle; and the same level run by the NTT engine gives the same bytes."""
+    k = server.keys
+    cts = np.concatenate([k.encrypt_bits([1, 0, 1, 1, 0], 93),
+                          rand_tlwe(np.random.default_rng(4), 4)])
+    cts[5:, 631] = 0x80000000  # b = 1/2: the test vector rotates by 1024 -> acc = +-mu everywhere, D = +-2 mu
+    route(2, 8)
+    got = A.to_host(server.debug_blind_rotate(A.to_device(cts), 630))
+    want = list(POOL.map(lambda c: okeys.blind_rotate(c[:631], 630), cts))
+    for i in range(len(cts)):
+        assert np.array_equal(got[i], want[i]), i
+    route(1, 5)
+    assert np.array_equal(A.to_host(server.debug_blind_rotate(A.to_device(cts), 630)), got)
+
+
+@pytest.mark.parametrize("extra", [0, 1, 150, 1183])
+def test_default_route_wave_and_tail_bit_exact(server, okeys, extra):
+    """The default routing of a level (K2F whole waves of 8 x SMs, then the tail on K2F with fewer warps or on the
+    NTT latency kernels): 2 CMux steps on 8 x 148 + extra inputs; sampled rows on both sides of the split and the
+    ragged end byte-equal to the oracle."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    count = 8 * sms + extra
+    rng = np.random.default_rng(100 + extra)
+    cts = rand_tlwe(rng, count)
+    cts[:, 631] = 0
+    got = A.to_host(server.debug_blind_rotate(A.to_device(cts), 2))
+    idx = sorted(set([i for i in (0, 7, 8, 8 * sms - 1, 8 * sms, 8 * sms + 1) if i < count] + [count - 2, count - 1] +
+                     random.Random(extra).sample(range(count), 8)))
+    want = list(POOL.map(lambda i: okeys.blind_rotate(cts[i, :631], 2), idx))
+    for i, w in zip(idx, want):
+        assert np.array_equal(got[i], w), (extra, i)
+
+
+def test_blind_rotate_steps_bit_exact(server, okeys, route):
+    """K2 (NTT engine, forced) after 1, 2 and 7 CMux steps (raw TRLWE accumulator) == oracle BlindRotate, 9 inputs (3 CTAs,
     ragged), uniformly random masks (every abar_i != 0 path) plus one trivial input."""
+    route(1, 0)
     rng = np.random.default_rng(1)
     cts = rand_tlwe(rng, 9)
     cts[:, 631] = 0
@@ -58,11 +123,12 @@ def test_blind_rotate_steps_bit_exact(server, okeys):
 
 
 @pytest.mark.parametrize("tail", [1, 50, 100, 150, 300, 600])
-def test_blind_rotate_wave_split_bit_exact(server, okeys, tail):
-    """A level of 5 x 148 + tail blind rotations runs as one whole wave (5 bootstraps per CTA) plus a tail
-    wave (kernels.cu launch_blind_rotate): tail 1 on the 6-CTA cluster kernel, 50 on the 2-CTA cluster
-    kernel, 100 on the 6-group latency kernel, 150 / 300 / 600 on 2 / 3 / 5 bootstraps per CTA.  2 CMux
+def test_blind_rotate_wave_split_bit_exact(server, okeys, route, tail):
+    """NTT engine (forced): a level of 5 x 148 + tail blind rotations runs as one whole wave (5 bootstraps per
+    CTA) plus a tail wave (kernels.cu launch_blind_rotate): tail 1 on the 6-CTA cluster kernel, 50 on the 2-CTA
+    cluster kernel, 100 on the 6-group latency kernel, 150 / 300 / 600 on 2 / 3 / 5 bootstraps per CTA.  2 CMux
     steps; sampled rows on both sides of the split and the ragged end byte-equal to the oracle."""
+    route(1, 0)
     count = 740 + tail
     rng = np.random.default_rng(tail)
     cts = rand_tlwe(rng, count)
@@ -84,9 +150,11 @@ def test_blind_rotate_full_bit_exact(server, okeys):
         assert np.array_equal(got[i], want[i]), i
 
 
-@pytest.mark.parametrize("count", [1, 17, 70])
+@pytest.mark.parametrize("count", [1, 17, 130, 300])
 def test_keyswitch_bit_exact(server, okeys, count):
-    """K3 on random N-LWE rows: 1 (16 coefficient splits), 17 (2 tiles, ragged), 70 (5 tiles)."""
+    """K3T (tcgen05 int8 GEMM key switch) on random N-LWE rows: 1 job (one M tile, 127 idle rows), 17, 130 (two
+    M tiles, ragged) and 300 (three M tiles; 30 tiles over the 10 N tiles, persistent CTAs): every output word
+    byte-equal to the oracle's KeySwitch (R6), pad word 0."""
     rng = np.random.default_rng(count)
     nl = rng.integers(0, 2 ** 32, (count, 1028), dtype=np.uint64).astype(np.uint32)
     nl[:, 1025:] = 0
@@ -229,7 +297,7 @@ def test_all_trivial_closed_form_full_size(server, cfg):
     assert [int(x) for x in out[:, 630]] == [0x20000000 if (want >> j) & 1 else 0xE0000000 for j in range(wl.l_S)]
 
 
-def _full_size_sampled(server, cfg, sample, keep_all=True):
+def _full_size_sampled(server, cfg, sample, keep_all=True, per_level=4):
     """A config at full size: decrypted result == plain predicate; the sampled records' validation bits and
     masked payloads are recomputed by the oracle (from the same seeded inputs) and byte-equal.  keep_all:
     every intermediate keeps its row (VLP_F_KEEP_ALL), so 4 random gates of every level are rechecked too;
@@ -253,9 +321,9 @@ def _full_size_sampled(server, cfg, sample, keep_all=True):
         assert np.array_equal(mid[prog.node_row(0, i), :631], v), ("v", i)
         for j in range(wl.l_S):
             assert np.array_equal(mid[prog.node_row(1, i, j), :631], masked[j]), ("mask", i, j)
-    if keep_all:  # plus pure-function parity of 4 random gates of every level (SURVEY 4 layer 3)
+    if keep_all:  # plus pure-function parity of per_level random gates of every level (SURVEY 4 layer 3)
         regions = {0: q, 1: db, 2: mid, 3: out}
-        assert _gate_checks(prog, regions, okeys, per_level=4, seed=cfg) >= 4 * (prog.info.levels - 6)
+        assert _gate_checks(prog, regions, okeys, per_level=per_level, seed=cfg) >= per_level * (prog.info.levels - 6)
     return wl, want
 
 
@@ -326,17 +394,28 @@ def test_config2_full_size_sampled(server):
 
 
 def test_config3_full_size_sampled(server):
-    """Config 3 at full size (rectangle containment, 4096 records, 1,060,832 BR): predicate + records 0 and
-    4095 byte-equal."""
-    _full_size_sampled(server, 3, [0, 4095])
+    """Config 3 at full size (rectangle containment, 4096 records, 1,060,832 BR; the bench headline): predicate +
+    8 records (incl. 0, 4095 and every record containing the query) byte-equal, and 16 random gates of every level
+    recomputed by the oracle from the GPU's own inputs."""
+    wl = make_workload(3, key_seed=SEED)
+    hits = [i for i in range(wl.M) if _contains(wl, i)]
+    sample = sorted(set([0, 4095] + hits[:4] + random.Random(3).sample(range(wl.M), 6)))
+    _full_size_sampled(server, 3, sample, per_level=16)
 
 
 def test_config4_full_size_sampled(server):
-    """Config 4 at full size (IdM, 65,536 records, 6,750,176 BR on one GPU): predicate + the matching record
-    (if the seed put the query id in the DB) and the last record byte-equal."""
+    """Config 4 at full size (IdM, 65,536 records, 6,750,176 BR on one GPU): predicate + 8 records (the matching
+    record if the seed put the query id in the DB, the last one, 6 random) byte-equal, and 16 random gates of every
+    level recomputed by the oracle."""
     wl = make_workload(4, key_seed=SEED)
     hits = [i for i in range(wl.M) if int(wl.records[i][0]) == int(wl.query[0])]
-    _full_size_sampled(server, 4, (hits[:1] or [1]) + [wl.M - 1])
+    sample = sorted(set((hits[:1] or [1]) + [wl.M - 1] + random.Random(4).sample(range(wl.M), 6)))
+    _full_size_sampled(server, 4, sample, per_level=16)
+
+
+def _contains(wl, i):
+    r = [int(v) for v in wl.records[i]]
+    return all(r[2 * k] <= int(wl.query[k]) <= r[2 * k + 1] for k in range(wl.d))
 
 
 def _full_parity_small(server, mode, d, l_I, l_S, flags, records, payloads, query, okeys_seed=SEED):
@@ -624,7 +703,6 @@ def _gate_checks(prog, regions, okeys, levels=None, per_level=None, seed=0):
     return len(todo)
 
 
-@pytest.mark.parametrize("variant", list(_VARIANT_FLAGS))
 def _linear_checks(prog, regions):
     """R24: every linear job's output row equals the sum of its input rows mod 2^32.  Returns the count."""
     def ct(slot):
