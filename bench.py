@@ -331,9 +331,10 @@ def main():
     keys = A.Keys(wl.key_seed)                 # client (every rank regenerates the same keys from the seed)
     srv = A.Server(keys, local)
     per = A.record_cts(m)
-    # device PubKeyGen + ServerEnc (byte-identical to the host calls; tests/test_gpu_parity.py)
-    db = A.encrypt_db_device(keys, m, wl.records[first:first + shard], wl.payloads[first:first + shard],
-                             pk_seed=wl.key_seed + 1, first=first, count=shard, device=local)
+    # the client's device PubKeyGen (takes sk) -> the server's device ServerEnc (pk samples only), byte-identical to
+    # the host calls (tests/test_gpu_parity.py)
+    pk = A.pubkeygen_device(keys, m, wl.key_seed + 1, first, shard, device=local)
+    db = A.server_encrypt_db_device(m, pk, wl.records[first:first + shard], wl.payloads[first:first + shard])
     nq = args.queries
     if nq > 1 and world > 1:
         raise SystemExit("--queries > 1 is single-GPU (multi-query packing of one shard)")

@@ -142,12 +142,39 @@ int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);
  * a second call returns VLP_EPKUSED.  Server side: needs no secret key. */
 int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* out);
 
-/* Device PubKeyGen + ServerEnc (both roles on one machine, e.g. to build benchmark
- * DBs): the encrypted DB of records [first, first+count) written straight to out_dev ([count][per_record]
+/* ---- GPU preprocessing, role-separated like P:192: the client's KeyGen and PubKeyGen take
+ * the secret key, the server's ServerEnc takes only public-key samples.  Each is byte-identical to its host call;
+ * the Gaussian noise is drawn on the host (the same libm Box-Muller: device libm may round differently), the
+ * counter-PRNG mask words, ring products and inner products run on `stream`'s device.  Synchronous. */
+
+/* Device KeyGen (client): the same sk / evk as vlp_keygen(seed, params), byte for byte -- the
+ * bootstrapping key's masks and ring products a*z (R4, O7) and the key-switching key's masks and <a, s> (O10) are
+ * computed on the device and copied back into the host evk.  scratch_dev >= vlp_keygen_device_scratch_bytes(). */
+size_t vlp_keygen_device_scratch_bytes(void);
+int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch_dev, size_t scratch_bytes,
+                      uint64_t stream, vlp_sk** sk, vlp_evk** evk);
+/* Device PubKeyGen (client; alg:PubKeyGen P:194-219): the single-use TLWE(0) samples of records
+ * [first, first+count) written to pk_dev ([count][per_record][632], the row order of vlp_server_encrypt_db),
+ * byte-identical to vlp_pubkeygen(sk, meta, seed, first, count)'s samples.  The copy of s placed in scratch_dev
+ * is zeroed before the call returns.  scratch_dev >= vlp_pubkeygen_device_scratch_bytes(meta, count). */
+int vlp_pubkeygen_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes);
+int vlp_pubkeygen_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                         uint32_t* pk_dev, void* scratch_dev, size_t scratch_bytes, uint64_t stream);
+/* Device ServerEnc (server; alg:ServerEnc P:223-247): out_dev = pk_dev + (0, Ecd(bit)) for every row of records
+ * [0, count) of the public-key samples (out_dev may equal pk_dev).  Needs no secret key.  words / payloads as in
+ * vlp_server_encrypt_db (host, range-checked: VLP_ERANGE).  scratch_dev >=
+ * vlp_server_encrypt_db_device_scratch_bytes(meta, count). */
+int vlp_server_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes);
+int vlp_server_encrypt_db_device(const vlp_meta* meta, size_t count, const uint32_t* pk_dev, const uint64_t* words,
+                                 const uint64_t* payloads, uint32_t* out_dev, void* scratch_dev, size_t scratch_bytes,
+                                 uint64_t stream);
+
+/* Device PubKeyGen + ServerEnc fused (both roles on one machine, e.g. to build benchmark DBs): the encrypted DB of records [first, first+count) written straight to out_dev ([count][per_record]
  * [632], the vlp_server_encrypt_db layout), byte-identical to vlp_pubkeygen(sk, meta, pk_seed, first, count)
  * followed by vlp_server_encrypt_db.  The Gaussian noise is drawn on the host (the same libm Box-Muller),
  * the PRNG mask words and inner products on the device.  words / payloads as in vlp_server_encrypt_db.
- * scratch_dev >= vlp_encrypt_db_device_scratch_bytes(meta, count).  Synchronous. */
+ * scratch_dev >= vlp_encrypt_db_device_scratch_bytes(meta, count); the copy of s in it is zeroed before
+ * returning.  Synchronous. */
 int vlp_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes);
 int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_seed, size_t first, size_t count,
                           const uint64_t* words, const uint64_t* payloads, uint32_t* out_dev, void* scratch_dev,

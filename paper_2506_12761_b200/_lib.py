@@ -69,6 +69,12 @@ SIGNATURES = {
     "vlp_server_encrypt_db": (_i, [_vp, _u64p, _u64p, _u32p]),
     "vlp_encrypt_db_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_encrypt_db_device": (_i, [_vp, ctypes.POINTER(VlpMeta), _u64, _sz, _sz, _u64p, _u64p, _vp, _vp, _sz, _u64]),
+    "vlp_keygen_device_scratch_bytes": (_sz, []),
+    "vlp_keygen_device": (_i, [_u64, ctypes.POINTER(VlpParams), _vp, _sz, _u64, _pp, _pp]),
+    "vlp_pubkeygen_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_pubkeygen_device": (_i, [_vp, ctypes.POINTER(VlpMeta), _u64, _sz, _sz, _vp, _vp, _sz, _u64]),
+    "vlp_server_encrypt_db_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_server_encrypt_db_device": (_i, [ctypes.POINTER(VlpMeta), _sz, _vp, _u64p, _u64p, _vp, _vp, _sz, _u64]),
     "vlp_server_evk_bytes": (_sz, []),
     "vlp_server_create": (_i, [_i, _vp, _vp, _sz, _u64, _pp]),
     "vlp_program_create": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _pp]),

@@ -38,10 +38,17 @@ def _stream_handle(stream, device=None) -> int:
 class Keys:
     """vlp_keygen: secret key + evaluation key, host side."""
 
-    def __init__(self, seed: int):
+    def __init__(self, seed: int, device: int | None = None):
+        """Host KeyGen (vlp_keygen), or with device= the byte-identical device KeyGen (vlp_keygen_device)."""
         self.seed = seed
         sk, evk = ctypes.c_void_p(), ctypes.c_void_p()
-        check(lib().vlp_keygen(seed, None, ctypes.byref(sk), ctypes.byref(evk)))
+        if device is None:
+            check(lib().vlp_keygen(seed, None, ctypes.byref(sk), ctypes.byref(evk)))
+        else:
+            import torch
+            sc = torch.empty(lib().vlp_keygen_device_scratch_bytes(), dtype=torch.uint8, device=f"cuda:{device}")
+            check(lib().vlp_keygen_device(seed, None, ctypes.c_void_p(sc.data_ptr()), sc.numel(),
+                                          _stream_handle(None, device), ctypes.byref(sk), ctypes.byref(evk)))
         self.sk, self.evk = sk, evk
 
     def __del__(self):
@@ -114,6 +121,45 @@ class Keys:
         return out
 
 
+def _payload_words(m: VlpMeta, payloads):
+    pw = (m.l_S + 63) // 64  # payload words per record (l_S up to 128)
+    if pw == 1:
+        return np.ascontiguousarray(np.asarray(payloads, dtype=np.uint64))
+    return np.array([[(int(v) >> (64 * w)) & (2 ** 64 - 1) for w in range(pw)] for v in payloads], dtype=np.uint64)
+
+
+def pubkeygen_device(keys: "Keys", m: VlpMeta, pk_seed: int, first: int, count: int, device: int = 0, stream=None):
+    """Client side, device PubKeyGen (alg:PubKeyGen P:194-219): the records' single-use TLWE(0) samples as a torch
+    int32 [count * per, 632] tensor, byte-identical to vlp_pubkeygen's samples."""
+    import torch
+    per = record_cts(m)
+    pk = torch.empty((count * per, CT_STRIDE), dtype=torch.int32, device=f"cuda:{device}")
+    sb = ctypes.c_size_t()
+    check(lib().vlp_pubkeygen_device_scratch_bytes(ctypes.byref(m), count, ctypes.byref(sb)))
+    sc = torch.empty(max(256, sb.value), dtype=torch.uint8, device=f"cuda:{device}")
+    check(lib().vlp_pubkeygen_device(keys.sk, ctypes.byref(m), pk_seed, first, count, ctypes.c_void_p(pk.data_ptr()),
+                                     ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream, device)))
+    return pk
+
+
+def server_encrypt_db_device(m: VlpMeta, pk_dev, words, payloads, out=None, stream=None):
+    """Server side, device ServerEnc (alg:ServerEnc P:223-247): pk + (0, Ecd(bit)) for every DB row, in place in
+    pk_dev unless out is given.  Takes no secret key."""
+    import torch
+    words = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+    pays = _payload_words(m, payloads)
+    count = len(payloads)
+    dev = pk_dev.device.index
+    out = pk_dev if out is None else out
+    sb = ctypes.c_size_t()
+    check(lib().vlp_server_encrypt_db_device_scratch_bytes(ctypes.byref(m), count, ctypes.byref(sb)))
+    sc = torch.empty(max(256, sb.value), dtype=torch.uint8, device=pk_dev.device)
+    check(lib().vlp_server_encrypt_db_device(ctypes.byref(m), count, ctypes.c_void_p(pk_dev.data_ptr()), _u64p(words),
+                                             _u64p(pays), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(sc.data_ptr()),
+                                             sc.numel(), _stream_handle(stream, dev)))
+    return out
+
+
 def encrypt_db_device(keys: "Keys", m: VlpMeta, words, payloads, pk_seed: int, first: int = 0,
                       count: int | None = None, device: int = 0, stream=None):
     """Device PubKeyGen + ServerEnc: the encrypted DB as a torch int32 [count * per, 632] tensor on `device`,
@@ -133,7 +179,7 @@ def encrypt_db_device(keys: "Keys", m: VlpMeta, words, payloads, pk_seed: int, f
     sc = torch.empty(max(256, sb.value), dtype=torch.uint8, device=f"cuda:{device}")
     check(lib().vlp_encrypt_db_device(keys.sk, ctypes.byref(m), pk_seed, first, count, _u64p(words), _u64p(pays),
                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(sc.data_ptr()), sc.numel(),
-                                      _stream_handle(stream)))
+                                      _stream_handle(stream, device)))
     return out
 
 

@@ -230,6 +230,20 @@ int build_program(vlp_server* server, std::unique_ptr<vlp_program>& p) {
 
 using namespace vlp;
 
+// No C++ exception crosses the C ABI: allocation failures while compiling become VLP_ENOMEM.
+extern "C++" {
+template <class F>
+static int no_throw(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(VLP_ENOMEM, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(VLP_EINVAL, e.what());
+  }
+}
+}  // extern "C++"
+
 extern "C" {
 
 int vlp_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
@@ -265,8 +279,119 @@ int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_se
   if ((e = launch_encrypt_db(s_dev, nz_dev, bits_dev, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
                              meta->l_I, first, nz.size(), out_dev, st)))
     return cuda_fail(e, "encrypt db");
+  if ((e = cudaMemsetAsync(s_dev, 0, n * 4, st))) return cuda_fail(e, "scrub");  // s does not outlive the call
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "encrypt db sync");
   return VLP_OK;
+}
+
+size_t vlp_keygen_device_scratch_bytes(void) {
+  return align256(kRawBskBytes) + align256(kKskBytes) + align256(kRawBskBytes / 2) + align256(static_cast<size_t>(N) * kKsT * 3 * 4) +
+         align256(n * 4) + align256(N * 4);
+}
+
+int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch, size_t scratch_bytes, uint64_t stream,
+                      vlp_sk** sk_out, vlp_evk** evk_out) {
+  if (!sk_out || !evk_out || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (scratch_bytes < vlp_keygen_device_scratch_bytes()) return fail(VLP_ENOMEM, "scratch too small");
+  vlp_params p;
+  if (int rc = resolve_params(params, &p)) return rc;
+  return no_throw([&] {
+    auto sk = std::make_unique<vlp_sk>();
+    auto evk = std::make_unique<vlp_evk>();
+    sk->params = p;
+    evk->params = p;
+    secret_keys(seed, sk.get());
+    evk->bsk.assign(static_cast<size_t>(n) * kRows * 2 * N, 0);
+    evk->ksk.assign(static_cast<size_t>(N) * kKsT * 3 * kCt, 0);
+    std::vector<uint32_t> e_bsk(static_cast<size_t>(n) * kRows * N), e_ksk(static_cast<size_t>(N) * kKsT * 3);
+    keygen_noise(seed, p, e_bsk.data(), e_ksk.data());  // host libm Box-Muller (byte-identical noise)
+    uint8_t* sc = static_cast<uint8_t*>(scratch);
+    uint32_t* bsk = reinterpret_cast<uint32_t*>(sc);
+    uint32_t* ksk = reinterpret_cast<uint32_t*>(sc + align256(kRawBskBytes));
+    uint32_t* eb = reinterpret_cast<uint32_t*>(sc + align256(kRawBskBytes) + align256(kKskBytes));
+    uint32_t* ek = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(eb) + align256(kRawBskBytes / 2));
+    uint32_t* s_dev = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(ek) + align256(e_ksk.size() * 4));
+    uint32_t* z_dev = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(s_dev) + align256(n * 4));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(s_dev, sk->s, n * 4, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(z_dev, sk->z, N * 4, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(eb, e_bsk.data(), e_bsk.size() * 4, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(ek, e_ksk.data(), e_ksk.size() * 4, cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "keygen upload");
+    if ((e = launch_keygen(prng_prefix(seed, kBskA), prng_prefix(seed, kKskA), s_dev, z_dev, eb, ek, bsk, ksk, st)))
+      return cuda_fail(e, "keygen kernels");
+    if ((e = cudaMemcpyAsync(evk->bsk.data(), bsk, kRawBskBytes, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(evk->ksk.data(), ksk, kKskBytes, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemsetAsync(s_dev, 0, align256(n * 4) + N * 4, st)))  // the secret keys do not outlive the call
+      return cuda_fail(e, "keygen download");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "keygen sync");
+    *sk_out = sk.release();
+    *evk_out = evk.release();
+    return static_cast<int>(VLP_OK);
+  });
+}
+
+int vlp_pubkeygen_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
+  size_t per = 0;
+  if (int rc = vlp_db_record_cts(meta, &per)) return rc;
+  if (!scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  *scratch_bytes = align256(n * 4) + align256(count * per * 4);
+  return VLP_OK;
+}
+
+int vlp_pubkeygen_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                         uint32_t* pk_dev, void* scratch, size_t scratch_bytes, uint64_t stream) {
+  if (!pk_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  return no_throw([&] {
+    std::vector<uint32_t> nz;
+    uint64_t h1 = 0;
+    if (int rc = prepare_pk_noise(sk, meta, seed, first, count, nz, &h1)) return rc;
+    size_t need = 0;
+    vlp_pubkeygen_device_scratch_bytes(meta, count, &need);
+    if (scratch_bytes < need) return fail(VLP_ENOMEM, "scratch too small");
+    const size_t per = nz.size() / count, W = record_words(*meta);
+    uint8_t* sc = static_cast<uint8_t*>(scratch);
+    uint32_t* s_dev = reinterpret_cast<uint32_t*>(sc);
+    uint32_t* nz_dev = reinterpret_cast<uint32_t*>(sc + align256(n * 4));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(s_dev, sk->s, n * 4, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(nz_dev, nz.data(), nz.size() * 4, cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "upload");
+    if ((e = launch_encrypt_db(s_dev, nz_dev, nullptr, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
+                               meta->l_I, first, nz.size(), pk_dev, st)))
+      return cuda_fail(e, "pubkeygen");
+    if ((e = cudaMemsetAsync(s_dev, 0, n * 4, st))) return cuda_fail(e, "scrub");  // s does not outlive the call
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "pubkeygen sync");
+    return static_cast<int>(VLP_OK);
+  });
+}
+
+int vlp_server_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
+  size_t per = 0;
+  if (int rc = vlp_db_record_cts(meta, &per)) return rc;
+  if (!scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  *scratch_bytes = align256(count * per);
+  return VLP_OK;
+}
+
+int vlp_server_encrypt_db_device(const vlp_meta* meta, size_t count, const uint32_t* pk_dev, const uint64_t* words,
+                                 const uint64_t* payloads, uint32_t* out_dev, void* scratch, size_t scratch_bytes,
+                                 uint64_t stream) {
+  if (!pk_dev || !out_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  return no_throw([&] {
+    std::vector<uint8_t> bits;
+    if (int rc = prepare_db_bits(meta, count, words, payloads, bits)) return rc;
+    if (scratch_bytes < align256(bits.size())) return fail(VLP_ENOMEM, "scratch too small");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(scratch, bits.data(), bits.size(), cudaMemcpyHostToDevice, st))) return cuda_fail(e, "upload");
+    if ((e = launch_server_enc(pk_dev, static_cast<const uint8_t*>(scratch), bits.size(), out_dev, st)))
+      return cuda_fail(e, "server enc");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server enc sync");
+    return static_cast<int>(VLP_OK);
+  });
 }
 
 size_t vlp_server_evk_bytes(void) { return kEvkBytes; }
@@ -328,19 +453,7 @@ static int finish_program(vlp_server* server, std::unique_ptr<vlp_program>& p, v
   *out = p.release();
   return VLP_OK;
 }
-// No C++ exception crosses the C ABI: allocation failures while compiling become VLP_ENOMEM.
-extern "C++" {
-template <class F>
-static int no_throw(F&& f) {
-  try {
-    return f();
-  } catch (const std::bad_alloc&) {
-    return fail(VLP_ENOMEM, "out of host memory");
-  } catch (const std::exception& e) {
-    return fail(VLP_EINVAL, e.what());
-  }
-}
-}  // extern "C++"
+
 
 int vlp_program_create(vlp_server* server, const vlp_meta* meta, size_t first, size_t count, vlp_program** out) {
   if (!meta || !out) return fail(VLP_EINVAL, "null argument");  // server may be NULL: compile only

@@ -85,6 +85,34 @@ int check_meta(const vlp_meta* m) {
   return VLP_OK;
 }
 
+int resolve_params(const vlp_params* params, vlp_params* p) {
+  *p = vlp_params{630, 1024, 1, 7, 3, 2, 8, 0x1p-15, 0x1p-25, 0x1p-15};
+  if (params) {
+    if (params->n != 630 || params->N != 1024 || params->k != 1 || params->bg_bits != 7 || params->ell != 3 ||
+        params->ks_base_bits != 2 || params->ks_t != 8)
+      return fail(VLP_EINVAL, "only the 128-bit parameter set of tab:tfhe_params is supported");
+    *p = *params;
+  }
+  return VLP_OK;
+}
+
+// Binary LWE key s and ring key z (O4): bit 63 of the counter PRNG.
+void secret_keys(uint64_t seed, vlp_sk* sk) {
+  for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(prng(seed, kSkLwe, 0, i) >> 63);
+  for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(prng(seed, kSkRing, 0, j) >> 63);
+}
+
+// Host half of vlp_keygen_device: every Gaussian noise word of the evaluation key, exactly the values vlp_keygen
+// draws -- bsk row (i, r) coefficient j at [(i*6 + r)*N + j] (sigma_bk), ksk row idx at [idx] (sigma_ks).
+void keygen_noise(uint64_t seed, const vlp_params& p, uint32_t* bsk_noise, uint32_t* ksk_noise) {
+  parallel_for(static_cast<size_t>(n) * kRows, [&](size_t ir) {
+    for (int j = 0; j < N; j++) bsk_noise[ir * N + j] = noise(seed, kBskE, ir, j, p.sigma_bk);
+  });
+  parallel_for(static_cast<size_t>(N) * kKsT * 3, [&](size_t idx) { ksk_noise[idx] = noise(seed, kKskE, idx, 0, p.sigma_ks); });
+}
+
+uint64_t prng_prefix(uint64_t seed, uint64_t dom) { return mix(seed ^ (dom * 0x9E3779B97F4A7C15ull)); }
+
 }  // namespace vlp
 
 using namespace vlp;
@@ -102,13 +130,7 @@ int vlp_params_tfhe128(vlp_params* p) {
 int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk** evk_out) {
   if (!sk_out || !evk_out) return fail(VLP_EINVAL, "null output");
   vlp_params p;
-  vlp_params_tfhe128(&p);
-  if (params) {
-    if (params->n != 630 || params->N != 1024 || params->k != 1 || params->bg_bits != 7 || params->ell != 3 ||
-        params->ks_base_bits != 2 || params->ks_t != 8)
-      return fail(VLP_EINVAL, "only the 128-bit parameter set of tab:tfhe_params is supported");
-    p = *params;
-  }
+  if (int rc = resolve_params(params, &p)) return rc;
   std::unique_ptr<vlp_sk> skp(new (std::nothrow) vlp_sk);
   std::unique_ptr<vlp_evk> evkp(new (std::nothrow) vlp_evk);
   if (!skp || !evkp) return fail(VLP_ENOMEM, "out of memory");
@@ -122,8 +144,7 @@ int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk
   }
   sk->params = p;
   evk->params = p;
-  for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(prng(seed, kSkLwe, 0, i) >> 63);
-  for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(prng(seed, kSkRing, 0, j) >> 63);
+  secret_keys(seed, sk);
   std::vector<int> support;
   support.reserve(N);
   for (int j = 0; j < N; j++)
@@ -271,13 +292,12 @@ namespace vlp {
 // Host half of vlp_encrypt_db_device (api.cu): range checks, the per-sample Gaussian noise of alg:PubKeyGen
 // (exactly the values vlp_pubkeygen draws), the plaintext bit of every DB row, and the PRNG prefix
 // h1 = mix(seed ^ PK_A * C1) the device continues from.
-int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
-                       const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
-                       std::vector<uint8_t>& bits, uint64_t* h1) {
-  if (!sk) return fail(VLP_EINVAL, "null argument");
+// ServerEnc's plaintext: range checks and the bit of every DB row (words then payload bits, see
+// vlp_server_encrypt_db).
+int prepare_db_bits(const vlp_meta* meta, size_t count, const uint64_t* words, const uint64_t* payloads,
+                    std::vector<uint8_t>& bits) {
   if (int rc = check_meta(meta)) return rc;
-  if (count == 0 || first + count > meta->M) return fail(VLP_EINVAL, "bad record range");
-  if (!words || !payloads) return fail(VLP_EINVAL, "null argument");
+  if (count && (!words || !payloads)) return fail(VLP_EINVAL, "null argument");
   const size_t W = record_words(*meta), lI = meta->l_I, lS = meta->l_S, per = W * lI + lS;
   const size_t PW = (lS + 63) / 64, top = lS - 64 * (PW - 1);
   for (size_t r = 0; r < count; r++) {
@@ -286,15 +306,12 @@ int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, si
     if (top < 64 && payloads[r * PW + PW - 1] >> top) return fail(VLP_ERANGE, "payload >= 2^l_S");
   }
   try {
-    nz.resize(count * per);
     bits.resize(count * per);
   } catch (...) {
     return fail(VLP_ENOMEM, "out of host memory");
   }
   parallel_for(count * per, [&](size_t idx) {
     const size_t rec = idx / per, row = idx % per;
-    const size_t local = row < W * lI ? (row % lI) * W + row / lI : row;
-    nz[idx] = noise(seed, kPkE, (first + rec) * per + local, 0, sk->params.sigma_lwe);
     if (row < W * lI) {
       bits[idx] = static_cast<uint8_t>((words[rec * W + row / lI] >> (row % lI)) & 1);
     } else {
@@ -302,8 +319,41 @@ int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, si
       bits[idx] = static_cast<uint8_t>((payloads[rec * PW + j / 64] >> (j % 64)) & 1);
     }
   });
-  *h1 = mix(seed ^ (kPkA * 0x9E3779B97F4A7C15ull));
   return VLP_OK;
+}
+
+// PubKeyGen's host half: the per-sample Gaussian noise of alg:PubKeyGen (exactly the values vlp_pubkeygen
+// draws) and the PRNG prefix h1 = mix(seed ^ PK_A * C1) the device continues from.
+int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                     std::vector<uint32_t>& nz, uint64_t* h1) {
+  if (!sk) return fail(VLP_EINVAL, "null argument");
+  if (int rc = check_meta(meta)) return rc;
+  if (count == 0 || first + count > meta->M) return fail(VLP_EINVAL, "bad record range");
+  const size_t W = record_words(*meta), lI = meta->l_I, lS = meta->l_S, per = W * lI + lS;
+  try {
+    nz.resize(count * per);
+  } catch (...) {
+    return fail(VLP_ENOMEM, "out of host memory");
+  }
+  parallel_for(count * per, [&](size_t idx) {
+    const size_t rec = idx / per, row = idx % per;
+    const size_t local = row < W * lI ? (row % lI) * W + row / lI : row;
+    nz[idx] = noise(seed, kPkE, (first + rec) * per + local, 0, sk->params.sigma_lwe);
+  });
+  *h1 = prng_prefix(seed, kPkA);
+  return VLP_OK;
+}
+
+// Host half of vlp_encrypt_db_device (api.cu): PubKeyGen's noise and PRNG prefix plus ServerEnc's row bits.
+int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                       const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
+                       std::vector<uint8_t>& bits, uint64_t* h1) {
+  if (!sk) return fail(VLP_EINVAL, "null argument");
+  if (int rc = check_meta(meta)) return rc;
+  if (count == 0 || first + count > meta->M) return fail(VLP_EINVAL, "bad record range");
+  if (!words || !payloads) return fail(VLP_EINVAL, "null argument");
+  if (int rc = prepare_db_bits(meta, count, words, payloads, bits)) return rc;
+  return prepare_pk_noise(sk, meta, seed, first, count, nz, h1);
 }
 }  // namespace vlp
 

@@ -1206,9 +1206,86 @@ __global__ void __launch_bounds__(256) vlp_encrypt_db_kernel(const uint32_t* __r
 #pragma unroll
   for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
   if (lane == 0) {
-    ct[n] = b + noise[idx] + (bits[idx] ? kMu : 0u - kMu);
+    ct[n] = b + noise[idx] + (bits ? (bits[idx] ? kMu : 0u - kMu) : 0u);  // bits == nullptr: the pk sample alone
     ct[n + 1] = 0;
   }
+}
+
+// Device ServerEnc (alg:ServerEnc P:223-247): out = pk + (0, Ecd(bit)), thread per word (out may alias pk).
+__global__ void __launch_bounds__(256) vlp_server_enc_kernel(const uint32_t* pk, const uint8_t* __restrict__ bits,
+                                                            uint64_t nsamples, uint32_t* out) {
+  const uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= nsamples * kCt) return;
+  const uint64_t idx = w / kCt;
+  const uint32_t col = static_cast<uint32_t>(w % kCt);
+  const uint32_t v = pk[w];
+  out[w] = col == static_cast<uint32_t>(n) ? v + (bits[idx] ? kMu : 0u - kMu) : v;
+}
+
+// Device KeyGen, bootstrapping key (R4, O7): CTA per row (i, r): a_j = uniform(BSK_A, obj = i*6 + r, word j),
+// b = a * z + e (negacyclic, z binary: the sum of the rotations X^k a over supp z), then s_i g_j on component
+// r / 3's constant coefficient -- the same words vlp_keygen computes on the host.
+__global__ void __launch_bounds__(256) vlp_keygen_bsk_kernel(uint64_t h1, const uint32_t* __restrict__ s,
+                                                            const uint32_t* __restrict__ z, const uint32_t* __restrict__ e,
+                                                            uint32_t* __restrict__ bsk) {
+  __shared__ uint32_t a[N];
+  __shared__ uint32_t zs[N];
+  const uint32_t ir = blockIdx.x;
+  const uint64_t h2 = prng_mix(h1 ^ (static_cast<uint64_t>(ir) * 0xC2B2AE3D27D4EB4Full));
+  for (uint32_t j = threadIdx.x; j < static_cast<uint32_t>(N); j += blockDim.x) {
+    a[j] = static_cast<uint32_t>(prng_mix(h2 ^ (static_cast<uint64_t>(j) * 0x165667B19E3779F9ull)) >> 32);
+    zs[j] = z[j];
+  }
+  __syncthreads();
+  uint32_t* ra = bsk + static_cast<size_t>(ir) * 2 * N;
+  uint32_t* rb = ra + N;
+  const uint32_t i = ir / kRows, r = ir % kRows;
+  const uint32_t g = s[i] ? 1u << (32 - kBgBits * (r % kEll + 1)) : 0u;
+  for (uint32_t t = threadIdx.x; t < static_cast<uint32_t>(N); t += blockDim.x) {
+    uint32_t acc = 0;
+    for (uint32_t k = 0; k <= t; k++) acc += zs[k] ? a[t - k] : 0u;
+    for (uint32_t k = t + 1; k < static_cast<uint32_t>(N); k++) acc -= zs[k] ? a[t + N - k] : 0u;
+    acc += e[static_cast<size_t>(ir) * N + t];
+    if (t == 0 && r / kEll == 1) acc += g;
+    rb[t] = acc;
+    ra[t] = a[t] + ((t == 0 && r / kEll == 0) ? g : 0u);
+  }
+}
+
+// Device KeyGen, key-switching key (O10): warp per row idx = (i*8 + j)*3 + v-1: TLWE_s(v z_i 2^(32-2(j+1))).
+__global__ void __launch_bounds__(256) vlp_keygen_ksk_kernel(uint64_t h1, const uint32_t* __restrict__ s,
+                                                            const uint32_t* __restrict__ z, const uint32_t* __restrict__ e,
+                                                            uint32_t* __restrict__ ksk) {
+  const uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  if (idx >= static_cast<uint32_t>(N * kKsT * 3)) return;
+  const uint32_t i = idx / (kKsT * 3), j = (idx / 3) % kKsT, v = idx % 3 + 1;
+  const uint64_t h2 = prng_mix(h1 ^ (static_cast<uint64_t>(idx) * 0xC2B2AE3D27D4EB4Full));
+  uint32_t* ct = ksk + static_cast<size_t>(idx) * kCt;
+  uint32_t b = 0;
+  for (uint32_t w = lane; w < static_cast<uint32_t>(n); w += 32) {
+    const uint32_t a = static_cast<uint32_t>(prng_mix(h2 ^ (static_cast<uint64_t>(w) * 0x165667B19E3779F9ull)) >> 32);
+    ct[w] = a;
+    b += a * s[w];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  if (lane == 0) {
+    ct[n] = b + v * z[i] * (1u << (32 - kKsBaseBits * (j + 1))) + e[idx];
+    ct[n + 1] = 0;
+  }
+}
+
+cudaError_t launch_server_enc(const uint32_t* pk, const uint8_t* bits, uint64_t nsamples, uint32_t* out, cudaStream_t st) {
+  const uint64_t words = nsamples * kCt;
+  if (words) vlp_server_enc_kernel<<<static_cast<unsigned>((words + 255) / 256), 256, 0, st>>>(pk, bits, nsamples, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keygen(uint64_t h_bsk, uint64_t h_ksk, const uint32_t* s, const uint32_t* z, const uint32_t* e_bsk,
+                          const uint32_t* e_ksk, uint32_t* bsk, uint32_t* ksk, cudaStream_t st) {
+  vlp_keygen_bsk_kernel<<<n * kRows, 256, 0, st>>>(h_bsk, s, z, e_bsk, bsk);
+  vlp_keygen_ksk_kernel<<<(N * kKsT * 3 + 7) / 8, 256, 0, st>>>(h_ksk, s, z, e_ksk, ksk);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,

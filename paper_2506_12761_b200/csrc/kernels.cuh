@@ -93,6 +93,9 @@ int set_br_route(int engine, int param);  // vlp_debug_route
 int br_launch_count(uint32_t njobs, int sm_count);
 cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
                               uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st);
+cudaError_t launch_server_enc(const uint32_t* pk, const uint8_t* bits, uint64_t nsamples, uint32_t* out, cudaStream_t st);
+cudaError_t launch_keygen(uint64_t h_bsk, uint64_t h_ksk, const uint32_t* s, const uint32_t* z, const uint32_t* e_bsk,
+                          const uint32_t* e_ksk, uint32_t* bsk, uint32_t* ksk, cudaStream_t st);
 void launch_kmat_sw(const uint32_t* ksk, int8_t* kmat_sw, cudaStream_t st);
 size_t ks_stage_bytes_t(uint32_t chunk);
 // K3T over all jobs of a level in chunks of `chunk`: prologue (S7 + R6) + tcgen05 GEMM with fused epilogue

@@ -32,6 +32,14 @@ enum : uint64_t {
 };
 uint64_t prng(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word);
 uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma);
+int resolve_params(const vlp_params* params, vlp_params* out);
+void secret_keys(uint64_t seed, vlp_sk* sk);
+void keygen_noise(uint64_t seed, const vlp_params& p, uint32_t* bsk_noise, uint32_t* ksk_noise);
+uint64_t prng_prefix(uint64_t seed, uint64_t dom);
+int prepare_db_bits(const vlp_meta* meta, size_t count, const uint64_t* words, const uint64_t* payloads,
+                    std::vector<uint8_t>& bits);
+int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                     std::vector<uint32_t>& nz, uint64_t* h1);
 int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
                        const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
                        std::vector<uint8_t>& bits, uint64_t* h1);

@@ -624,6 +624,30 @@ def test_noise_over_depth_at_scale(server):
     assert max(sds) / min(sds) < 1.1, sds  # bootstrapping refreshes: no growth with depth
 
 
+def test_device_keygen_equals_host():
+    """vlp_keygen_device (masks, ring products a*z and <a, s> on the device, noise on the host)
+    gives the same s, z, bsk and ksk as vlp_keygen, byte for byte."""
+    kh, kd = A.Keys(321), A.Keys(321, device=0)
+    for x, y in zip(kh.export(), kd.export()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("cfg,count", [(1, None), (9, 16), (3, 512)])
+def test_role_separated_device_preprocessing(server, cfg, count):
+    """P:192 roles on the GPU: the client's device PubKeyGen (takes sk) then the server's device ServerEnc (takes
+    only the pk samples) equal the host PubKeyGen + ServerEnc and the fused device call, byte for byte."""
+    wl = make_workload(cfg, key_seed=SEED)
+    count = wl.M if count is None else count
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    k = server.keys
+    pk = A.pubkeygen_device(k, m, 4321, 0, count)
+    db = A.server_encrypt_db_device(m, pk, wl.records[:count], wl.payloads[:count])
+    host = k.encrypt_db(m, wl.records[:count], wl.payloads[:count], pk_seed=4321, count=count)
+    assert np.array_equal(A.to_host(db), host)
+    fused = A.encrypt_db_device(k, m, wl.records[:count], wl.payloads[:count], pk_seed=4321, count=count)
+    assert np.array_equal(A.to_host(fused), host)
+
+
 @pytest.mark.parametrize("cfg,count", [(1, None), (9, 16), (4, 4096)])
 def test_device_encrypt_db_equals_host(server, cfg, count):
     """Device PubKeyGen + ServerEnc (vlp_encrypt_db_device) is byte-identical to the host vlp_pubkeygen +
