@@ -1614,7 +1614,9 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
     // a tail of at most one bootstrap per SM runs in latency mode (warp groups per bootstrap); at most one per
     // two SMs, on a 2-CTA cluster per bootstrap; at most one per resident 6-CTA cluster, on a 6-CTA cluster
     const uint32_t per = (tail + sm_count - 1) / sm_count;
-    if (fft && tail > static_cast<uint32_t>(sm_count)) return launch_blind_rotate_fft(r, static_cast<int>(per), sm_count, st);
+    // K2F's single-warp bootstraps have a long per-step latency (one bootstrap per SM takes ~11 ms for 630 steps,
+    // 2-4 per SM about the same), so tails of at most kBrBoot per SM run on the NTT kernels (K2<b>: 6.1-12.7 ms)
+    if (fft && per > static_cast<uint32_t>(kBrBoot)) return launch_blind_rotate_fft(r, static_cast<int>(per), sm_count, st);
     const int b = tail <= c6_max_clusters() ? -2
                   : tail <= static_cast<uint32_t>(sm_count / 2) ? -1
                   : tail <= static_cast<uint32_t>(sm_count) ? 0

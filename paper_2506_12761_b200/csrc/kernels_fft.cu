@@ -188,21 +188,84 @@ __device__ __forceinline__ uint32_t round_u32s(double v, const Lane& c) {
   return static_cast<uint32_t>(__double2loint((A & 1) ? fma(c.sgn, v, 6755399441055744.0) : v + 6755399441055744.0));
 }
 
-// TMEM (32x32b: lane = thread): one double <-> 2 consecutive columns (lo, hi word).  x2 ops take the double's own
-// aligned register pair, so no register moves are needed to gather operands (an x16 op needs 16 consecutive
-// registers and cost ~2 moves per word).  Loads are asynchronous until tcgen05.wait::ld.
-__device__ __forceinline__ void tm_st_d(uint32_t ta, double v) {
-  asm volatile("{ .reg .b32 lo, hi; mov.b64 {lo, hi}, %1; tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {lo, hi}; }" ::"r"(ta),
-               "d"(v)
-               : "memory");
+// TMEM (32x32b: lane = thread): one double <-> 2 consecutive columns (lo, hi word).  Each helper is one asm block
+// whose 32-bit temporaries ptxas allocates onto the doubles' own register pairs (no gather moves), with the
+// tcgen05.wait::ld inside the block, before the temporaries are read.
+__device__ __forceinline__ void tm_ld8d(uint32_t ta, double (&v)[8]) {
+  asm volatile(
+      "{\n .reg .b32 t<16>;\n"
+      " tcgen05.ld.sync.aligned.32x32b.x16.b32 {t0,t1,t2,t3,t4,t5,t6,t7,t8,t9,t10,t11,t12,t13,t14,t15}, [%8];\n"
+      " tcgen05.wait::ld.sync.aligned;\n"
+      " mov.b64 %0, {t0,t1};\n"
+      " mov.b64 %1, {t2,t3};\n"
+      " mov.b64 %2, {t4,t5};\n"
+      " mov.b64 %3, {t6,t7};\n"
+      " mov.b64 %4, {t8,t9};\n"
+      " mov.b64 %5, {t10,t11};\n"
+      " mov.b64 %6, {t12,t13};\n"
+      " mov.b64 %7, {t14,t15};\n"
+      "}\n"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+      : "r"(ta)
+      : "memory");
 }
-__device__ __forceinline__ void tm_ld_d(uint32_t ta, double& v) {
-  asm volatile("{ .reg .b32 lo, hi; tcgen05.ld.sync.aligned.32x32b.x2.b32 {lo, hi}, [%1]; mov.b64 %0, {lo, hi}; }"
-               : "=d"(v)
-               : "r"(ta)
-               : "memory");
+__device__ __forceinline__ void tm_st8d(uint32_t ta, const double (&v)[8]) {
+  asm volatile(
+      "{\n .reg .b32 t<16>;\n"
+      " mov.b64 {t0,t1}, %1;\n"
+      " mov.b64 {t2,t3}, %2;\n"
+      " mov.b64 {t4,t5}, %3;\n"
+      " mov.b64 {t6,t7}, %4;\n"
+      " mov.b64 {t8,t9}, %5;\n"
+      " mov.b64 {t10,t11}, %6;\n"
+      " mov.b64 {t12,t13}, %7;\n"
+      " mov.b64 {t14,t15}, %8;\n"
+      " tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {t0,t1,t2,t3,t4,t5,t6,t7,t8,t9,t10,t11,t12,t13,t14,t15};\n"
+      "}\n" ::"r"(ta),
+      "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "d"(v[4]), "d"(v[5]), "d"(v[6]), "d"(v[7])
+      : "memory");
 }
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_ld_col16(uint32_t ta, cd (&V)[16]) {
+  asm volatile(
+      "{\n .reg .b32 t<64>;\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t0,t1,t2,t3}, [%32];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t4,t5,t6,t7}, [%33];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t8,t9,t10,t11}, [%34];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t12,t13,t14,t15}, [%35];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t16,t17,t18,t19}, [%36];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t20,t21,t22,t23}, [%37];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t24,t25,t26,t27}, [%38];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t28,t29,t30,t31}, [%39];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t32,t33,t34,t35}, [%40];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t36,t37,t38,t39}, [%41];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t40,t41,t42,t43}, [%42];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t44,t45,t46,t47}, [%43];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t48,t49,t50,t51}, [%44];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t52,t53,t54,t55}, [%45];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t56,t57,t58,t59}, [%46];\n"
+      " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t60,t61,t62,t63}, [%47];\n"
+      " tcgen05.wait::ld.sync.aligned;\n"
+      " mov.b64 %0, {t0,t1};\n mov.b64 %1, {t2,t3};\n"
+      " mov.b64 %2, {t4,t5};\n mov.b64 %3, {t6,t7};\n"
+      " mov.b64 %4, {t8,t9};\n mov.b64 %5, {t10,t11};\n"
+      " mov.b64 %6, {t12,t13};\n mov.b64 %7, {t14,t15};\n"
+      " mov.b64 %8, {t16,t17};\n mov.b64 %9, {t18,t19};\n"
+      " mov.b64 %10, {t20,t21};\n mov.b64 %11, {t22,t23};\n"
+      " mov.b64 %12, {t24,t25};\n mov.b64 %13, {t26,t27};\n"
+      " mov.b64 %14, {t28,t29};\n mov.b64 %15, {t30,t31};\n"
+      " mov.b64 %16, {t32,t33};\n mov.b64 %17, {t34,t35};\n"
+      " mov.b64 %18, {t36,t37};\n mov.b64 %19, {t38,t39};\n"
+      " mov.b64 %20, {t40,t41};\n mov.b64 %21, {t42,t43};\n"
+      " mov.b64 %22, {t44,t45};\n mov.b64 %23, {t46,t47};\n"
+      " mov.b64 %24, {t48,t49};\n mov.b64 %25, {t50,t51};\n"
+      " mov.b64 %26, {t52,t53};\n mov.b64 %27, {t54,t55};\n"
+      " mov.b64 %28, {t56,t57};\n mov.b64 %29, {t58,t59};\n"
+      " mov.b64 %30, {t60,t61};\n mov.b64 %31, {t62,t63};\n"
+      "}\n"
+      : "=d"(V[0].x), "=d"(V[0].y), "=d"(V[1].x), "=d"(V[1].y), "=d"(V[2].x), "=d"(V[2].y), "=d"(V[3].x), "=d"(V[3].y), "=d"(V[4].x), "=d"(V[4].y), "=d"(V[5].x), "=d"(V[5].y), "=d"(V[6].x), "=d"(V[6].y), "=d"(V[7].x), "=d"(V[7].y), "=d"(V[8].x), "=d"(V[8].y), "=d"(V[9].x), "=d"(V[9].y), "=d"(V[10].x), "=d"(V[10].y), "=d"(V[11].x), "=d"(V[11].y), "=d"(V[12].x), "=d"(V[12].y), "=d"(V[13].x), "=d"(V[13].y), "=d"(V[14].x), "=d"(V[14].y), "=d"(V[15].x), "=d"(V[15].y)
+      : "r"(ta + 0u), "r"(ta + 16u), "r"(ta + 32u), "r"(ta + 48u), "r"(ta + 64u), "r"(ta + 80u), "r"(ta + 96u), "r"(ta + 112u), "r"(ta + 128u), "r"(ta + 144u), "r"(ta + 160u), "r"(ta + 176u), "r"(ta + 192u), "r"(ta + 208u), "r"(ta + 224u), "r"(ta + 240u)
+      : "memory");
+}
 // MAC of one key chunk (digit row r, registers 8h .. 8h + 7): acc[o][l] (+)= X * B_r[o][l] per point, the
 // accumulators (doubles, re/im, ol = o * 2 + l) at TMEM columns rho * 16 + ol * 4 + {0: re, 2: im}.
 template <bool FIRST>
@@ -211,12 +274,8 @@ __device__ __forceinline__ void mac_half(const cd (&X)[16], int h, const double2
   for (int rp = 0; rp < 8; rp++) {
     const int rho = 8 * h + rp;
     const uint32_t ta = tm + rho * 16;
-    double ac[8];
-    if (!FIRST) {
-#pragma unroll
-      for (int q = 0; q < 8; q++) tm_ld_d(ta + 2 * q, ac[q]);
-      tm_wait_ld();
-    }
+    double ac[8];  // [ol][re, im]
+    if (!FIRST) tm_ld8d(ta, ac);
 #pragma unroll
     for (int ol = 0; ol < 4; ol++) {
       const double2 k = kc[(rp * 4 + ol) * 32];
@@ -228,8 +287,7 @@ __device__ __forceinline__ void mac_half(const cd (&X)[16], int h, const double2
         ac[2 * ol + 1] = fma(X[rho].x, k.y, fma(X[rho].y, k.x, ac[2 * ol + 1]));
       }
     }
-#pragma unroll
-    for (int q = 0; q < 8; q++) tm_st_d(ta + 2 * q, ac[q]);
+    tm_st8d(ta, ac);
   }
 }
 
@@ -402,12 +460,7 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
 #pragma unroll 1
       for (int ol = 0; ol < 4; ol++) {
         cd V[16];
-#pragma unroll
-        for (int r = 0; r < 16; r++) {
-          tm_ld_d(tm + r * 16 + ol * 4, V[r].x);
-          tm_ld_d(tm + r * 16 + ol * 4 + 2, V[r].y);
-        }
-        tm_wait_ld();
+        tm_ld_col16(tm + ol * 4, V);
         fft_inv(V, lc, tr);
         uint32_t* ao = acc + (ol >> 1) * N + lane;
         const uint32_t sh = (ol & 1) * 16u;

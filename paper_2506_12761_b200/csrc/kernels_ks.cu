@@ -4,7 +4,7 @@
 // Definition (R6): for each coefficient i < 1024 of the N-LWE a', abar_i = floor((a'_i + 2^15) / 2^16) mod 2^16 and
 // its 8 base-4 digits d_ij (field f = 7 - j holds bits 2f, 2f + 1); out = (0, b') - sum_{i,j: d_ij != 0}
 // ksk[i][j][d_ij].  Written as a GEMM: D[c][n] = sum_k ind[c][k] * kmat[n][k] with the one-hot digit indicator
-// ind[c][k] = [d_ij(c) = v] at k = (v - 1) * 8192 + i * 8 + f (K = 24576) and kmat the ksk split into 4 balanced
+// ind[c][k] = [d_ij(c) = v] at k = ((i / 16) * 3 + v - 1) * 128 + (i % 16) * 8 + f (K = 24576) and kmat the ksk split into 4 balanced
 // signed byte limbs, n = col * 4 + limb (N = 2528, padded to 2560).  |D| <= 8192 * 128 < 2^31: exact; then
 // out[col] = (col == 630 ? b' : 0) - sum_l D[c][4 col + l] 2^(8l) mod 2^32 -- bit-identical to the definition.
 //
@@ -180,13 +180,23 @@ __global__ void __launch_bounds__(kKsThreads, 1) vlp_ks_gemm_kernel(const KsArgs
       const uint32_t c = mt * kKsTileM + r;
       const bool valid = c < cnt;
       const uint4* arow = reinterpret_cast<const uint4*>(abuf + static_cast<size_t>(valid ? c : 0) * N);
+      // K blocks are ordered (coefficient block, digit value): kb = (i0 / 16) * 3 + v - 1, so the 16 abar words of
+      // a coefficient block serve 3 consecutive blocks; they are loaded one coefficient block ahead.
+      uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0, w0 = n0, w1 = n0;
+      if (valid) {
+        n0 = __ldg(arow);
+        n1 = __ldg(arow + 1);
+      }
       for (uint32_t kb = 0; kb < static_cast<uint32_t>(kKsKBlocks); kb++, it++) {
         const uint32_t s = it % kKsStages, ph = (it / kKsStages) & 1u;
-        const uint32_t v = kb / 64 + 1, i0 = (kb % 64) * 16;  // digit value, first coefficient of the block
-        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
-        if (valid) {
-          w0 = __ldg(arow + i0 / 8);
-          w1 = __ldg(arow + i0 / 8 + 1);
+        const uint32_t v = kb % 3 + 1, ib = kb / 3;  // digit value, coefficient block (16 coefficients)
+        if (v == 1) {
+          w0 = n0;
+          w1 = n1;
+          if (valid && ib + 1 < static_cast<uint32_t>(N / 16)) {
+            n0 = __ldg(arow + 2 * (ib + 1));
+            n1 = __ldg(arow + 2 * (ib + 1) + 1);
+          }
         }
         const uint32_t pat = v * 0x55555555u;  // v in every 2-bit field
         const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};  // 2 coefficients each
@@ -254,7 +264,8 @@ __global__ void __launch_bounds__(kKsThreads, 1) vlp_ks_gemm_kernel(const KsArgs
 
 // ================================================================================ setup: kmat in UMMA order
 // kmat_sw[nt][kb][r][128 B] (SWIZZLE_128B: 16-byte chunk c of row r at (c ^ (r & 7)) * 16); row n = nt * 256 + r =
-// col * 4 + limb, byte k = kb * 128 + b = (v - 1) * 8192 + i * 8 + f -> ksk[i][j = 7 - f][v - 1][col]'s limb.
+// col * 4 + limb; K block kb = (coefficient block ib, digit value v): kb = ib * 3 + v - 1, byte b of the block ->
+// coefficient i = ib * 16 + b / 8, field f = b % 8 -> ksk[i][j = 7 - f][v - 1][col]'s limb.
 __global__ void vlp_kmat_sw_kernel(const uint32_t* __restrict__ ksk, int8_t* __restrict__ out) {
   const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // one 4-byte group per thread
   const size_t total = static_cast<size_t>(kKsNt) * kKsKBlocks * kKsTileN * (kKsBlockK / 4);
@@ -268,8 +279,8 @@ __global__ void vlp_kmat_sw_kernel(const uint32_t* __restrict__ ksk, int8_t* __r
   uint32_t packed = 0;
 #pragma unroll
   for (int e = 0; e < 4; e++) {
-    const uint32_t k = kb * kKsBlockK + b4 * 4 + e;
-    const uint32_t vi = k / 8192, rem = k % 8192, i = rem / 8, f = rem % 8, j = 7 - f;
+    const uint32_t b = b4 * 4 + e;  // byte within the block: coefficient ib * 16 + b / 8, field b % 8
+    const uint32_t vi = kb % 3, i = (kb / 3) * 16 + b / 8, f = b % 8, j = 7 - f;
     int32_t limb = 0;
     if (col < static_cast<uint32_t>(kCt)) {
       int64_t x = static_cast<int64_t>(ksk[((static_cast<size_t>(i) * kKsT + j) * 3 + vi) * kCt + col]);

@@ -88,11 +88,11 @@ def test_fft_engine_full_630_and_extreme_digits(server, okeys, route):
     assert np.array_equal(A.to_host(server.debug_blind_rotate(A.to_device(cts), 630)), got)
 
 
-@pytest.mark.parametrize("extra", [0, 1, 150, 1183])
+@pytest.mark.parametrize("extra", [0, 1, 150, 900, 1183])
 def test_default_route_wave_and_tail_bit_exact(server, okeys, extra):
-    """The default routing of a level (K2F whole waves of 8 x SMs, then the tail on K2F with fewer warps or on the
-    NTT latency kernels): 2 CMux steps on 8 x 148 + extra inputs; sampled rows on both sides of the split and the
-    ragged end byte-equal to the oracle."""
+    """The default routing of a level (K2F whole waves of 8 x SMs, then the tail: <= 1 per SM on the NTT latency /
+    cluster kernels, 2-5 per SM on NTT K2<b>, 6-8 per SM on K2F with that many warps): 2 CMux steps on 8 x 148 +
+    extra inputs; sampled rows on both sides of the split and the ragged end byte-equal to the oracle."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     count = 8 * sms + extra
     rng = np.random.default_rng(100 + extra)

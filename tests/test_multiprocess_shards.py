@@ -94,3 +94,69 @@ def test_two_rank_gloo_shards_equal_single_shot(tmp_path):
     R1, _, _ = C.velopir(C.TfheBackend(keys), C.MODE_INTV, q, recs, pays, L_I, 1, L_S, FLAGS)
     assert np.array_equal(R2[:, :631], np.stack(R1)[:, :631])
     assert P.decrypt_bits(keys, R1) == C.plain_result(C.MODE_INTV, QUERY, RECORDS, PAYLOADS, 1, FLAGS)
+
+
+# ----------------------------------------------------------------------------------- the library's shard path
+def _gpu_worker(rank, world, port, cfg, out_path):
+    """One rank of dist.sharded_step with the real library on cuda:0: the rank's shard is built by the device
+    preprocessing calls and evaluated by vlp_server_eval; the query broadcast and the root gather are gloo (CPU
+    tensors, staged around the device calls); rank 0 runs vlp_server_combine.  The ranks' kernels never wait on one
+    another (each evaluates an independent shard), so running them as processes on one GPU is safe."""
+    import torch
+    from paper_2506_12761_b200 import api as A
+    from synth import make_workload
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl = make_workload(cfg)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    keys = A.Keys(wl.key_seed)
+    srv = A.Server(keys, 0)
+    first, count = shard_range(wl.M, world, rank)
+    pk = A.pubkeygen_device(keys, m, wl.key_seed + 1, first, count)
+    db = A.server_encrypt_db_device(m, pk, wl.records[first:first + count], wl.payloads[first:first + count])
+    nq = wl.l_I * (1 if wl.mode == 2 else wl.d)
+    q = torch.from_numpy(keys.encrypt_query(m, wl.query, 7).view(np.int32)) if rank == 0 else \
+        torch.zeros((nq, 632), dtype=torch.int32)
+
+    def eval_shard(qc):
+        out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+        srv.eval(m, qc.to("cuda:0"), db, out, first=first, count=count)
+        return out.cpu()
+
+    def combine(roots):
+        out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+        srv.combine(m, world, roots.to("cuda:0"), out)
+        return out.cpu()
+
+    R = sharded_step(q, eval_shard, combine, world, rank)
+    if rank == 0:
+        np.save(out_path, R.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,world", [(2, 2), (2, 4), (3, 2), (3, 4)])
+def test_library_shards_on_ranks_equal_single_shot(tmp_path, cfg, world):
+    """SURVEY 8(e) / R15 with the real library: `world` processes each evaluate a contiguous power-of-two shard
+    of config `cfg` through dist.sharded_step (broadcast -> vlp_server_eval -> gather to rank 0 ->
+    vlp_server_combine); the result is byte-identical to one vlp_server_eval over all records and decrypts to the
+    plain predicate."""
+    import torch
+    from paper_2506_12761_b200 import api as A
+    from synth import make_workload
+    from synth.workloads import expected_result
+    out = str(tmp_path / "R.npy")
+    mp.spawn(_gpu_worker, args=(world, _free_port(), cfg, out), nprocs=world, join=True)
+    Rg = np.load(out).view(np.uint32)
+    wl = make_workload(cfg)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    keys = A.Keys(wl.key_seed)
+    srv = A.Server(keys, 0)
+    db = A.encrypt_db_device(keys, m, wl.records, wl.payloads, pk_seed=wl.key_seed + 1)
+    q = A.to_device(keys.encrypt_query(m, wl.query, 7))
+    R1 = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+    srv.eval(m, q, db, R1)
+    R1 = A.to_host(R1)
+    assert np.array_equal(Rg, R1)
+    assert keys.decrypt_value(R1) == expected_result(wl)
