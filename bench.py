@@ -284,7 +284,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3,
                     help="1-4: BASELINE.json configs; 5: NAND sweep; 6-9: synthetic stand-ins shaped like the paper's "
-                         "datasets (covid-kor, covid-usa, gdacs, weather-usa; synth/workloads.py)")
+                         "datasets (covid-kor, covid-usa, gdacs, weather-usa); 10: paper CoV on 4096 points "
+                         "(synth/workloads.py)")
     ap.add_argument("--nand", type=int, default=1 << 17, help="config 5: NAND gates per step (split over ranks)")
     ap.add_argument("--queries", type=int, default=1,
                     help="queries per step (multi-query packing on one GPU: every level launch carries all of them)")
@@ -314,7 +315,12 @@ def main():
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
+        # NCCL communicator init lines on stderr (the rank count is visible in the driver's log)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(dev))
+        if rank == 0:
+            print(f"[bench] torch.distributed nccl process group: world_size={world}", file=sys.stderr, flush=True)
     stream = torch.cuda.current_stream()
 
     from paper_2506_12761_b200.dist import shard_range, sharded_step

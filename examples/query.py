@@ -2,8 +2,9 @@
 
     python examples/query.py [--records 256] [--mode intv|cov|idm]
 
-Client: keygen, PubKeyGen, query encryption, decryption.  Server: evaluation key upload, ServerEnc
-(on the GPU here), server_eval.  The result is checked against the plaintext predicate.
+Client: keygen, PubKeyGen, query encryption, decryption -- all from OS randomness (the *_secure calls;
+the seeded calls are the reproducible test / benchmark mode).  Server: evaluation key upload, ServerEnc (from the
+client's public-key samples only), server_eval.  The result is checked against the plaintext predicate.
 """
 import argparse
 import os
@@ -42,10 +43,10 @@ def main():
     m = A.meta(mode, M, l_I, l_S, d)
 
     t0 = time.time()
-    keys = A.Keys(seed=2024)                      # client: secret key + evaluation key
-    server = A.Server(keys, device=0)             # server: evk on the GPU (bsk -> NTT domain)
-    db = A.encrypt_db_device(keys, m, records, payloads, pk_seed=7)  # PubKeyGen + ServerEnc
-    q = A.to_device(keys.encrypt_query(m, query, seed=11))            # client: encrypted query
+    keys = A.Keys()                               # client: secret key + evaluation key (OS randomness)
+    server = A.Server(keys, device=0)             # server: evk on the GPU (bsk -> FFT / NTT domains)
+    db = A.to_device(keys.encrypt_db(m, records, payloads))  # client PubKeyGen (OS randomness) + server ServerEnc
+    q = A.to_device(keys.encrypt_query(m, query))            # client: encrypted query (OS randomness)
     out = torch.zeros((l_S, A.CT_STRIDE), dtype=torch.int32, device="cuda:0")
     torch.cuda.synchronize()
     server.eval(m, q, db, out)                    # first call compiles and caches the level schedule

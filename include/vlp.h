@@ -106,10 +106,18 @@ const char* vlp_last_error(void);
 /* Fills the 128-bit parameter set of tab:tfhe_params; sigma_lwe = 2^-15 (R2). */
 int vlp_params_tfhe128(vlp_params* out);
 
+/* Randomness.  Every seeded call (a `seed` argument) is byte-reproducible from its 64-bit seed through the counter
+ * PRNG of R3: the test / benchmark mode, whose keys and noise are only as secret as the
+ * seed -- do NOT use it to protect data.  The *_secure calls draw a fresh 256-bit key from the OS (getrandom) per
+ * call and generate every mask, noise and key bit with ChaCha20 (RFC 8439) under it; the algorithms and layouts are
+ * the same.  VLP_EINVAL if the OS has no randomness to give. */
+
 /* KeyGen.  Host.  s in B^630, ring key z in B^1024 (R4), bsk (630 TRGSW,
  * rows r = u*3 + j, R4) and ksk ([1024][8][3] TLWE samples, R6), all from `seed` (R3).
  * Only the default parameter set is supported (VLP_EINVAL otherwise). */
 int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk, vlp_evk** evk);
+/* KeyGen from OS randomness (see "Randomness"). */
+int vlp_keygen_secure(const vlp_params* params, vlp_sk** sk, vlp_evk** evk);
 /* Copies of the key material for the byte-equality tests: s[630], z[1024] as 0/1 words;
  * bsk[630][6][2][1024] torus32; ksk[1024][8][3][631] torus32.  Any pointer may be NULL. */
 int vlp_sk_export(const vlp_sk* sk, uint32_t* s, uint32_t* z);
@@ -124,6 +132,9 @@ int vlp_encrypt_bits(const vlp_sk* sk, const uint8_t* bits, size_t count, uint64
  * VLP_ERANGE if a value >= 2^l_I. */
 int vlp_encrypt_query(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint64_t seed,
                       uint32_t* out);
+/* The same encryptions from OS randomness (see "Randomness"). */
+int vlp_encrypt_query_secure(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint32_t* out);
+int vlp_encrypt_bits_secure(const vlp_sk* sk, const uint8_t* bits, size_t count, uint32_t* out);
 /* Dec: bit = [int32(b - <a, s>) > 0] (ties -> 0, R18).  Host. */
 int vlp_decrypt_bits(const vlp_sk* sk, const uint32_t* ct, size_t count, uint8_t* bits_out);
 
@@ -132,6 +143,11 @@ int vlp_decrypt_bits(const vlp_sk* sk, const uint32_t* ct, size_t count, uint8_t
  * then pk^S, materialised on the host (the client sends them to the server).  Multi-threaded. */
 int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
                   vlp_pk** pk);
+/* PubKeyGen from OS randomness (see "Randomness"). */
+int vlp_pubkeygen_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, size_t count, vlp_pk** pk);
+/* Test hook: one ChaCha20 block (RFC 8439 section 2.3) -- key[8], counter, nonce[3] -> out[16] (words, little
+ * endian), to pin the secure generator against an independent implementation. */
+int vlp_debug_chacha20_block(const uint32_t* key, uint32_t counter, const uint32_t* nonce, uint32_t* out);
 /* Ciphertexts per record in the encrypted DB: W * l_I + l_S. */
 int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);
 /* alg:ServerEnc for the pk's records: ct = (0, Ecd(bit)) + pk sample.

@@ -59,6 +59,11 @@ SIGNATURES = {
     "vlp_last_error": (ctypes.c_char_p, []),
     "vlp_params_tfhe128": (_i, [ctypes.POINTER(VlpParams)]),
     "vlp_keygen": (_i, [_u64, ctypes.POINTER(VlpParams), _pp, _pp]),
+    "vlp_keygen_secure": (_i, [ctypes.POINTER(VlpParams), _pp, _pp]),
+    "vlp_encrypt_query_secure": (_i, [_vp, ctypes.POINTER(VlpMeta), _u64p, _u32p]),
+    "vlp_encrypt_bits_secure": (_i, [_vp, ctypes.POINTER(ctypes.c_uint8), _sz, _u32p]),
+    "vlp_pubkeygen_secure": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _pp]),
+    "vlp_debug_chacha20_block": (_i, [_u32p, ctypes.c_uint32, _u32p, _u32p]),
     "vlp_sk_export": (_i, [_vp, _u32p, _u32p]),
     "vlp_evk_export": (_i, [_vp, _u32p, _u32p]),
     "vlp_encrypt_bits": (_i, [_vp, _u8p, _sz, _u64, _u64, _u32p]),

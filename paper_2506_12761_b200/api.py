@@ -38,11 +38,17 @@ def _stream_handle(stream, device=None) -> int:
 class Keys:
     """vlp_keygen: secret key + evaluation key, host side."""
 
-    def __init__(self, seed: int, device: int | None = None):
-        """Host KeyGen (vlp_keygen), or with device= the byte-identical device KeyGen (vlp_keygen_device)."""
+    def __init__(self, seed: int | None = None, device: int | None = None):
+        """KeyGen.  seed=None (the default): fresh keys from OS randomness (vlp_keygen_secure).  An integer seed: the
+        reproducible test / benchmark keys of vlp_keygen (only as secret as the seed), on the host, or with device=
+        the byte-identical device KeyGen (vlp_keygen_device)."""
         self.seed = seed
         sk, evk = ctypes.c_void_p(), ctypes.c_void_p()
-        if device is None:
+        if seed is None:
+            if device is not None:
+                raise ValueError("the device KeyGen is the seeded (test / benchmark) mode: pass a seed")
+            check(lib().vlp_keygen_secure(None, ctypes.byref(sk), ctypes.byref(evk)))
+        elif device is None:
             check(lib().vlp_keygen(seed, None, ctypes.byref(sk), ctypes.byref(evk)))
         else:
             import torch
@@ -67,18 +73,26 @@ class Keys:
         check(lib().vlp_evk_export(self.evk, _u32p(bsk), _u32p(ksk)))
         return s, z, bsk.reshape(L.n, 6, 2, L.N), ksk.reshape(L.N, 8, 3, L.n + 1)
 
-    def encrypt_bits(self, bits, seed: int, obj0: int = 0) -> np.ndarray:
+    def encrypt_bits(self, bits, seed: int | None = None, obj0: int = 0) -> np.ndarray:
+        """Fresh encryptions; seed=None: OS randomness (vlp_encrypt_bits_secure), else the seeded test mode."""
         bits = np.ascontiguousarray(np.asarray(bits, dtype=np.uint8))
         out = np.zeros((len(bits), CT_STRIDE), np.uint32)
-        check(lib().vlp_encrypt_bits(self.sk, bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), len(bits),
-                                     seed, obj0, _u32p(out)))
+        bp = bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+        if seed is None:
+            check(lib().vlp_encrypt_bits_secure(self.sk, bp, len(bits), _u32p(out)))
+        else:
+            check(lib().vlp_encrypt_bits(self.sk, bp, len(bits), seed, obj0, _u32p(out)))
         return out
 
-    def encrypt_query(self, m: VlpMeta, values, seed: int) -> np.ndarray:
+    def encrypt_query(self, m: VlpMeta, values, seed: int | None = None) -> np.ndarray:
+        """encrypt_query; seed=None: OS randomness (vlp_encrypt_query_secure), else the seeded test mode."""
         vals = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
         words = 1 if m.mode == L.MODE_IDM else m.d
         out = np.zeros((words * m.l_I, CT_STRIDE), np.uint32)
-        check(lib().vlp_encrypt_query(self.sk, ctypes.byref(m), _u64p(vals), seed, _u32p(out)))
+        if seed is None:
+            check(lib().vlp_encrypt_query_secure(self.sk, ctypes.byref(m), _u64p(vals), _u32p(out)))
+        else:
+            check(lib().vlp_encrypt_query(self.sk, ctypes.byref(m), _u64p(vals), seed, _u32p(out)))
         return out
 
     def decrypt_bits(self, ct: np.ndarray) -> np.ndarray:
@@ -100,8 +114,10 @@ class Keys:
     def decrypt_value(self, ct: np.ndarray) -> int:  # any l_S (Python int)
         return int(sum(int(b) << j for j, b in enumerate(self.decrypt_bits(ct))))
 
-    def encrypt_db(self, m: VlpMeta, words, payloads, pk_seed: int, first: int = 0, count: int | None = None):
-        """Client PubKeyGen (alg:PubKeyGen) + server ServerEnc (alg:ServerEnc) for records [first, first+count)."""
+    def encrypt_db(self, m: VlpMeta, words, payloads, pk_seed: int | None = None, first: int = 0,
+                   count: int | None = None):
+        """Client PubKeyGen (alg:PubKeyGen) + server ServerEnc (alg:ServerEnc) for records [first, first+count);
+        pk_seed=None: the pk from OS randomness (vlp_pubkeygen_secure), else the seeded test mode."""
         words = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
         count = len(payloads) if count is None else count
         pw = (m.l_S + 63) // 64  # payload words per record (l_S up to 128)
@@ -111,7 +127,10 @@ class Keys:
             payloads = np.array([[(int(v) >> (64 * w)) & (2 ** 64 - 1) for w in range(pw)] for v in payloads],
                                 dtype=np.uint64)
         pk = ctypes.c_void_p()
-        check(lib().vlp_pubkeygen(self.sk, ctypes.byref(m), pk_seed, first, count, ctypes.byref(pk)))
+        if pk_seed is None:
+            check(lib().vlp_pubkeygen_secure(self.sk, ctypes.byref(m), first, count, ctypes.byref(pk)))
+        else:
+            check(lib().vlp_pubkeygen(self.sk, ctypes.byref(m), pk_seed, first, count, ctypes.byref(pk)))
         try:
             per = record_cts(m)
             out = np.zeros((count * per, CT_STRIDE), np.uint32)

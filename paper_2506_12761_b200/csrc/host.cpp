@@ -1,9 +1,14 @@
 // host.cpp -- client-side and preprocessing calls of the C ABI (include/vlp.h): parameters, KeyGen,
-// TLWE encryption / decryption, PubKeyGen, ServerEnc.  Host C++, deterministic in the seeds (R3).
+// TLWE encryption / decryption, PubKeyGen, ServerEnc.  Host C++.  The seeded calls are deterministic in their
+// 64-bit seed (R3: reproducible test / benchmark mode, not secret); the *_secure calls draw a fresh 256-bit key
+// from the OS (getrandom) and use ChaCha20 as the counter generator.
 //
 // Independent of the test oracle (oracle/): same published conventions, separate
 // code.  The ring products a*z of KeyGen are computed here as sums of rotations X^j * a over the
 // support of the binary key z (the oracle uses an NTT), and are exact mod 2^32.
+#include <sys/random.h>
+
+#include <cerrno>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -33,29 +38,92 @@ uint64_t prng(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word) {
   return mix(h ^ (word * 0x165667B19E3779F9ull));
 }
 
+// ---- ChaCha20 block function (RFC 8439 section 2.3): the keyed counter generator of the secure calls.
+static inline uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+static inline void quarter(uint32_t* x, int a, int b, int c, int d) {
+  x[a] += x[b]; x[d] = rotl32(x[d] ^ x[a], 16);
+  x[c] += x[d]; x[b] = rotl32(x[b] ^ x[c], 12);
+  x[a] += x[b]; x[d] = rotl32(x[d] ^ x[a], 8);
+  x[c] += x[d]; x[b] = rotl32(x[b] ^ x[c], 7);
+}
+void chacha20_block(const uint32_t key[8], uint32_t counter, const uint32_t nonce[3], uint32_t out[16]) {
+  uint32_t in[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key[0], key[1], key[2], key[3],
+                     key[4], key[5], key[6], key[7], counter, nonce[0], nonce[1], nonce[2]};
+  uint32_t x[16];
+  std::memcpy(x, in, sizeof(x));
+  for (int i = 0; i < 10; i++) {
+    quarter(x, 0, 4, 8, 12); quarter(x, 1, 5, 9, 13); quarter(x, 2, 6, 10, 14); quarter(x, 3, 7, 11, 15);
+    quarter(x, 0, 5, 10, 15); quarter(x, 1, 6, 11, 12); quarter(x, 2, 7, 8, 13); quarter(x, 3, 4, 9, 14);
+  }
+  for (int i = 0; i < 16; i++) out[i] = x[i] + in[i];
+}
+
+// The randomness of one call: the seeded counter PRNG (R3; reproducible, 64-bit seed: tests and benchmarks), or
+// ChaCha20 under a 256-bit key drawn from the OS (getrandom) for the *_secure calls.  Either way a random-access
+// generator u64(dom, obj, word); the secure one uses nonce (dom, obj), block counter word / 8.
+struct Rng {
+  uint64_t seed = 0;
+  bool secure = false;
+  uint32_t key[8] = {};
+  uint64_t u64(uint64_t dom, uint64_t obj, uint64_t word) const {
+    if (!secure) return prng(seed, dom, obj, word);
+    const uint32_t nonce[3] = {static_cast<uint32_t>(dom), static_cast<uint32_t>(obj), static_cast<uint32_t>(obj >> 32)};
+    uint32_t blk[16];
+    chacha20_block(key, static_cast<uint32_t>(word >> 3), nonce, blk);
+    const int w = static_cast<int>(word & 7);
+    return static_cast<uint64_t>(blk[2 * w]) | (static_cast<uint64_t>(blk[2 * w + 1]) << 32);
+  }
+  ~Rng() {  // the key does not outlive the call
+    volatile uint32_t* k = key;
+    for (int i = 0; i < 8; i++) k[i] = 0;
+  }
+};
+static Rng seeded(uint64_t seed) {
+  Rng r;
+  r.seed = seed;
+  return r;
+}
+static int os_random(Rng* r) {
+  r->secure = true;
+  size_t got = 0;
+  uint8_t* dst = reinterpret_cast<uint8_t*>(r->key);
+  while (got < sizeof(r->key)) {
+    const ssize_t k = getrandom(dst + got, sizeof(r->key) - got, 0);
+    if (k < 0) {
+      if (errno == EINTR) continue;
+      return fail(VLP_EINVAL, "getrandom failed: no OS randomness for a secure call");
+    }
+    got += static_cast<size_t>(k);
+  }
+  return VLP_OK;
+}
+
 // Box-Muller Gaussian, "N(0, sigma)" (R2, R3); scalar glibc libm, no FMA contraction.
-uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
-  const uint64_t w1 = prng(seed, dom, obj, 2 * t), w2 = prng(seed, dom, obj, 2 * t + 1);
+static uint32_t noise(const Rng& g, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
+  const uint64_t w1 = g.u64(dom, obj, 2 * t), w2 = g.u64(dom, obj, 2 * t + 1);
   const double u1 = (static_cast<double>(w1 >> 11) + 1.0) * 0x1p-53;
   const double u2 = static_cast<double>(w2 >> 11) * 0x1p-53;
   const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
   const long long e = std::llround(z * (sigma * 4294967296.0));
   return static_cast<uint32_t>(static_cast<uint64_t>(e));
 }
+uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
+  return noise(seeded(seed), dom, obj, t, sigma);
+}
 
-static inline uint32_t uniform(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word) {
-  return static_cast<uint32_t>(prng(seed, dom, obj, word) >> 32);
+static inline uint32_t uniform(const Rng& g, uint64_t dom, uint64_t obj, uint64_t word) {
+  return static_cast<uint32_t>(g.u64(dom, obj, word) >> 32);
 }
 
 // TLWE sample: a_i uniform (dom_a, obj, word i), b = <a, s> + mu + e (dom_e, obj, pair 0).
-static void tlwe_sample(const uint32_t* s, uint32_t mu, double sigma, uint64_t seed, uint64_t dom_a,
+static void tlwe_sample(const uint32_t* s, uint32_t mu, double sigma, const Rng& g, uint64_t dom_a,
                         uint64_t dom_e, uint64_t obj, uint32_t* ct) {
   uint32_t b = 0;
   for (int i = 0; i < n; i++) {
-    ct[i] = uniform(seed, dom_a, obj, i);
+    ct[i] = uniform(g, dom_a, obj, i);
     b += ct[i] * s[i];
   }
-  ct[n] = b + mu + noise(seed, dom_e, obj, 0, sigma);
+  ct[n] = b + mu + noise(g, dom_e, obj, 0, sigma);
   ct[n + 1] = 0;
 }
 
@@ -96,11 +164,12 @@ int resolve_params(const vlp_params* params, vlp_params* p) {
   return VLP_OK;
 }
 
-// Binary LWE key s and ring key z (O4): bit 63 of the counter PRNG.
-void secret_keys(uint64_t seed, vlp_sk* sk) {
-  for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(prng(seed, kSkLwe, 0, i) >> 63);
-  for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(prng(seed, kSkRing, 0, j) >> 63);
+// Binary LWE key s and ring key z (O4): bit 63 of the generator.
+static void secret_keys(const Rng& g, vlp_sk* sk) {
+  for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(g.u64(kSkLwe, 0, i) >> 63);
+  for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(g.u64(kSkRing, 0, j) >> 63);
 }
+void secret_keys(uint64_t seed, vlp_sk* sk) { secret_keys(seeded(seed), sk); }
 
 // Host half of vlp_keygen_device: every Gaussian noise word of the evaluation key, exactly the values vlp_keygen
 // draws -- bsk row (i, r) coefficient j at [(i*6 + r)*N + j] (sigma_bk), ksk row idx at [idx] (sigma_ks).
@@ -127,7 +196,7 @@ int vlp_params_tfhe128(vlp_params* p) {
   return VLP_OK;
 }
 
-int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk** evk_out) {
+static int keygen_impl(const Rng& g, const vlp_params* params, vlp_sk** sk_out, vlp_evk** evk_out) {
   if (!sk_out || !evk_out) return fail(VLP_EINVAL, "null output");
   vlp_params p;
   if (int rc = resolve_params(params, &p)) return rc;
@@ -144,7 +213,7 @@ int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk
   }
   sk->params = p;
   evk->params = p;
-  secret_keys(seed, sk);
+  secret_keys(g, sk);
   std::vector<int> support;
   support.reserve(N);
   for (int j = 0; j < N; j++)
@@ -155,14 +224,14 @@ int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk
     const uint64_t obj = ir;
     uint32_t* a = evk->bsk.data() + ir * 2 * N;
     uint32_t* b = a + N;
-    for (int j = 0; j < N; j++) a[j] = uniform(seed, kBskA, obj, j);
+    for (int j = 0; j < N; j++) a[j] = uniform(g, kBskA, obj, j);
     // a*z = sum_{k in supp z} X^k * a  (negacyclic: coefficient i moves to i+k, negated past N)
     for (int j = 0; j < N; j++) b[j] = 0;
     for (int k : support) {
       for (int i = 0; i < N - k; i++) b[i + k] += a[i];
       for (int i = N - k; i < N; i++) b[i + k - N] -= a[i];
     }
-    for (int j = 0; j < N; j++) b[j] += noise(seed, kBskE, obj, j, p.sigma_bk);
+    for (int j = 0; j < N; j++) b[j] += noise(g, kBskE, obj, j, p.sigma_bk);
     const int i = static_cast<int>(ir / kRows), r = static_cast<int>(ir % kRows);
     if (sk->s[i]) (r / kEll == 0 ? a : b)[0] += 1u << (32 - kBgBits * (r % kEll + 1));
   });
@@ -172,11 +241,21 @@ int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk
     const int i = static_cast<int>(idx / (kKsT * 3)), j = static_cast<int>((idx / 3) % kKsT);
     const uint32_t v = static_cast<uint32_t>(idx % 3) + 1;
     const uint32_t mu = v * sk->z[i] * (1u << (32 - kKsBaseBits * (j + 1)));
-    tlwe_sample(sk->s, mu, p.sigma_ks, seed, kKskA, kKskE, idx, evk->ksk.data() + idx * kCt);
+    tlwe_sample(sk->s, mu, p.sigma_ks, g, kKskA, kKskE, idx, evk->ksk.data() + idx * kCt);
   });
   *sk_out = skp.release();
   *evk_out = evkp.release();
   return VLP_OK;
+}
+
+int vlp_keygen(uint64_t seed, const vlp_params* params, vlp_sk** sk_out, vlp_evk** evk_out) {
+  return keygen_impl(seeded(seed), params, sk_out, evk_out);
+}
+
+int vlp_keygen_secure(const vlp_params* params, vlp_sk** sk_out, vlp_evk** evk_out) {
+  Rng g;
+  if (int rc = os_random(&g)) return rc;
+  return keygen_impl(g, params, sk_out, evk_out);
 }
 
 int vlp_sk_export(const vlp_sk* sk, uint32_t* s, uint32_t* z) {
@@ -195,18 +274,27 @@ int vlp_evk_export(const vlp_evk* evk, uint32_t* bsk, uint32_t* ksk) {
   return VLP_OK;
 }
 
-int vlp_encrypt_bits(const vlp_sk* sk, const uint8_t* bits, size_t count, uint64_t seed, uint64_t obj0,
-                     uint32_t* out) {
+static int encrypt_bits_impl(const vlp_sk* sk, const uint8_t* bits, size_t count, const Rng& g, uint64_t obj0,
+                             uint32_t* out) {
   if (!sk || (!bits && count) || (!out && count)) return fail(VLP_EINVAL, "null argument");
   parallel_for(count, [&](size_t i) {
-    tlwe_sample(sk->s, bits[i] ? kMu : 0u - kMu, sk->params.sigma_lwe, seed, kFreshA, kFreshE, obj0 + i,
+    tlwe_sample(sk->s, bits[i] ? kMu : 0u - kMu, sk->params.sigma_lwe, g, kFreshA, kFreshE, obj0 + i,
                 out + i * kCt);
   });
   return VLP_OK;
 }
+int vlp_encrypt_bits(const vlp_sk* sk, const uint8_t* bits, size_t count, uint64_t seed, uint64_t obj0,
+                     uint32_t* out) {
+  return encrypt_bits_impl(sk, bits, count, seeded(seed), obj0, out);
+}
+int vlp_encrypt_bits_secure(const vlp_sk* sk, const uint8_t* bits, size_t count, uint32_t* out) {
+  Rng g;
+  if (int rc = os_random(&g)) return rc;
+  return encrypt_bits_impl(sk, bits, count, g, 0, out);
+}
 
-int vlp_encrypt_query(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint64_t seed,
-                      uint32_t* out) {
+static int encrypt_query_impl(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, const Rng& g,
+                              uint32_t* out) {
   if (!sk || !values || !out) return fail(VLP_EINVAL, "null argument");
   if (int rc = check_meta(meta)) return rc;
   const size_t W = query_words(*meta), l = meta->l_I;
@@ -215,9 +303,18 @@ int vlp_encrypt_query(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* va
   parallel_for(W * l, [&](size_t idx) {
     const size_t w = idx / l, j = idx % l;
     const uint32_t bit = static_cast<uint32_t>((values[w] >> j) & 1);
-    tlwe_sample(sk->s, bit ? kMu : 0u - kMu, sk->params.sigma_lwe, seed, kQryA, kQryE, idx, out + idx * kCt);
+    tlwe_sample(sk->s, bit ? kMu : 0u - kMu, sk->params.sigma_lwe, g, kQryA, kQryE, idx, out + idx * kCt);
   });
   return VLP_OK;
+}
+int vlp_encrypt_query(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint64_t seed,
+                      uint32_t* out) {
+  return encrypt_query_impl(sk, meta, values, seeded(seed), out);
+}
+int vlp_encrypt_query_secure(const vlp_sk* sk, const vlp_meta* meta, const uint64_t* values, uint32_t* out) {
+  Rng g;
+  if (int rc = os_random(&g)) return rc;
+  return encrypt_query_impl(sk, meta, values, g, out);
 }
 
 int vlp_decrypt_bits(const vlp_sk* sk, const uint32_t* ct, size_t count, uint8_t* bits) {
@@ -250,8 +347,8 @@ int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record) {
   return VLP_OK;
 }
 
-int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
-                  vlp_pk** out) {
+static int pubkeygen_impl(const vlp_sk* sk, const vlp_meta* meta, const Rng& g, size_t first, size_t count,
+                          vlp_pk** out) {
   if (!sk || !out) return fail(VLP_EINVAL, "null argument");
   if (int rc = check_meta(meta)) return rc;
   if (first + count > meta->M) return fail(VLP_EINVAL, "record range exceeds M");
@@ -279,10 +376,25 @@ int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t 
     } else {
       local = row;  // W*l_I + j
     }
-    tlwe_sample(sk->s, 0u, sk->params.sigma_lwe, seed, kPkA, kPkE, i * per + local,
+    tlwe_sample(sk->s, 0u, sk->params.sigma_lwe, g, kPkA, kPkE, i * per + local,
                 pk->samples.data() + idx * kCt);
   });
   *out = pk;
+  return VLP_OK;
+}
+int vlp_pubkeygen(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                  vlp_pk** out) {
+  return pubkeygen_impl(sk, meta, seeded(seed), first, count, out);
+}
+int vlp_pubkeygen_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, size_t count, vlp_pk** out) {
+  Rng g;
+  if (int rc = os_random(&g)) return rc;
+  return pubkeygen_impl(sk, meta, g, first, count, out);
+}
+
+int vlp_debug_chacha20_block(const uint32_t* key, uint32_t counter, const uint32_t* nonce, uint32_t* out) {
+  if (!key || !nonce || !out) return fail(VLP_EINVAL, "null argument");
+  chacha20_block(key, counter, nonce, out);
   return VLP_OK;
 }
 

@@ -13,6 +13,8 @@ plane, points / ids are distinct uniform draws, payloads uniform; the query hits
   7 covid-usa shape  IntV d=2 (rectangles)  M=58,  l_I=16, l_S=22
   8 gdacs shape      CoV  d=2 (points)      M=9,   l_I=16, l_S=16
   9 weather-usa shape IdM                   M=304, l_I=16, l_S=128
+ 10 paper CoV (alg:BB2) at scale: M=4096 distinct 16-bit (lat, lon) points, l_I=16, l_S=32; the
+    query is one of the points (probability 3/4) or none ("paper CoV on a 4096-point shape")
 Seeds: keys 1000 + cfg, data 2000 + cfg (overridable).
 """
 from __future__ import annotations
@@ -56,6 +58,7 @@ CONFIGS = {
     7: dict(name="usa_shape_intv2d_58", mode=MODE_INTV, M=58, l_I=16, l_S=22, d=2),
     8: dict(name="gdacs_shape_cov_9", mode=MODE_COV, M=9, l_I=16, l_S=16, d=2),
     9: dict(name="weather_shape_idm_304", mode=MODE_IDM, M=304, l_I=16, l_S=128, d=1),
+    10: dict(name="cov_points_4096", mode=MODE_COV, M=4096, l_I=16, l_S=32, d=2),
 }
 
 
@@ -157,8 +160,8 @@ def make_workload(cfg: int, data_seed: int | None = None, key_seed: int | None =
                 query = [int(rng.integers(0, top)), int(rng.integers(0, top))]
                 if not any(r[0] <= query[0] <= r[1] and r[2] <= query[1] <= r[3] for r in recs.tolist()):
                     break
-    elif cfg in (8, 9):  # distinct points (CoV, d = 2) or distinct ids (IdM)
-        W = 2 if cfg == 8 else 1
+    elif cfg in (8, 9, 10):  # distinct points (CoV, d = 2) or distinct ids (IdM)
+        W = 1 if cfg == 9 else 2
         flat = rng.choice(top ** W, size=M, replace=False)
         recs = np.array([[(int(v) >> (16 * a)) & (top - 1) for a in range(W)] for v in flat], np.uint64)
         if bool(rng.integers(0, 4)) if hits is None else hits > 0:

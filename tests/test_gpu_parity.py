@@ -413,6 +413,15 @@ def test_config4_full_size_sampled(server):
     _full_size_sampled(server, 4, sample, per_level=16)
 
 
+def test_paper_cov_4096_full_size_sampled(server):
+    """the paper's CoV mode (alg:BB2: HomEQ trees on both coordinates + AND) on a
+    4096-point database (config 10): predicate + 8 records (incl. the matching one, if any) byte-equal, and 16
+    random gates of every level recomputed by the oracle from the GPU's own inputs."""
+    wl = make_workload(10, key_seed=SEED)
+    sample = sorted(set(wl.forced[:1] + [0, wl.M - 1] + random.Random(10).sample(range(wl.M), 6)))
+    _full_size_sampled(server, 10, sample, per_level=16)
+
+
 def _contains(wl, i):
     r = [int(v) for v in wl.records[i]]
     return all(r[2 * k] <= int(wl.query[k]) <= r[2 * k + 1] for k in range(wl.d))

@@ -201,3 +201,55 @@ def test_oversized_schedules_are_refused():
     assert L.lib().vlp_program_create(None, ctypes.byref(m), 0, 1 << 23, ctypes.byref(h)) == L.VLP_EINVAL
     assert "too large" in L.lib().vlp_last_error().decode()
     assert L.lib().vlp_program_create_combine(None, ctypes.byref(m), 1 << 20, ctypes.byref(h)) == L.VLP_EINVAL
+
+
+# ----------------------------------------------------------------------------------- secure randomness (ADVICE)
+def test_chacha20_block_matches_independent_implementation():
+    """The secure calls' generator is ChaCha20 (RFC 8439 2.3): vlp_debug_chacha20_block equals the keystream of
+    the `cryptography` package's ChaCha20 (an independent implementation) for random keys, nonces and counters,
+    and the RFC's own block-function example."""
+    import ctypes
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms
+    lib = L.lib()
+    rng = np.random.default_rng(8439)
+    cases = [(np.arange(32, dtype=np.uint8).view(np.uint32), 1,
+              np.frombuffer(bytes.fromhex("000000090000004a00000000"), dtype=np.uint32))]
+    for _ in range(8):
+        cases.append((rng.integers(0, 2 ** 32, 8, dtype=np.uint64).astype(np.uint32), int(rng.integers(0, 2 ** 32)),
+                      rng.integers(0, 2 ** 32, 3, dtype=np.uint64).astype(np.uint32)))
+    for key, ctr, nonce in cases:
+        key, nonce = np.ascontiguousarray(key), np.ascontiguousarray(nonce)
+        out = np.zeros(16, np.uint32)
+        p = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))  # noqa: E731
+        assert lib.vlp_debug_chacha20_block(p(key), ctr, p(nonce), p(out)) == 0
+        full_nonce = np.uint32(ctr).tobytes() + nonce.tobytes()  # cryptography: 4-byte LE counter || 12-byte nonce
+        ks = Cipher(algorithms.ChaCha20(key.tobytes(), full_nonce), mode=None).encryptor().update(bytes(64))
+        assert out.tobytes() == ks
+    # RFC 8439 2.3.2 test vector, first serialized bytes
+    key, ctr, nonce = cases[0]
+    out = np.zeros(16, np.uint32)
+    lib.vlp_debug_chacha20_block(key.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), ctr,
+                                 nonce.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
+    assert out.tobytes()[:16].hex() == "10f1e7e4d13b5915500fdd1fa32071c4"
+
+
+def test_secure_calls_are_fresh_and_correct():
+    """ADVICE (secure randomness): two OS-random KeyGens give different keys; OS-random query encryptions of the
+    same value differ yet decrypt to it; secure encryptions of random bits decrypt correctly; the secure pk
+    encrypts a DB that decrypts to its plaintext bits."""
+    k1, k2 = A.Keys(), A.Keys()
+    s1, z1, _, _ = k1.export()
+    s2, z2, _, _ = k2.export()
+    assert not np.array_equal(s1, s2) and not np.array_equal(z1, z2)
+    assert 200 < int(s1.sum()) < 430 and 400 < int(z1.sum()) < 624  # binary keys, about half ones
+    m = A.meta(L.MODE_INTV, 2, 8, 4, 1)
+    q1, q2 = k1.encrypt_query(m, [173]), k1.encrypt_query(m, [173])
+    assert not np.array_equal(q1, q2)
+    for q in (q1, q2):
+        assert int(sum(int(b) << j for j, b in enumerate(k1.decrypt_bits(q)))) == 173
+    bits = np.random.default_rng(1).integers(0, 2, 64, dtype=np.uint8)
+    assert np.array_equal(k1.decrypt_bits(k1.encrypt_bits(bits)), bits)
+    db = k1.encrypt_db(m, np.array([[3, 9], [0, 200]], np.uint64), np.array([5, 10], np.uint64))
+    want = [(3 >> j) & 1 for j in range(8)] + [(9 >> j) & 1 for j in range(8)] + [(5 >> j) & 1 for j in range(4)]
+    assert list(k1.decrypt_bits(db[:20])) == want
