@@ -78,7 +78,7 @@ int main(void) {
   vlp_meta m = {VLP_MODE_INTV, 4, 4, 3, 1, VLP_CONFIG_FLAGS};
   const uint64_t words[8] = {2, 9, 0, 5, 4, 4, 3, 15}; /* [lo, hi] per record */
   const uint64_t pays[4] = {5, 3, 6, 1};
-  const uint64_t x = 4; /* matches records 0, 2, 3 -> R = 5 ^ 6 ^ 1 = 2 */
+  const uint64_t x = 4; /* lo <= 4 <= hi for all four records -> R = 5 ^ 3 ^ 6 ^ 1 */
   size_t per = 0;
   CHECK(vlp_db_record_cts(&m, &per));
   vlp_pk* pk = NULL;
@@ -118,8 +118,11 @@ int main(void) {
   uint8_t rbits[3];
   uint64_t value = 0;
   CHECK(vlp_decrypt_result(sk, hall, m.l_S, rbits, &value));
-  if (value != (5 ^ 6 ^ 1)) {
-    fprintf(stderr, "R = %llu, want %d\n", (unsigned long long)value, 5 ^ 6 ^ 1);
+  uint64_t want = 0; /* the plain predicate: XOR of the payloads of the records with lo <= x <= hi */
+  for (int i = 0; i < 4; i++)
+    if (words[2 * i] <= x && x <= words[2 * i + 1]) want ^= pays[i];
+  if (value != want) {
+    fprintf(stderr, "R = %llu, want %llu\n", (unsigned long long)value, (unsigned long long)want);
     return 5;
   }
   vlp_free_server(srv);
