@@ -112,16 +112,15 @@ __device__ __forceinline__ cd shfl16(cd v) {
 //    rho then holds k1 = mrev(rho) ^ 8h.  So the registers rho with mrev(rho) < 8 ("A": rho & 2 == 0) hold each
 //    lane's own 8 k1 values and the lane-pair partner (b ^ 16) holds the matching values in register rho | 2 --
 //    the lane-pair radix-2 stage needs no lane-dependent selects (tools/emulate_br_fft.py --v3).
-//  * tw[r] = psi^{b (1 + 4 k1(rho = r))} for r < 8 (the fold twist's psi^b merged in); registers rho and rho + 8
-//    differ by psi^{8b} (tw[8]).
+//  * tw[r] = psi^{b (1 + 4 k1(rho = r))} (the fold twist's psi^b merged in), all 16 held in registers.
 //  * tau = (h ? -1 : 1) w32^bb, the twiddle of the pair's difference (the sign makes both lanes use own - partner).
 struct Lane {
-  cd tw[9];
+  cd tw[16];
   cd tau;
   double sgn, off;  // sgn = h ? -1 : 1; off = -sgn (2^52 + 64) (odd-a digit conversion)
   uint32_t lane, tbase;  // tbase: this lane's transpose offset (8h * kTrStride + bb) in complex
 };
-__device__ __forceinline__ cd twid(const Lane& c, int r) { return r < 8 ? c.tw[r] : cmul(c.tw[r - 8], c.tw[8]); }
+__device__ __forceinline__ cd twid(const Lane& c, int r) { return c.tw[r]; }
 
 // Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
 // 32 q + lane, q < 32) -> v[rho] = point lane + 32 mrev(rho).
@@ -345,12 +344,10 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   {
     const uint32_t h = lane >> 4;
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
+    for (int r = 0; r < 16; r++) {
       const double2 t = a.psi[(lane * (1u + 4u * (static_cast<uint32_t>(mrev(r)) ^ (8u * h)))) & 2047u];
       lc.tw[r] = {t.x, t.y};
     }
-    const double2 t8 = a.psi[(8u * lane) & 2047u];
-    lc.tw[8] = {t8.x, t8.y};
     const double2 w32 = a.psi[(64u * (lane & 15u)) & 2047u];
     lc.sgn = h ? -1.0 : 1.0;
     lc.tau = {lc.sgn * w32.x, lc.sgn * w32.y};
@@ -370,7 +367,7 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   auto release = [&]() {  // this warp is done with ring slot sl
     __syncwarp();
     if (lane == 0) {
-      __threadfence_block();
+      // no fence: this warp's reads of the slot are complete (their values fed the MAC before the release)
       if (atomicAdd(&rel[sl], 1u) == W - 1) {
         atomicExch(&rel[sl], 0u);
         if (nseq + kFSlots < total_chunks) {

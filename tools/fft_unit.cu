@@ -16,11 +16,10 @@ __global__ void fft_unit_kernel(const int* x, const double2* key, const double2*
   __shared__ double2 trb[2 * 16 * kTrStride];
   const uint32_t lane = threadIdx.x, h = lane >> 4;
   Lane lc;
-  for (int r = 0; r < 8; r++) {
+  for (int r = 0; r < 16; r++) {
     const double2 t = psi[(lane * (1u + 4u * (static_cast<uint32_t>(mrev(r)) ^ (8u * h)))) & 2047u];
     lc.tw[r] = {t.x, t.y};
   }
-  lc.tw[8] = {psi[(8u * lane) & 2047u].x, psi[(8u * lane) & 2047u].y};
   const double2 w32 = psi[(64u * (lane & 15u)) & 2047u];
   lc.sgn = h ? -1.0 : 1.0;
   lc.tau = {lc.sgn * w32.x, lc.sgn * w32.y};
