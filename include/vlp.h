@@ -185,6 +185,14 @@ int vlp_server_encrypt_db_device(const vlp_meta* meta, size_t count, const uint3
                                  const uint64_t* payloads, uint32_t* out_dev, void* scratch_dev, size_t scratch_bytes,
                                  uint64_t stream);
 
+/* load records: the server's ServerEnc of a received host pk (vlp_pubkeygen / _secure) straight into
+ * device memory -- the pk's samples are uploaded into db_dev ([pk count][per_record][632], record pk->first at row
+ * 0) and (0, Ecd(bit)) is added on the device; marks the pk used (a second call: VLP_EPKUSED) and frees its host
+ * samples.  words / payloads as in vlp_server_encrypt_db.  scratch_dev as vlp_server_encrypt_db_device.
+ * Synchronous.  Needs no secret key. */
+int vlp_server_load_records(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* db_dev,
+                            void* scratch_dev, size_t scratch_bytes, uint64_t stream);
+
 /* Device PubKeyGen + ServerEnc fused (both roles on one machine, e.g. to build benchmark DBs): the encrypted DB of records [first, first+count) written straight to out_dev ([count][per_record]
  * [632], the vlp_server_encrypt_db layout), byte-identical to vlp_pubkeygen(sk, meta, pk_seed, first, count)
  * followed by vlp_server_encrypt_db.  The Gaussian noise is drawn on the host (the same libm Box-Muller),

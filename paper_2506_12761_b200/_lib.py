@@ -79,6 +79,7 @@ SIGNATURES = {
     "vlp_pubkeygen_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_pubkeygen_device": (_i, [_vp, ctypes.POINTER(VlpMeta), _u64, _sz, _sz, _vp, _vp, _sz, _u64]),
     "vlp_server_encrypt_db_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_server_load_records": (_i, [_vp, _u64p, _u64p, _vp, _vp, _sz, _u64]),
     "vlp_server_encrypt_db_device": (_i, [ctypes.POINTER(VlpMeta), _sz, _vp, _u64p, _u64p, _vp, _vp, _sz, _u64]),
     "vlp_server_evk_bytes": (_sz, []),
     "vlp_server_create": (_i, [_i, _vp, _vp, _sz, _u64, _pp]),

@@ -140,6 +140,41 @@ class Keys:
         return out
 
 
+class PublicKey:
+    """alg:PubKeyGen's single-use samples (vlp_pk), held on the host until the server consumes them."""
+
+    def __init__(self, keys: "Keys", m: VlpMeta, first: int, count: int, seed: int | None = None):
+        self.m, self.first, self.count = m, first, count
+        h = ctypes.c_void_p()
+        if seed is None:
+            check(lib().vlp_pubkeygen_secure(keys.sk, ctypes.byref(m), first, count, ctypes.byref(h)))
+        else:
+            check(lib().vlp_pubkeygen(keys.sk, ctypes.byref(m), seed, first, count, ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().vlp_free_pk(self.h)
+        except Exception:
+            pass
+
+
+def server_load_records(pk: PublicKey, words, payloads, device: int = 0, stream=None):
+    """Server side (vlp_server_load_records): ServerEnc of a received pk straight into a torch int32
+    [count * per, 632] tensor on `device`; consumes the pk (a second call raises VLP_EPKUSED)."""
+    import torch
+    words = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+    pays = _payload_words(pk.m, payloads)
+    per = record_cts(pk.m)
+    out = torch.empty((pk.count * per, CT_STRIDE), dtype=torch.int32, device=f"cuda:{device}")
+    sb = ctypes.c_size_t()
+    check(lib().vlp_server_encrypt_db_device_scratch_bytes(ctypes.byref(pk.m), pk.count, ctypes.byref(sb)))
+    sc = torch.empty(max(256, sb.value), dtype=torch.uint8, device=f"cuda:{device}")
+    check(lib().vlp_server_load_records(pk.h, _u64p(words), _u64p(pays), ctypes.c_void_p(out.data_ptr()),
+                                        ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream, device)))
+    return out
+
+
 def _payload_words(m: VlpMeta, payloads):
     pw = (m.l_S + 63) // 64  # payload words per record (l_S up to 128)
     if pw == 1:

@@ -394,6 +394,23 @@ int vlp_server_encrypt_db_device(const vlp_meta* meta, size_t count, const uint3
   });
 }
 
+int vlp_server_load_records(vlp_pk* pk, const uint64_t* words, const uint64_t* payloads, uint32_t* db_dev,
+                            void* scratch, size_t scratch_bytes, uint64_t stream) {
+  if (!pk || !db_dev || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (pk->used) return fail(VLP_EPKUSED, "public-key samples already used (single-use, alg:PubKeyGen)");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(db_dev, pk->samples.data(), pk->samples.size() * 4, cudaMemcpyHostToDevice, st)))
+    return cuda_fail(e, "upload pk");
+  if (int rc = vlp_server_encrypt_db_device(&pk->meta, pk->count, db_dev, words, payloads, db_dev, scratch,
+                                            scratch_bytes, stream))
+    return rc;  // synchronous: the pk upload is complete
+  pk->used = true;
+  pk->samples.clear();
+  pk->samples.shrink_to_fit();
+  return VLP_OK;
+}
+
 size_t vlp_server_evk_bytes(void) { return kEvkBytes; }
 
 int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_bytes, uint64_t stream,

@@ -657,6 +657,20 @@ def test_role_separated_device_preprocessing(server, cfg, count):
     assert np.array_equal(A.to_host(fused), host)
 
 
+def test_server_load_records_single_use(server):
+    """SURVEY 8(b) load records: the server's vlp_server_load_records of a received host pk equals the host
+    PubKeyGen + ServerEnc byte for byte, and the pk is single-use (VLP_EPKUSED)."""
+    wl = make_workload(9, key_seed=SEED)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    k = server.keys
+    pk = A.PublicKey(k, m, 0, 16, seed=777)
+    db = A.server_load_records(pk, wl.records[:16], wl.payloads[:16])
+    assert np.array_equal(A.to_host(db), k.encrypt_db(m, wl.records[:16], wl.payloads[:16], pk_seed=777, count=16))
+    with pytest.raises(L.VlpError) as err:
+        A.server_load_records(pk, wl.records[:16], wl.payloads[:16])
+    assert err.value.code == L.VLP_EPKUSED
+
+
 @pytest.mark.parametrize("cfg,count", [(1, None), (9, 16), (4, 4096)])
 def test_device_encrypt_db_equals_host(server, cfg, count):
     """Device PubKeyGen + ServerEnc (vlp_encrypt_db_device) is byte-identical to the host vlp_pubkeygen +
