@@ -480,6 +480,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "records_per_s": records_per_s, "ks_per_s": (prog.info.ks * world + (comb.info.ks if comb else 0)) / (ms_per_step / 1e3),  # all queries
+            "gates_per_s": (prog.info.gates * world + (comb.info.gates if comb else 0)) / (ms_per_step / 1e3),  # MUX = 1
             "config": {"workload": f"cfg{args.config}_{wname}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S,
                        "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels, "queries_per_step": nq,
                        "parallelism": f"records sharded x{world}" if world > 1 else "single GPU",
