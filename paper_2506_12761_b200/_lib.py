@@ -6,7 +6,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvlp.so")
+LIB_PATH = os.environ.get("VLP_LIB", os.path.join(HERE, "libvlp.so"))  # VLP_LIB: dev builds (tools/)
 
 CT_STRIDE = 632
 NLWE_STRIDE = 1028

@@ -10,8 +10,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libvlp.so")
+# VLP_BUILD_VARIANT=name (dev tools only): extra -D flags from VLP_BUILD_DEFS, objects and library under other names
+VARIANT = os.environ.get("VLP_BUILD_VARIANT", "")
+DEFS = os.environ.get("VLP_BUILD_DEFS", "").split() if VARIANT else []
+BUILD = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(HERE, f"libvlp_{VARIANT}.so" if VARIANT else "libvlp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["kernels.cu", "kernels_fft.cu", "kernels_ks.cu", "api.cu"]
@@ -32,7 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for f in CU:
         o = os.path.join(BUILD, f + ".o")
         if force or _newer([f] + HDR, o):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+            cmd = [NVCC, *ARCH, *DEFS, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                    "-c", os.path.join(CSRC, f), "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:

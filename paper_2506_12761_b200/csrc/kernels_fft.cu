@@ -292,6 +292,28 @@ __device__ __forceinline__ void mac_half(const cd (&X)[16], int h, const double2
 
 }  // namespace
 
+// Phase timing (dev builds with -DVLP_PHASE_TIMING, tools/fft_phases.py): clock64 deltas per step phase, summed over
+// the warps of a launch (read by vlp_debug_phase_read).  Compiled out of the product library.
+#ifdef VLP_PHASE_TIMING
+__device__ unsigned long long g_phase[8];
+#define VLP_PHASE_DECL \
+  unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; \
+  long long ph_t = clock64();
+#define VLP_PHASE_MARK(k)                                   \
+  {                                                          \
+    const long long t_ = clock64();                          \
+    ph_acc[k] += static_cast<unsigned long long>(t_ - ph_t); \
+    ph_t = t_;                                               \
+  }
+#define VLP_PHASE_OUT \
+  if (lane == 0)      \
+    for (int k_ = 0; k_ < 8; k_++) atomicAdd(&g_phase[k_], ph_acc[k_]);
+#else
+#define VLP_PHASE_DECL
+#define VLP_PHASE_MARK(k)
+#define VLP_PHASE_OUT
+#endif
+
 // ================================================================================ K2F blind rotation
 // W warps per CTA, one bootstrap per warp; persistent over groups of W jobs.  Per CMux step and warp:
 //   for u in {0 (mask), 1 (body)}: D = X^abar acc_u - acc_u (offset 0x81020400, R5); for each gadget digit j:
@@ -417,6 +439,7 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
     __syncwarp();
 
     // ---- S5: CMux steps
+    VLP_PHASE_DECL
     for (uint32_t i = 0; i < steps; i++) {
       const uint32_t ab = abar[i];
 #pragma unroll 1
@@ -431,26 +454,33 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
           v = kk >= static_cast<uint32_t>(N) ? 0u - v : v;
           wv[q] = v - au[j] + 0x81020400u;
         }
+        VLP_PHASE_MARK(0)
 #pragma unroll 1
         for (int dj = 0; dj < 3; dj++) {
           cd X[16];
           fft_fwd(X, wv, 25u - 7u * dj, lc, tr);
+          VLP_PHASE_MARK(1)
           if (u == 0 && dj == 0) {
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               mbar_wait(&mbar[sl], ph);
+              VLP_PHASE_MARK(2)
               mac_half<true>(X, h, ring + sl * (kFftChunkBytes / 16) + lane, tm);
               release();
+              VLP_PHASE_MARK(3)
             }
           } else {
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               mbar_wait(&mbar[sl], ph);
+              VLP_PHASE_MARK(2)
               mac_half<false>(X, h, ring + sl * (kFftChunkBytes / 16) + lane, tm);
               release();
+              VLP_PHASE_MARK(3)
             }
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          VLP_PHASE_MARK(3)
         }
       }
       // inverse transforms, rounding: acc_o += R_lo, acc_o += 2^16 R_hi (mod 2^32), one limb at a time
@@ -458,7 +488,9 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
       for (int ol = 0; ol < 4; ol++) {
         cd V[16];
         tm_ld_col16(tm + ol * 4, V);
+        VLP_PHASE_MARK(4)
         fft_inv(V, lc, tr);
+        VLP_PHASE_MARK(5)
         uint32_t* ao = acc + (ol >> 1) * N + lane;
         const uint32_t sh = (ol & 1) * 16u;
 #pragma unroll
@@ -468,9 +500,11 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
           ao[32 * q] += rx << sh;
           ao[512 + 32 * q] += ry << sh;
         }
+        VLP_PHASE_MARK(6)
       }
       __syncwarp();
     }
+    VLP_PHASE_OUT
 
     // ---- S6 SampleExtract: a'_0 = a_0, a'_k = -a_{N-k}, b' = b_0
     if (a.raw_acc) {
@@ -523,6 +557,15 @@ __global__ void __launch_bounds__(512) vlp_bsk_fft_kernel(const uint32_t* __rest
 #pragma unroll
   for (int q = 0; q < 4; q++) dst[(rp * 4 + q) * 32 + L] = make_double2(re[q] / 512.0, im[q] / 512.0);
 }
+
+#ifdef VLP_PHASE_TIMING
+extern "C" int vlp_debug_phase_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 8);
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  return 0;
+}
+#endif
 
 void launch_bsk_fft(const uint32_t* raw, double2* out, const double2* psi, cudaStream_t st) {
   vlp_bsk_fft_kernel<<<n * kRows, 512, 0, st>>>(raw, out, psi);

@@ -1,0 +1,36 @@
+"""Developer tool: where a K2F step's time goes -- clock64 deltas per phase summed over the warps of one whole
+wave, from a dev build with -DVLP_PHASE_TIMING:
+    VLP_BUILD_VARIANT=phase VLP_BUILD_DEFS=-DVLP_PHASE_TIMING python -m paper_2506_12761_b200.build
+    VLP_LIB=paper_2506_12761_b200/libvlp_phase.so python tools/fft_phases.py"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_12761_b200 import _lib as L  # noqa: E402
+from paper_2506_12761_b200 import api as A  # noqa: E402
+
+NAMES = ["digit words (acc reads)", "forward FFT", "key-ring wait", "MAC (TMEM + key LDS)", "TMEM column load",
+         "inverse FFT", "round + acc update", "-"]
+keys = A.Keys(123)
+srv = A.Server(keys, 0)
+L.lib().vlp_debug_route(2, 8)
+rng = np.random.default_rng(0)
+cnt = 8 * torch.cuda.get_device_properties(0).multi_processor_count
+x = A.to_device(rng.integers(0, 2 ** 32, (cnt, 632), dtype=np.uint64).astype(np.uint32))
+f = L.lib().vlp_debug_phase_read
+f.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+buf = (ctypes.c_ulonglong * 8)()
+srv.debug_blind_rotate(x, 630)
+f(buf)
+srv.debug_blind_rotate(x, 630)
+torch.cuda.synchronize()
+f(buf)
+tot = sum(buf[:7])
+per = tot / cnt / 630
+print(f"{cnt} bootstraps x 630 steps: {per:.0f} warp-cycles per step (SM clock)")
+for k in range(7):
+    print(f"  {NAMES[k]:28s} {buf[k] / tot * 100:5.1f} %  {buf[k] / cnt / 630:8.0f} cycles/step")
