@@ -258,30 +258,32 @@ int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_se
                           const uint64_t* words, const uint64_t* payloads, uint32_t* out_dev, void* scratch,
                           size_t scratch_bytes, uint64_t stream) {
   if (!out_dev || !scratch) return fail(VLP_EINVAL, "null argument");
-  std::vector<uint32_t> nz;
-  std::vector<uint8_t> bits;
-  uint64_t h1 = 0;
-  if (int rc = prepare_encrypt_db(sk, meta, pk_seed, first, count, words, payloads, nz, bits, &h1)) return rc;
-  size_t need = 0;
-  vlp_encrypt_db_device_scratch_bytes(meta, count, &need);
-  if (scratch_bytes < need) return fail(VLP_ENOMEM, "scratch too small");
-  const size_t per = nz.size() / count, W = record_words(*meta);
-  uint8_t* sc = static_cast<uint8_t*>(scratch);
-  uint32_t* s_dev = reinterpret_cast<uint32_t*>(sc);
-  uint32_t* nz_dev = reinterpret_cast<uint32_t*>(sc + align256(n * 4));
-  uint8_t* bits_dev = sc + align256(n * 4) + align256(nz.size() * 4);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  if ((e = cudaMemcpyAsync(s_dev, sk->s, n * 4, cudaMemcpyHostToDevice, st)) ||
-      (e = cudaMemcpyAsync(nz_dev, nz.data(), nz.size() * 4, cudaMemcpyHostToDevice, st)) ||
-      (e = cudaMemcpyAsync(bits_dev, bits.data(), bits.size(), cudaMemcpyHostToDevice, st)))
-    return cuda_fail(e, "upload");
-  if ((e = launch_encrypt_db(s_dev, nz_dev, bits_dev, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
-                             meta->l_I, first, nz.size(), out_dev, st)))
-    return cuda_fail(e, "encrypt db");
-  if ((e = cudaMemsetAsync(s_dev, 0, n * 4, st))) return cuda_fail(e, "scrub");  // s does not outlive the call
-  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "encrypt db sync");
-  return VLP_OK;
+  return no_throw([&] {
+    std::vector<uint32_t> nz;
+    std::vector<uint8_t> bits;
+    uint64_t h1 = 0;
+    if (int rc = prepare_encrypt_db(sk, meta, pk_seed, first, count, words, payloads, nz, bits, &h1)) return rc;
+    size_t need = 0;
+    vlp_encrypt_db_device_scratch_bytes(meta, count, &need);
+    if (scratch_bytes < need) return fail(VLP_ENOMEM, "scratch too small");
+    const size_t per = nz.size() / count, W = record_words(*meta);
+    uint8_t* sc = static_cast<uint8_t*>(scratch);
+    uint32_t* s_dev = reinterpret_cast<uint32_t*>(sc);
+    uint32_t* nz_dev = reinterpret_cast<uint32_t*>(sc + align256(n * 4));
+    uint8_t* bits_dev = sc + align256(n * 4) + align256(nz.size() * 4);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(s_dev, sk->s, n * 4, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(nz_dev, nz.data(), nz.size() * 4, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(bits_dev, bits.data(), bits.size(), cudaMemcpyHostToDevice, st)))
+      return cuda_fail(e, "upload");
+    if ((e = launch_encrypt_db(s_dev, nz_dev, bits_dev, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
+                               meta->l_I, first, nz.size(), out_dev, st)))
+      return cuda_fail(e, "encrypt db");
+    if ((e = cudaMemsetAsync(s_dev, 0, n * 4, st))) return cuda_fail(e, "scrub");  // s does not outlive the call
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "encrypt db sync");
+    return static_cast<int>(VLP_OK);
+  });
 }
 
 size_t vlp_keygen_device_scratch_bytes(void) {
@@ -421,48 +423,50 @@ int vlp_server_create(int device, const vlp_evk* evk, void* evk_dev, size_t evk_
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(VLP_ENODEV, "no CUDA device");
   DeviceGuard dg;
   if (cudaError_t e = dg.set(device)) return cuda_fail(e, "cudaSetDevice");
-  auto srv = std::make_unique<vlp_server>();
-  srv->device = device;
-  cudaDeviceGetAttribute(&srv->sm_count, cudaDevAttrMultiProcessorCount, device);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  uint8_t* base = static_cast<uint8_t*>(evk_dev);
-  srv->evk_dev = base;
-  srv->bsk_ntt = reinterpret_cast<uint32_t*>(base);
-  srv->ksk = reinterpret_cast<uint32_t*>(base + kBskNttBytes);
-  srv->tw_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes);
-  srv->twl_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes);
-  srv->twl_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes + kTwlBytes);
-  uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes);
-  srv->kmat = reinterpret_cast<int8_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes);
-  srv->bsk_fft = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->kmat) + kKmatSwBytes);
-  srv->psi = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->bsk_fft) + kBskFftBytes);
+  return no_throw([&] {
+    auto srv = std::make_unique<vlp_server>();
+    srv->device = device;
+    cudaDeviceGetAttribute(&srv->sm_count, cudaDevAttrMultiProcessorCount, device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint8_t* base = static_cast<uint8_t*>(evk_dev);
+    srv->evk_dev = base;
+    srv->bsk_ntt = reinterpret_cast<uint32_t*>(base);
+    srv->ksk = reinterpret_cast<uint32_t*>(base + kBskNttBytes);
+    srv->tw_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes);
+    srv->twl_fwd = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes);
+    srv->twl_inv = reinterpret_cast<uint2*>(base + kBskNttBytes + kKskBytes + kTwBytes + kTwlBytes);
+    uint32_t* raw = reinterpret_cast<uint32_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes);
+    srv->kmat = reinterpret_cast<int8_t*>(base + kBskNttBytes + kKskBytes + kTwBytes + 2 * kTwlBytes + kRawBskBytes);
+    srv->bsk_fft = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->kmat) + kKmatSwBytes);
+    srv->psi = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(srv->bsk_fft) + kBskFftBytes);
 
-  std::vector<uint2> fwd, inv, lf, li;
-  make_twiddles(fwd, inv);
-  make_layout_twiddles(fwd, lf);
-  make_layout_twiddles(inv, li);
-  set_const_twiddles(fwd.data(), inv.data());
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(srv->bsk_ntt, 0, kBskNttBytes, st))) return cuda_fail(e, "memset");
-  if ((e = cudaMemcpyAsync(srv->tw_fwd, fwd.data(), kTwBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "tw");
-  if ((e = cudaMemcpyAsync(srv->twl_fwd, lf.data(), kTwlBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "twl");
-  if ((e = cudaMemcpyAsync(srv->twl_inv, li.data(), kTwlBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "twl");
-  if ((e = cudaMemcpyAsync(srv->ksk, evk->ksk.data(), kKskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "ksk");
-  if ((e = cudaMemcpyAsync(raw, evk->bsk.data(), kRawBskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "bsk");
-  // Montgomery factor with N^-1 folded in: c = N^-1 * 2^32 mod p
-  const uint32_t c_mont = static_cast<uint32_t>(mulmod(powmod(N, kP - 2), (1ull << 32) % kP));
-  launch_bsk_convert(raw, srv->bsk_ntt, srv->tw_fwd, c_mont, st);
-  // K2F: psi^e = exp(i pi e / 1024) in double (host libm), the FFT-domain key by a direct DFT on the device
-  std::vector<double2> psi(2048);
-  for (int k = 0; k < 2048; k++) psi[k] = make_double2(cos(M_PI * k / 1024.0), sin(M_PI * k / 1024.0));
-  set_fft_constants(psi.data());
-  if ((e = cudaMemcpyAsync(srv->psi, psi.data(), kPsiBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "psi");
-  launch_bsk_fft(raw, srv->bsk_fft, srv->psi, st);
-  launch_kmat_sw(srv->ksk, srv->kmat, st);
-  if ((e = cudaGetLastError())) return cuda_fail(e, "bsk convert launch");
-  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server create");
-  *out = srv.release();
-  return VLP_OK;
+    std::vector<uint2> fwd, inv, lf, li;
+    make_twiddles(fwd, inv);
+    make_layout_twiddles(fwd, lf);
+    make_layout_twiddles(inv, li);
+    set_const_twiddles(fwd.data(), inv.data());
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(srv->bsk_ntt, 0, kBskNttBytes, st))) return cuda_fail(e, "memset");
+    if ((e = cudaMemcpyAsync(srv->tw_fwd, fwd.data(), kTwBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "tw");
+    if ((e = cudaMemcpyAsync(srv->twl_fwd, lf.data(), kTwlBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "twl");
+    if ((e = cudaMemcpyAsync(srv->twl_inv, li.data(), kTwlBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "twl");
+    if ((e = cudaMemcpyAsync(srv->ksk, evk->ksk.data(), kKskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "ksk");
+    if ((e = cudaMemcpyAsync(raw, evk->bsk.data(), kRawBskBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "bsk");
+    // Montgomery factor with N^-1 folded in: c = N^-1 * 2^32 mod p
+    const uint32_t c_mont = static_cast<uint32_t>(mulmod(powmod(N, kP - 2), (1ull << 32) % kP));
+    launch_bsk_convert(raw, srv->bsk_ntt, srv->tw_fwd, c_mont, st);
+    // K2F: psi^e = exp(i pi e / 1024) in double (host libm), the FFT-domain key by a direct DFT on the device
+    std::vector<double2> psi(2048);
+    for (int k = 0; k < 2048; k++) psi[k] = make_double2(cos(M_PI * k / 1024.0), sin(M_PI * k / 1024.0));
+    set_fft_constants(psi.data());
+    if ((e = cudaMemcpyAsync(srv->psi, psi.data(), kPsiBytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "psi");
+    launch_bsk_fft(raw, srv->bsk_fft, srv->psi, st);
+    launch_kmat_sw(srv->ksk, srv->kmat, st);
+    if ((e = cudaGetLastError())) return cuda_fail(e, "bsk convert launch");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server create");
+    *out = srv.release();
+    return static_cast<int>(VLP_OK);
+  });
 }
 
 static int finish_program(vlp_server* server, std::unique_ptr<vlp_program>& p, vlp_program** out) {
