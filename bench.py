@@ -216,6 +216,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(ms, world, dev):
+    """The device-timed milliseconds of this rank -> the maximum over all ranks (NCCL: a CUDA tensor; gloo: CPU)."""
+    if world == 1:
+        return float(ms)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_nand(args, rank, world, local, dev, stream, A, L, dist):
     """Config 5: a batch of independent NAND bootstraps (BR + extract + KS) on fresh encryptions of uniform
     bits, split evenly over the ranks (no collective on the data path; the total batch is fixed, so the
@@ -255,10 +266,7 @@ def run_nand(args, rank, world, local, dev, stream, A, L, dist):
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     br_ms, ks_ms, br_n, _ = prog.profile_read(reset=True)
-    tot = torch.tensor([sum(a0.elapsed_time(b0) for a0, b0 in ev)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms = float(tot.item()) / args.steps
+    ms = max_over_ranks(sum(a0.elapsed_time(b0) for a0, b0 in ev), world, dev) / args.steps
     if rank == 0:
         peak, how = int_peak()
         achieved = alg_ops_per_br() * per * args.steps / (br_ms / 1e3) / 1e9
@@ -312,15 +320,25 @@ def main():
     from paper_2506_12761_b200 import _lib as L
     from paper_2506_12761_b200 import api as A
 
+    # VLP_BENCH_ONE_GPU_GLOO=1 (tests only, tests/test_bench_contract.py): every rank on cuda:0 over gloo, to run the
+    # N > 1 code path on a one-GPU box; the ranks' kernels never wait on one another (independent shards), the
+    # timings of ranks sharing a GPU are not a scaling measurement
+    one_gpu = world > 1 and os.environ.get("VLP_BENCH_ONE_GPU_GLOO") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        # NCCL communicator init lines on stderr (the rank count is visible in the driver's log)
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            # NCCL communicator init lines on stderr (the rank count is visible in the driver's log)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device(dev))
         if rank == 0:
-            print(f"[bench] torch.distributed nccl process group: world_size={world}", file=sys.stderr, flush=True)
+            print(f"[bench] torch.distributed {dist.get_backend()} process group: world_size={world}", file=sys.stderr,
+                  flush=True)
     stream = torch.cuda.current_stream()
 
     from paper_2506_12761_b200.dist import shard_range, sharded_step
@@ -404,10 +422,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     br_ms, ks_ms, br_n, ks_n = prog.profile_read(reset=True)
     prog.profile(False)
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms = float(tot.item())
+    total_ms = max_over_ranks(sum(step_ms), world, dev)
     ms_per_step = total_ms / args.steps
     br_per_query = (CONFIG_BR.get(args.config) if not extra else None) or \
         prog.info.br // nq * world + (comb.info.br if comb else 0)
@@ -451,10 +466,7 @@ def main():
                 out_pin.copy_(out, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e_ms = float(et.item()) / e2e_steps
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / e2e_steps
         if rank == 0:
             check_all(out_pin.numpy().view(np.uint32))
         e2e = {"value": nq * br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": nq * wl.M / (e2e_ms / 1e3),

@@ -31,12 +31,24 @@ def sharded_step(q, eval_shard, combine, world: int, rank: int, gathered=None):
         return eval_shard(q)
     import torch
     import torch.distributed as dist
-    dist.broadcast(q, src=0)
+    staged = q.is_cuda and dist.get_backend() != "nccl"  # gloo: collectives on host copies of device tensors
+    if staged:
+        qh = q.cpu()
+        dist.broadcast(qh, src=0)
+        q.copy_(qh)
+    else:
+        dist.broadcast(q, src=0)
     part = eval_shard(q)
     if gathered is None:  # concatenated along dim 0: [G * l_S, 632] (rank order = shard order)
         gathered = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype, device=part.device)
+    send = part.contiguous().cpu() if staged else part.contiguous()
     if rank == 0:
-        dist.gather(part.contiguous(), gather_list=list(gathered.chunk(world, dim=0)), dst=0)
+        if staged:
+            host = torch.empty(gathered.shape, dtype=gathered.dtype)
+            dist.gather(send, gather_list=list(host.chunk(world, dim=0)), dst=0)
+            gathered.copy_(host)
+        else:
+            dist.gather(send, gather_list=list(gathered.chunk(world, dim=0)), dst=0)
         return combine(gathered)
-    dist.gather(part.contiguous(), dst=0)
+    dist.gather(send, dst=0)
     return None

@@ -1,9 +1,12 @@
 """The bench.py JSON contract on CPU: the reference arm (the CPU oracle, `--impl reference`) prints one JSON
-line with the keys the driver reads, and exits 0 without work on non-zero ranks (torchrun N > 1)."""
+line with the keys the driver reads, and exits 0 without work on non-zero ranks (torchrun N > 1); on a GPU, the
+N > 1 path of our arm under torchrun with the ranks sharing one GPU."""
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -46,3 +49,42 @@ def test_algorithmic_ops_per_br_is_survey_8d():
     peak, how = bench.int_peak()
     assert how.startswith("measured") and 25_000 < peak < 40_000  # profiles/int_peak_r1.json, Gop/s
     assert 17_000 < bench.fp64_peak() < 19_000  # profiles/fp64_bench_r2.json
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,world", [(2, 2), (5, 2)])
+def test_bench_multi_rank_path_on_one_gpu(cfg, world):
+    """bench.py's N > 1 path as the driver launches it (torchrun, one process per rank, WORLD_SIZE / RANK /
+    LOCAL_RANK from the env) with every rank on cuda:0 over gloo (VLP_BENCH_ONE_GPU_GLOO=1, CPU-staged
+    broadcast / gather in dist.sharded_step): records sharded x2, the gathered shard roots combined on rank 0 and
+    checked against the plain predicate inside bench.py (config 2), or the NAND batch split over the ranks
+    (config 5); rank 0 alone prints one JSON line with n_gpus = world.  The ranks' kernels never wait on one another,
+    so sharing one GPU is safe; the timings are not a scaling measurement."""
+    env = dict(os.environ, VLP_BENCH_ONE_GPU_GLOO="1")
+    args = ["--config", str(cfg), "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    if cfg == 5:
+        args += ["--nand", str(1 << 12)]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+                        os.path.join(ROOT, "bench.py"), "--gpus", str(world), *args],
+                       capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["value"] > 0 and d["steps"] == 1
+    if cfg == 2:
+        assert d["config"]["parallelism"] == f"records sharded x{world}"
+        assert d["config"]["br_per_query"] == 132_080
+        assert d["e2e"]["value"] > 0
+    else:
+        assert d["config"]["gates"] == 1 << 12
