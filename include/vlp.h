@@ -148,6 +148,10 @@ int vlp_pubkeygen_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, s
 /* Test hook: one ChaCha20 block (RFC 8439 section 2.3) -- key[8], counter, nonce[3] -> out[16] (words, little
  * endian), to pin the secure generator against an independent implementation. */
 int vlp_debug_chacha20_block(const uint32_t* key, uint32_t counter, const uint32_t* nonce, uint32_t* out);
+/* Test hook: the calling thread's NEXT *_secure call (host or device) uses key[8] instead of a getrandom key, then
+ * the hook is cleared.  Lets a test compare a device secure call with the host secure call under one key; never
+ * use it to protect data (the key is whatever the caller passed). */
+int vlp_debug_next_secure_key(const uint32_t* key);
 /* Ciphertexts per record in the encrypted DB: W * l_I + l_S. */
 int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);
 /* alg:ServerEnc for the pk's records: ct = (0, Ecd(bit)) + pk sample.
@@ -169,6 +173,10 @@ int vlp_server_encrypt_db(vlp_pk* pk, const uint64_t* words, const uint64_t* pay
 size_t vlp_keygen_device_scratch_bytes(void);
 int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch_dev, size_t scratch_bytes,
                       uint64_t stream, vlp_sk** sk, vlp_evk** evk);
+/* The same from OS randomness (see "Randomness"): equal, byte for byte, to vlp_keygen_secure under the same
+ * ChaCha20 key (the device draws the masks from ChaCha20 blocks, the host the secret keys and the noise). */
+int vlp_keygen_device_secure(const vlp_params* params, void* scratch_dev, size_t scratch_bytes, uint64_t stream,
+                             vlp_sk** sk, vlp_evk** evk);
 /* Device PubKeyGen (client; alg:PubKeyGen P:194-219): the single-use TLWE(0) samples of records
  * [first, first+count) written to pk_dev ([count][per_record][632], the row order of vlp_server_encrypt_db),
  * byte-identical to vlp_pubkeygen(sk, meta, seed, first, count)'s samples.  The copy of s placed in scratch_dev
@@ -176,6 +184,9 @@ int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch_dev
 int vlp_pubkeygen_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes);
 int vlp_pubkeygen_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
                          uint32_t* pk_dev, void* scratch_dev, size_t scratch_bytes, uint64_t stream);
+/* The same from OS randomness: equal to vlp_pubkeygen_secure's samples under the same ChaCha20 key. */
+int vlp_pubkeygen_device_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, size_t count, uint32_t* pk_dev,
+                                void* scratch_dev, size_t scratch_bytes, uint64_t stream);
 /* Device ServerEnc (server; alg:ServerEnc P:223-247): out_dev = pk_dev + (0, Ecd(bit)) for every row of records
  * [0, count) of the public-key samples (out_dev may equal pk_dev).  Needs no secret key.  words / payloads as in
  * vlp_server_encrypt_db (host, range-checked: VLP_ERANGE).  scratch_dev >=

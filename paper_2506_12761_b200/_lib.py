@@ -64,6 +64,7 @@ SIGNATURES = {
     "vlp_encrypt_bits_secure": (_i, [_vp, ctypes.POINTER(ctypes.c_uint8), _sz, _u32p]),
     "vlp_pubkeygen_secure": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _pp]),
     "vlp_debug_chacha20_block": (_i, [_u32p, ctypes.c_uint32, _u32p, _u32p]),
+    "vlp_debug_next_secure_key": (_i, [_u32p]),
     "vlp_sk_export": (_i, [_vp, _u32p, _u32p]),
     "vlp_evk_export": (_i, [_vp, _u32p, _u32p]),
     "vlp_encrypt_bits": (_i, [_vp, _u8p, _sz, _u64, _u64, _u32p]),
@@ -76,8 +77,10 @@ SIGNATURES = {
     "vlp_encrypt_db_device": (_i, [_vp, ctypes.POINTER(VlpMeta), _u64, _sz, _sz, _u64p, _u64p, _vp, _vp, _sz, _u64]),
     "vlp_keygen_device_scratch_bytes": (_sz, []),
     "vlp_keygen_device": (_i, [_u64, ctypes.POINTER(VlpParams), _vp, _sz, _u64, _pp, _pp]),
+    "vlp_keygen_device_secure": (_i, [ctypes.POINTER(VlpParams), _vp, _sz, _u64, _pp, _pp]),
     "vlp_pubkeygen_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_pubkeygen_device": (_i, [_vp, ctypes.POINTER(VlpMeta), _u64, _sz, _sz, _vp, _vp, _sz, _u64]),
+    "vlp_pubkeygen_device_secure": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _vp, _vp, _sz, _u64]),
     "vlp_server_encrypt_db_device_scratch_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_server_load_records": (_i, [_vp, _u64p, _u64p, _vp, _vp, _sz, _u64]),
     "vlp_server_encrypt_db_device": (_i, [ctypes.POINTER(VlpMeta), _sz, _vp, _u64p, _u64p, _vp, _vp, _sz, _u64]),

@@ -39,22 +39,27 @@ class Keys:
     """vlp_keygen: secret key + evaluation key, host side."""
 
     def __init__(self, seed: int | None = None, device: int | None = None):
-        """KeyGen.  seed=None (the default): fresh keys from OS randomness (vlp_keygen_secure).  An integer seed: the
-        reproducible test / benchmark keys of vlp_keygen (only as secret as the seed), on the host, or with device=
-        the byte-identical device KeyGen (vlp_keygen_device)."""
+        """KeyGen.  seed=None (the default): fresh keys from OS randomness (vlp_keygen_secure; with device= the
+        device KeyGen, vlp_keygen_device_secure).  An integer seed: the reproducible test / benchmark keys of
+        vlp_keygen (only as secret as the seed), on the host, or with device= the byte-identical device KeyGen
+        (vlp_keygen_device)."""
         self.seed = seed
         sk, evk = ctypes.c_void_p(), ctypes.c_void_p()
-        if seed is None:
-            if device is not None:
-                raise ValueError("the device KeyGen is the seeded (test / benchmark) mode: pass a seed")
-            check(lib().vlp_keygen_secure(None, ctypes.byref(sk), ctypes.byref(evk)))
-        elif device is None:
-            check(lib().vlp_keygen(seed, None, ctypes.byref(sk), ctypes.byref(evk)))
+        if device is None:
+            if seed is None:
+                check(lib().vlp_keygen_secure(None, ctypes.byref(sk), ctypes.byref(evk)))
+            else:
+                check(lib().vlp_keygen(seed, None, ctypes.byref(sk), ctypes.byref(evk)))
         else:
             import torch
             sc = torch.empty(lib().vlp_keygen_device_scratch_bytes(), dtype=torch.uint8, device=f"cuda:{device}")
-            check(lib().vlp_keygen_device(seed, None, ctypes.c_void_p(sc.data_ptr()), sc.numel(),
-                                          _stream_handle(None, device), ctypes.byref(sk), ctypes.byref(evk)))
+            st = _stream_handle(None, device)
+            if seed is None:
+                check(lib().vlp_keygen_device_secure(None, ctypes.c_void_p(sc.data_ptr()), sc.numel(), st,
+                                                     ctypes.byref(sk), ctypes.byref(evk)))
+            else:
+                check(lib().vlp_keygen_device(seed, None, ctypes.c_void_p(sc.data_ptr()), sc.numel(), st,
+                                              ctypes.byref(sk), ctypes.byref(evk)))
         self.sk, self.evk = sk, evk
 
     def __del__(self):
@@ -182,17 +187,23 @@ def _payload_words(m: VlpMeta, payloads):
     return np.array([[(int(v) >> (64 * w)) & (2 ** 64 - 1) for w in range(pw)] for v in payloads], dtype=np.uint64)
 
 
-def pubkeygen_device(keys: "Keys", m: VlpMeta, pk_seed: int, first: int, count: int, device: int = 0, stream=None):
+def pubkeygen_device(keys: "Keys", m: VlpMeta, pk_seed: int | None, first: int, count: int, device: int = 0,
+                     stream=None):
     """Client side, device PubKeyGen (alg:PubKeyGen P:194-219): the records' single-use TLWE(0) samples as a torch
-    int32 [count * per, 632] tensor, byte-identical to vlp_pubkeygen's samples."""
+    int32 [count * per, 632] tensor, byte-identical to vlp_pubkeygen's samples.  pk_seed=None: OS randomness
+    (vlp_pubkeygen_device_secure)."""
     import torch
     per = record_cts(m)
     pk = torch.empty((count * per, CT_STRIDE), dtype=torch.int32, device=f"cuda:{device}")
     sb = ctypes.c_size_t()
     check(lib().vlp_pubkeygen_device_scratch_bytes(ctypes.byref(m), count, ctypes.byref(sb)))
     sc = torch.empty(max(256, sb.value), dtype=torch.uint8, device=f"cuda:{device}")
-    check(lib().vlp_pubkeygen_device(keys.sk, ctypes.byref(m), pk_seed, first, count, ctypes.c_void_p(pk.data_ptr()),
-                                     ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream, device)))
+    if pk_seed is None:
+        check(lib().vlp_pubkeygen_device_secure(keys.sk, ctypes.byref(m), first, count, ctypes.c_void_p(pk.data_ptr()),
+                                                ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream, device)))
+    else:
+        check(lib().vlp_pubkeygen_device(keys.sk, ctypes.byref(m), pk_seed, first, count, ctypes.c_void_p(pk.data_ptr()),
+                                         ctypes.c_void_p(sc.data_ptr()), sc.numel(), _stream_handle(stream, device)))
     return pk
 
 

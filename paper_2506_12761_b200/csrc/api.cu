@@ -244,6 +244,20 @@ static int no_throw(F&& f) {
 }
 }  // extern "C++"
 
+extern "C++" {
+// The device half of a call's generator (host.cpp Rng): the mask words of domain `dom`.
+static MaskGen mask_gen(const Rng& g, uint64_t dom) {
+  MaskGen m{};
+  m.secure = g.secure ? 1u : 0u;
+  m.dom = static_cast<uint32_t>(dom);
+  if (g.secure)
+    std::memcpy(m.key, g.key, sizeof(m.key));
+  else
+    m.h1 = prng_prefix(g.seed, dom);
+  return m;
+}
+}  // extern "C++"
+
 extern "C" {
 
 int vlp_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
@@ -261,8 +275,8 @@ int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_se
   return no_throw([&] {
     std::vector<uint32_t> nz;
     std::vector<uint8_t> bits;
-    uint64_t h1 = 0;
-    if (int rc = prepare_encrypt_db(sk, meta, pk_seed, first, count, words, payloads, nz, bits, &h1)) return rc;
+    const Rng g = seeded(pk_seed);
+    if (int rc = prepare_encrypt_db(sk, meta, g, first, count, words, payloads, nz, bits)) return rc;
     size_t need = 0;
     vlp_encrypt_db_device_scratch_bytes(meta, count, &need);
     if (scratch_bytes < need) return fail(VLP_ENOMEM, "scratch too small");
@@ -277,7 +291,7 @@ int vlp_encrypt_db_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t pk_se
         (e = cudaMemcpyAsync(nz_dev, nz.data(), nz.size() * 4, cudaMemcpyHostToDevice, st)) ||
         (e = cudaMemcpyAsync(bits_dev, bits.data(), bits.size(), cudaMemcpyHostToDevice, st)))
       return cuda_fail(e, "upload");
-    if ((e = launch_encrypt_db(s_dev, nz_dev, bits_dev, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
+    if ((e = launch_encrypt_db(s_dev, nz_dev, bits_dev, mask_gen(g, kPkA), static_cast<uint32_t>(per), static_cast<uint32_t>(W),
                                meta->l_I, first, nz.size(), out_dev, st)))
       return cuda_fail(e, "encrypt db");
     if ((e = cudaMemsetAsync(s_dev, 0, n * 4, st))) return cuda_fail(e, "scrub");  // s does not outlive the call
@@ -291,8 +305,8 @@ size_t vlp_keygen_device_scratch_bytes(void) {
          align256(n * 4) + align256(N * 4);
 }
 
-int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch, size_t scratch_bytes, uint64_t stream,
-                      vlp_sk** sk_out, vlp_evk** evk_out) {
+static int keygen_device_impl(const Rng& g, const vlp_params* params, void* scratch, size_t scratch_bytes,
+                              uint64_t stream, vlp_sk** sk_out, vlp_evk** evk_out) {
   if (!sk_out || !evk_out || !scratch) return fail(VLP_EINVAL, "null argument");
   if (scratch_bytes < vlp_keygen_device_scratch_bytes()) return fail(VLP_ENOMEM, "scratch too small");
   vlp_params p;
@@ -302,11 +316,11 @@ int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch, si
     auto evk = std::make_unique<vlp_evk>();
     sk->params = p;
     evk->params = p;
-    secret_keys(seed, sk.get());
+    secret_keys(g, sk.get());
     evk->bsk.assign(static_cast<size_t>(n) * kRows * 2 * N, 0);
     evk->ksk.assign(static_cast<size_t>(N) * kKsT * 3 * kCt, 0);
     std::vector<uint32_t> e_bsk(static_cast<size_t>(n) * kRows * N), e_ksk(static_cast<size_t>(N) * kKsT * 3);
-    keygen_noise(seed, p, e_bsk.data(), e_ksk.data());  // host libm Box-Muller (byte-identical noise)
+    keygen_noise(g, p, e_bsk.data(), e_ksk.data());  // host libm Box-Muller (byte-identical noise)
     uint8_t* sc = static_cast<uint8_t*>(scratch);
     uint32_t* bsk = reinterpret_cast<uint32_t*>(sc);
     uint32_t* ksk = reinterpret_cast<uint32_t*>(sc + align256(kRawBskBytes));
@@ -321,7 +335,7 @@ int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch, si
         (e = cudaMemcpyAsync(eb, e_bsk.data(), e_bsk.size() * 4, cudaMemcpyHostToDevice, st)) ||
         (e = cudaMemcpyAsync(ek, e_ksk.data(), e_ksk.size() * 4, cudaMemcpyHostToDevice, st)))
       return cuda_fail(e, "keygen upload");
-    if ((e = launch_keygen(prng_prefix(seed, kBskA), prng_prefix(seed, kKskA), s_dev, z_dev, eb, ek, bsk, ksk, st)))
+    if ((e = launch_keygen(mask_gen(g, kBskA), mask_gen(g, kKskA), s_dev, z_dev, eb, ek, bsk, ksk, st)))
       return cuda_fail(e, "keygen kernels");
     if ((e = cudaMemcpyAsync(evk->bsk.data(), bsk, kRawBskBytes, cudaMemcpyDeviceToHost, st)) ||
         (e = cudaMemcpyAsync(evk->ksk.data(), ksk, kKskBytes, cudaMemcpyDeviceToHost, st)) ||
@@ -334,6 +348,18 @@ int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch, si
   });
 }
 
+int vlp_keygen_device(uint64_t seed, const vlp_params* params, void* scratch, size_t scratch_bytes, uint64_t stream,
+                      vlp_sk** sk_out, vlp_evk** evk_out) {
+  return keygen_device_impl(seeded(seed), params, scratch, scratch_bytes, stream, sk_out, evk_out);
+}
+
+int vlp_keygen_device_secure(const vlp_params* params, void* scratch, size_t scratch_bytes, uint64_t stream,
+                             vlp_sk** sk_out, vlp_evk** evk_out) {
+  Rng g;
+  if (int rc = os_random(&g)) return rc;
+  return keygen_device_impl(g, params, scratch, scratch_bytes, stream, sk_out, evk_out);
+}
+
 int vlp_pubkeygen_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
   size_t per = 0;
   if (int rc = vlp_db_record_cts(meta, &per)) return rc;
@@ -342,13 +368,12 @@ int vlp_pubkeygen_device_scratch_bytes(const vlp_meta* meta, size_t count, size_
   return VLP_OK;
 }
 
-int vlp_pubkeygen_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
-                         uint32_t* pk_dev, void* scratch, size_t scratch_bytes, uint64_t stream) {
+static int pubkeygen_device_impl(const vlp_sk* sk, const vlp_meta* meta, const Rng& g, size_t first, size_t count,
+                                 uint32_t* pk_dev, void* scratch, size_t scratch_bytes, uint64_t stream) {
   if (!pk_dev || !scratch) return fail(VLP_EINVAL, "null argument");
   return no_throw([&] {
     std::vector<uint32_t> nz;
-    uint64_t h1 = 0;
-    if (int rc = prepare_pk_noise(sk, meta, seed, first, count, nz, &h1)) return rc;
+    if (int rc = prepare_pk_noise(sk, meta, g, first, count, nz)) return rc;
     size_t need = 0;
     vlp_pubkeygen_device_scratch_bytes(meta, count, &need);
     if (scratch_bytes < need) return fail(VLP_ENOMEM, "scratch too small");
@@ -361,13 +386,25 @@ int vlp_pubkeygen_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, 
     if ((e = cudaMemcpyAsync(s_dev, sk->s, n * 4, cudaMemcpyHostToDevice, st)) ||
         (e = cudaMemcpyAsync(nz_dev, nz.data(), nz.size() * 4, cudaMemcpyHostToDevice, st)))
       return cuda_fail(e, "upload");
-    if ((e = launch_encrypt_db(s_dev, nz_dev, nullptr, h1, static_cast<uint32_t>(per), static_cast<uint32_t>(W),
+    if ((e = launch_encrypt_db(s_dev, nz_dev, nullptr, mask_gen(g, kPkA), static_cast<uint32_t>(per), static_cast<uint32_t>(W),
                                meta->l_I, first, nz.size(), pk_dev, st)))
       return cuda_fail(e, "pubkeygen");
     if ((e = cudaMemsetAsync(s_dev, 0, n * 4, st))) return cuda_fail(e, "scrub");  // s does not outlive the call
     if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "pubkeygen sync");
     return static_cast<int>(VLP_OK);
   });
+}
+
+int vlp_pubkeygen_device(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+                         uint32_t* pk_dev, void* scratch, size_t scratch_bytes, uint64_t stream) {
+  return pubkeygen_device_impl(sk, meta, seeded(seed), first, count, pk_dev, scratch, scratch_bytes, stream);
+}
+
+int vlp_pubkeygen_device_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, size_t count, uint32_t* pk_dev,
+                                void* scratch, size_t scratch_bytes, uint64_t stream) {
+  Rng g;
+  if (int rc = os_random(&g)) return rc;
+  return pubkeygen_device_impl(sk, meta, g, first, count, pk_dev, scratch, scratch_bytes, stream);
 }
 
 int vlp_server_encrypt_db_device_scratch_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {

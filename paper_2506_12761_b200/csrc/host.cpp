@@ -58,33 +58,39 @@ void chacha20_block(const uint32_t key[8], uint32_t counter, const uint32_t nonc
   for (int i = 0; i < 16; i++) out[i] = x[i] + in[i];
 }
 
-// The randomness of one call: the seeded counter PRNG (R3; reproducible, 64-bit seed: tests and benchmarks), or
-// ChaCha20 under a 256-bit key drawn from the OS (getrandom) for the *_secure calls.  Either way a random-access
-// generator u64(dom, obj, word); the secure one uses nonce (dom, obj), block counter word / 8.
-struct Rng {
-  uint64_t seed = 0;
-  bool secure = false;
-  uint32_t key[8] = {};
-  uint64_t u64(uint64_t dom, uint64_t obj, uint64_t word) const {
-    if (!secure) return prng(seed, dom, obj, word);
-    const uint32_t nonce[3] = {static_cast<uint32_t>(dom), static_cast<uint32_t>(obj), static_cast<uint32_t>(obj >> 32)};
-    uint32_t blk[16];
-    chacha20_block(key, static_cast<uint32_t>(word >> 3), nonce, blk);
-    const int w = static_cast<int>(word & 7);
-    return static_cast<uint64_t>(blk[2 * w]) | (static_cast<uint64_t>(blk[2 * w + 1]) << 32);
-  }
-  ~Rng() {  // the key does not outlive the call
-    volatile uint32_t* k = key;
-    for (int i = 0; i < 8; i++) k[i] = 0;
-  }
-};
-static Rng seeded(uint64_t seed) {
+Rng seeded(uint64_t seed) {
   Rng r;
   r.seed = seed;
   return r;
 }
-static int os_random(Rng* r) {
+
+uint64_t Rng::u64(uint64_t dom, uint64_t obj, uint64_t word) const {
+  if (!secure) return prng(seed, dom, obj, word);
+  const uint32_t nonce[3] = {static_cast<uint32_t>(dom), static_cast<uint32_t>(obj), static_cast<uint32_t>(obj >> 32)};
+  uint32_t blk[16];
+  chacha20_block(key, static_cast<uint32_t>(word >> 3), nonce, blk);
+  const int w = static_cast<int>(word & 7);
+  return static_cast<uint64_t>(blk[2 * w]) | (static_cast<uint64_t>(blk[2 * w + 1]) << 32);
+}
+
+Rng::~Rng() {  // the key does not outlive the call
+  volatile uint32_t* k = key;
+  for (int i = 0; i < 8; i++) k[i] = 0;
+}
+
+// vlp_debug_next_secure_key: a key the calling thread's next secure call takes instead of getrandom (tests only)
+static thread_local bool g_next_key_set = false;
+static thread_local uint32_t g_next_key[8];
+
+int os_random(Rng* r) {
   r->secure = true;
+  if (g_next_key_set) {
+    std::memcpy(r->key, g_next_key, sizeof(r->key));
+    volatile uint32_t* k = g_next_key;
+    for (int i = 0; i < 8; i++) k[i] = 0;
+    g_next_key_set = false;
+    return VLP_OK;
+  }
   size_t got = 0;
   uint8_t* dst = reinterpret_cast<uint8_t*>(r->key);
   while (got < sizeof(r->key)) {
@@ -99,16 +105,13 @@ static int os_random(Rng* r) {
 }
 
 // Box-Muller Gaussian, "N(0, sigma)" (R2, R3); scalar glibc libm, no FMA contraction.
-static uint32_t noise(const Rng& g, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
+uint32_t noise(const Rng& g, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
   const uint64_t w1 = g.u64(dom, obj, 2 * t), w2 = g.u64(dom, obj, 2 * t + 1);
   const double u1 = (static_cast<double>(w1 >> 11) + 1.0) * 0x1p-53;
   const double u2 = static_cast<double>(w2 >> 11) * 0x1p-53;
   const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
   const long long e = std::llround(z * (sigma * 4294967296.0));
   return static_cast<uint32_t>(static_cast<uint64_t>(e));
-}
-uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma) {
-  return noise(seeded(seed), dom, obj, t, sigma);
 }
 
 static inline uint32_t uniform(const Rng& g, uint64_t dom, uint64_t obj, uint64_t word) {
@@ -165,19 +168,18 @@ int resolve_params(const vlp_params* params, vlp_params* p) {
 }
 
 // Binary LWE key s and ring key z (O4): bit 63 of the generator.
-static void secret_keys(const Rng& g, vlp_sk* sk) {
+void secret_keys(const Rng& g, vlp_sk* sk) {
   for (int i = 0; i < n; i++) sk->s[i] = static_cast<uint32_t>(g.u64(kSkLwe, 0, i) >> 63);
   for (int j = 0; j < N; j++) sk->z[j] = static_cast<uint32_t>(g.u64(kSkRing, 0, j) >> 63);
 }
-void secret_keys(uint64_t seed, vlp_sk* sk) { secret_keys(seeded(seed), sk); }
 
 // Host half of vlp_keygen_device: every Gaussian noise word of the evaluation key, exactly the values vlp_keygen
 // draws -- bsk row (i, r) coefficient j at [(i*6 + r)*N + j] (sigma_bk), ksk row idx at [idx] (sigma_ks).
-void keygen_noise(uint64_t seed, const vlp_params& p, uint32_t* bsk_noise, uint32_t* ksk_noise) {
+void keygen_noise(const Rng& g, const vlp_params& p, uint32_t* bsk_noise, uint32_t* ksk_noise) {
   parallel_for(static_cast<size_t>(n) * kRows, [&](size_t ir) {
-    for (int j = 0; j < N; j++) bsk_noise[ir * N + j] = noise(seed, kBskE, ir, j, p.sigma_bk);
+    for (int j = 0; j < N; j++) bsk_noise[ir * N + j] = noise(g, kBskE, ir, j, p.sigma_bk);
   });
-  parallel_for(static_cast<size_t>(N) * kKsT * 3, [&](size_t idx) { ksk_noise[idx] = noise(seed, kKskE, idx, 0, p.sigma_ks); });
+  parallel_for(static_cast<size_t>(N) * kKsT * 3, [&](size_t idx) { ksk_noise[idx] = noise(g, kKskE, idx, 0, p.sigma_ks); });
 }
 
 uint64_t prng_prefix(uint64_t seed, uint64_t dom) { return mix(seed ^ (dom * 0x9E3779B97F4A7C15ull)); }
@@ -392,6 +394,13 @@ int vlp_pubkeygen_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, s
   return pubkeygen_impl(sk, meta, g, first, count, out);
 }
 
+int vlp_debug_next_secure_key(const uint32_t* key) {
+  if (!key) return fail(VLP_EINVAL, "null argument");
+  std::memcpy(g_next_key, key, sizeof(g_next_key));
+  g_next_key_set = true;
+  return VLP_OK;
+}
+
 int vlp_debug_chacha20_block(const uint32_t* key, uint32_t counter, const uint32_t* nonce, uint32_t* out) {
   if (!key || !nonce || !out) return fail(VLP_EINVAL, "null argument");
   chacha20_block(key, counter, nonce, out);
@@ -434,10 +443,10 @@ int prepare_db_bits(const vlp_meta* meta, size_t count, const uint64_t* words, c
   return VLP_OK;
 }
 
-// PubKeyGen's host half: the per-sample Gaussian noise of alg:PubKeyGen (exactly the values vlp_pubkeygen
-// draws) and the PRNG prefix h1 = mix(seed ^ PK_A * C1) the device continues from.
-int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
-                     std::vector<uint32_t>& nz, uint64_t* h1) {
+// PubKeyGen's host half: the per-sample Gaussian noise of alg:PubKeyGen (exactly the values vlp_pubkeygen /
+// vlp_pubkeygen_secure draw under the same generator); the device continues the mask words.
+int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, const Rng& g, size_t first, size_t count,
+                     std::vector<uint32_t>& nz) {
   if (!sk) return fail(VLP_EINVAL, "null argument");
   if (int rc = check_meta(meta)) return rc;
   if (count == 0 || first + count > meta->M) return fail(VLP_EINVAL, "bad record range");
@@ -450,22 +459,21 @@ int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size
   parallel_for(count * per, [&](size_t idx) {
     const size_t rec = idx / per, row = idx % per;
     const size_t local = row < W * lI ? (row % lI) * W + row / lI : row;
-    nz[idx] = noise(seed, kPkE, (first + rec) * per + local, 0, sk->params.sigma_lwe);
+    nz[idx] = noise(g, kPkE, (first + rec) * per + local, 0, sk->params.sigma_lwe);
   });
-  *h1 = prng_prefix(seed, kPkA);
   return VLP_OK;
 }
 
-// Host half of vlp_encrypt_db_device (api.cu): PubKeyGen's noise and PRNG prefix plus ServerEnc's row bits.
-int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+// Host half of vlp_encrypt_db_device (api.cu): PubKeyGen's noise plus ServerEnc's row bits.
+int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, const Rng& g, size_t first, size_t count,
                        const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
-                       std::vector<uint8_t>& bits, uint64_t* h1) {
+                       std::vector<uint8_t>& bits) {
   if (!sk) return fail(VLP_EINVAL, "null argument");
   if (int rc = check_meta(meta)) return rc;
   if (count == 0 || first + count > meta->M) return fail(VLP_EINVAL, "bad record range");
   if (!words || !payloads) return fail(VLP_EINVAL, "null argument");
   if (int rc = prepare_db_bits(meta, count, words, payloads, bits)) return rc;
-  return prepare_pk_noise(sk, meta, seed, first, count, nz, h1);
+  return prepare_pk_noise(sk, meta, g, first, count, nz);
 }
 }  // namespace vlp
 

@@ -1176,8 +1176,9 @@ __global__ void __cluster_dims__(kC6, 1, 1) __launch_bounds__(kBT, 1) vlp_blind_
 
 // ================================================================================ device PubKeyGen + ServerEnc
 // (setup) one warp per DB ciphertext: the TLWE(0) public-key sample of alg:PubKeyGen
-// (mask words from the counter PRNG of R3, b = <a, s> + e with e computed on the host by the same libm
-// Box-Muller as vlp_pubkeygen) plus (0, Ecd(bit)) of alg:ServerEnc -- byte-identical to the host calls.
+// (mask words from the call's generator -- the seeded counter PRNG of R3 or ChaCha20 under the secure call's
+// key --, b = <a, s> + e with e computed on the host by the same libm Box-Muller as vlp_pubkeygen) plus
+// (0, Ecd(bit)) of alg:ServerEnc -- byte-identical to the host calls under the same generator.
 __device__ __forceinline__ uint64_t prng_mix(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -1185,8 +1186,65 @@ __device__ __forceinline__ uint64_t prng_mix(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// ChaCha20 block (RFC 8439 section 2.3) for the secure mask generator: key g.key, block counter `counter`,
+// nonce (dom, obj lo, obj hi) -- the words host.cpp's secure Rng draws (mask word w = output 2 (w mod 8) + 1 of block
+// w / 8, i.e. the high half of the generator's 64-bit word).
+__device__ __forceinline__ void chacha_qr(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  a += b; d = __funnelshift_l(d ^ a, d ^ a, 16);
+  c += d; b = __funnelshift_l(b ^ c, b ^ c, 12);
+  a += b; d = __funnelshift_l(d ^ a, d ^ a, 8);
+  c += d; b = __funnelshift_l(b ^ c, b ^ c, 7);
+}
+__device__ void chacha20_dev(const MaskGen& g, uint32_t counter, uint64_t obj, uint32_t (&out)[16]) {
+  const uint32_t in[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, g.key[0], g.key[1], g.key[2], g.key[3],
+                           g.key[4], g.key[5], g.key[6], g.key[7], counter, g.dom, static_cast<uint32_t>(obj),
+                           static_cast<uint32_t>(obj >> 32)};
+  uint32_t x[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) x[i] = in[i];
+#pragma unroll 1
+  for (int r = 0; r < 10; r++) {
+    chacha_qr(x[0], x[4], x[8], x[12]); chacha_qr(x[1], x[5], x[9], x[13]);
+    chacha_qr(x[2], x[6], x[10], x[14]); chacha_qr(x[3], x[7], x[11], x[15]);
+    chacha_qr(x[0], x[5], x[10], x[15]); chacha_qr(x[1], x[6], x[11], x[12]);
+    chacha_qr(x[2], x[7], x[8], x[13]); chacha_qr(x[3], x[4], x[9], x[14]);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; i++) out[i] = x[i] + in[i];
+}
+
+// The n uniform mask words of TLWE sample `obj` by one warp: ct[w] = a_w; returns <a, s> (all lanes).
+__device__ uint32_t warp_tlwe_mask(const MaskGen& g, uint64_t obj, const uint32_t* __restrict__ s, uint32_t* ct,
+                                   uint32_t lane) {
+  uint32_t b = 0;
+  if (g.secure) {
+    for (uint32_t c = lane; 8 * c < static_cast<uint32_t>(n); c += 32) {
+      uint32_t blk[16];
+      chacha20_dev(g, c, obj, blk);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t w = 8 * c + i;
+        if (w < static_cast<uint32_t>(n)) {
+          ct[w] = blk[2 * i + 1];
+          b += blk[2 * i + 1] * s[w];
+        }
+      }
+    }
+  } else {
+    const uint64_t h2 = prng_mix(g.h1 ^ (obj * 0xC2B2AE3D27D4EB4Full));
+    for (uint32_t w = lane; w < static_cast<uint32_t>(n); w += 32) {
+      const uint32_t a = static_cast<uint32_t>(prng_mix(h2 ^ (w * 0x165667B19E3779F9ull)) >> 32);
+      ct[w] = a;
+      b += a * s[w];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  return b;
+}
+
 __global__ void __launch_bounds__(256) vlp_encrypt_db_kernel(const uint32_t* __restrict__ s, const uint32_t* __restrict__ noise,
-                                                            const uint8_t* __restrict__ bits, uint64_t h1, uint32_t per,
+                                                            const uint8_t* __restrict__ bits, MaskGen g, uint32_t per,
                                                             uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples,
                                                             uint32_t* __restrict__ out) {
   const uint64_t idx = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1195,16 +1253,8 @@ __global__ void __launch_bounds__(256) vlp_encrypt_db_kernel(const uint32_t* __r
   const uint64_t rec = idx / per, row = idx % per;
   const uint64_t local = row < static_cast<uint64_t>(W) * lI ? (row % lI) * W + row / lI : row;  // alg:PubKeyGen order
   const uint64_t obj = (first + rec) * per + local;
-  const uint64_t h2 = prng_mix(h1 ^ (obj * 0xC2B2AE3D27D4EB4Full));
   uint32_t* ct = out + idx * kCt;
-  uint32_t b = 0;
-  for (uint32_t w = lane; w < static_cast<uint32_t>(n); w += 32) {
-    const uint32_t a = static_cast<uint32_t>(prng_mix(h2 ^ (w * 0x165667B19E3779F9ull)) >> 32);
-    ct[w] = a;
-    b += a * s[w];
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  const uint32_t b = warp_tlwe_mask(g, obj, s, ct, lane);
   if (lane == 0) {
     ct[n] = b + noise[idx] + (bits ? (bits[idx] ? kMu : 0u - kMu) : 0u);  // bits == nullptr: the pk sample alone
     ct[n + 1] = 0;
@@ -1225,50 +1275,50 @@ __global__ void __launch_bounds__(256) vlp_server_enc_kernel(const uint32_t* pk,
 // Device KeyGen, bootstrapping key (R4, O7): CTA per row (i, r): a_j = uniform(BSK_A, obj = i*6 + r, word j),
 // b = a * z + e (negacyclic, z binary: the sum of the rotations X^k a over supp z), then s_i g_j on component
 // r / 3's constant coefficient -- the same words vlp_keygen computes on the host.
-__global__ void __launch_bounds__(256) vlp_keygen_bsk_kernel(uint64_t h1, const uint32_t* __restrict__ s,
+__global__ void __launch_bounds__(256) vlp_keygen_bsk_kernel(MaskGen g, const uint32_t* __restrict__ s,
                                                             const uint32_t* __restrict__ z, const uint32_t* __restrict__ e,
                                                             uint32_t* __restrict__ bsk) {
   __shared__ uint32_t a[N];
   __shared__ uint32_t zs[N];
   const uint32_t ir = blockIdx.x;
-  const uint64_t h2 = prng_mix(h1 ^ (static_cast<uint64_t>(ir) * 0xC2B2AE3D27D4EB4Full));
-  for (uint32_t j = threadIdx.x; j < static_cast<uint32_t>(N); j += blockDim.x) {
-    a[j] = static_cast<uint32_t>(prng_mix(h2 ^ (static_cast<uint64_t>(j) * 0x165667B19E3779F9ull)) >> 32);
-    zs[j] = z[j];
+  if (g.secure) {
+    for (uint32_t c = threadIdx.x; c < static_cast<uint32_t>(N) / 8; c += blockDim.x) {
+      uint32_t blk[16];
+      chacha20_dev(g, c, ir, blk);
+#pragma unroll
+      for (int q = 0; q < 8; q++) a[8 * c + q] = blk[2 * q + 1];
+    }
+  } else {
+    const uint64_t h2 = prng_mix(g.h1 ^ (static_cast<uint64_t>(ir) * 0xC2B2AE3D27D4EB4Full));
+    for (uint32_t j = threadIdx.x; j < static_cast<uint32_t>(N); j += blockDim.x)
+      a[j] = static_cast<uint32_t>(prng_mix(h2 ^ (static_cast<uint64_t>(j) * 0x165667B19E3779F9ull)) >> 32);
   }
+  for (uint32_t j = threadIdx.x; j < static_cast<uint32_t>(N); j += blockDim.x) zs[j] = z[j];
   __syncthreads();
   uint32_t* ra = bsk + static_cast<size_t>(ir) * 2 * N;
   uint32_t* rb = ra + N;
   const uint32_t i = ir / kRows, r = ir % kRows;
-  const uint32_t g = s[i] ? 1u << (32 - kBgBits * (r % kEll + 1)) : 0u;
+  const uint32_t sg = s[i] ? 1u << (32 - kBgBits * (r % kEll + 1)) : 0u;  // s_i g_j
   for (uint32_t t = threadIdx.x; t < static_cast<uint32_t>(N); t += blockDim.x) {
     uint32_t acc = 0;
     for (uint32_t k = 0; k <= t; k++) acc += zs[k] ? a[t - k] : 0u;
     for (uint32_t k = t + 1; k < static_cast<uint32_t>(N); k++) acc -= zs[k] ? a[t + N - k] : 0u;
     acc += e[static_cast<size_t>(ir) * N + t];
-    if (t == 0 && r / kEll == 1) acc += g;
+    if (t == 0 && r / kEll == 1) acc += sg;
     rb[t] = acc;
-    ra[t] = a[t] + ((t == 0 && r / kEll == 0) ? g : 0u);
+    ra[t] = a[t] + ((t == 0 && r / kEll == 0) ? sg : 0u);
   }
 }
 
 // Device KeyGen, key-switching key (O10): warp per row idx = (i*8 + j)*3 + v-1: TLWE_s(v z_i 2^(32-2(j+1))).
-__global__ void __launch_bounds__(256) vlp_keygen_ksk_kernel(uint64_t h1, const uint32_t* __restrict__ s,
+__global__ void __launch_bounds__(256) vlp_keygen_ksk_kernel(MaskGen g, const uint32_t* __restrict__ s,
                                                             const uint32_t* __restrict__ z, const uint32_t* __restrict__ e,
                                                             uint32_t* __restrict__ ksk) {
   const uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
   if (idx >= static_cast<uint32_t>(N * kKsT * 3)) return;
   const uint32_t i = idx / (kKsT * 3), j = (idx / 3) % kKsT, v = idx % 3 + 1;
-  const uint64_t h2 = prng_mix(h1 ^ (static_cast<uint64_t>(idx) * 0xC2B2AE3D27D4EB4Full));
   uint32_t* ct = ksk + static_cast<size_t>(idx) * kCt;
-  uint32_t b = 0;
-  for (uint32_t w = lane; w < static_cast<uint32_t>(n); w += 32) {
-    const uint32_t a = static_cast<uint32_t>(prng_mix(h2 ^ (static_cast<uint64_t>(w) * 0x165667B19E3779F9ull)) >> 32);
-    ct[w] = a;
-    b += a * s[w];
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  const uint32_t b = warp_tlwe_mask(g, idx, s, ct, lane);
   if (lane == 0) {
     ct[n] = b + v * z[i] * (1u << (32 - kKsBaseBits * (j + 1))) + e[idx];
     ct[n + 1] = 0;
@@ -1281,18 +1331,18 @@ cudaError_t launch_server_enc(const uint32_t* pk, const uint8_t* bits, uint64_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_keygen(uint64_t h_bsk, uint64_t h_ksk, const uint32_t* s, const uint32_t* z, const uint32_t* e_bsk,
+cudaError_t launch_keygen(const MaskGen& g_bsk, const MaskGen& g_ksk, const uint32_t* s, const uint32_t* z, const uint32_t* e_bsk,
                           const uint32_t* e_ksk, uint32_t* bsk, uint32_t* ksk, cudaStream_t st) {
-  vlp_keygen_bsk_kernel<<<n * kRows, 256, 0, st>>>(h_bsk, s, z, e_bsk, bsk);
-  vlp_keygen_ksk_kernel<<<(N * kKsT * 3 + 7) / 8, 256, 0, st>>>(h_ksk, s, z, e_ksk, ksk);
+  vlp_keygen_bsk_kernel<<<n * kRows, 256, 0, st>>>(g_bsk, s, z, e_bsk, bsk);
+  vlp_keygen_ksk_kernel<<<(N * kKsT * 3 + 7) / 8, 256, 0, st>>>(g_ksk, s, z, e_ksk, ksk);
   return cudaGetLastError();
 }
 
-cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
+cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, const MaskGen& g, uint32_t per,
                               uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st) {
   if (!nsamples) return cudaSuccess;
   const uint64_t blocks = (nsamples * 32 + 255) / 256;
-  vlp_encrypt_db_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(s, noise, bits, h1, per, W, lI, first, nsamples, out);
+  vlp_encrypt_db_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(s, noise, bits, g, per, W, lI, first, nsamples, out);
   return cudaGetLastError();
 }
 

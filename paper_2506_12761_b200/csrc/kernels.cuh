@@ -91,10 +91,18 @@ void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st);
 int set_br_route(int engine, int param);  // vlp_debug_route
 int br_launch_count(uint32_t njobs, int sm_count);
-cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, uint64_t h1, uint32_t per,
+// The mask generator a device kernel continues (host.cpp's Rng of the call): seeded, h1 = mix(seed ^ dom * C1)
+// (R3); secure, ChaCha20 under `key` with nonce (dom, obj lo, obj hi) and block counter word / 8.
+struct MaskGen {
+  uint64_t h1;
+  uint32_t key[8];
+  uint32_t dom;
+  uint32_t secure;
+};
+cudaError_t launch_encrypt_db(const uint32_t* s, const uint32_t* noise, const uint8_t* bits, const MaskGen& g, uint32_t per,
                               uint32_t W, uint32_t lI, uint64_t first, uint64_t nsamples, uint32_t* out, cudaStream_t st);
 cudaError_t launch_server_enc(const uint32_t* pk, const uint8_t* bits, uint64_t nsamples, uint32_t* out, cudaStream_t st);
-cudaError_t launch_keygen(uint64_t h_bsk, uint64_t h_ksk, const uint32_t* s, const uint32_t* z, const uint32_t* e_bsk,
+cudaError_t launch_keygen(const MaskGen& g_bsk, const MaskGen& g_ksk, const uint32_t* s, const uint32_t* z, const uint32_t* e_bsk,
                           const uint32_t* e_ksk, uint32_t* bsk, uint32_t* ksk, cudaStream_t st);
 void launch_kmat_sw(const uint32_t* ksk, int8_t* kmat_sw, cudaStream_t st);
 size_t ks_stage_bytes_t(uint32_t chunk);

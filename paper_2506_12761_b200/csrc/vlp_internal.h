@@ -31,18 +31,33 @@ enum : uint64_t {
   kPkA = 7, kPkE = 8, kQryA = 9, kQryE = 10, kFreshA = 12, kFreshE = 13
 };
 uint64_t prng(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t word);
-uint32_t noise(uint64_t seed, uint64_t dom, uint64_t obj, uint64_t t, double sigma);
-int resolve_params(const vlp_params* params, vlp_params* out);
-void secret_keys(uint64_t seed, vlp_sk* sk);
-void keygen_noise(uint64_t seed, const vlp_params& p, uint32_t* bsk_noise, uint32_t* ksk_noise);
 uint64_t prng_prefix(uint64_t seed, uint64_t dom);
+void chacha20_block(const uint32_t key[8], uint32_t counter, const uint32_t nonce[3], uint32_t out[16]);
+
+// The randomness of one call: the seeded counter PRNG (R3; reproducible, 64-bit seed: tests and benchmarks), or
+// ChaCha20 under a 256-bit key drawn from the OS (getrandom) for the *_secure calls.  Either way a random-access
+// generator u64(dom, obj, word); the secure one uses nonce (dom, obj), block counter word / 8.
+struct Rng {
+  uint64_t seed = 0;
+  bool secure = false;
+  uint32_t key[8] = {};
+  uint64_t u64(uint64_t dom, uint64_t obj, uint64_t word) const;
+  ~Rng();
+};
+Rng seeded(uint64_t seed);
+int os_random(Rng* r);  // secure generator: getrandom key (or the key of vlp_debug_next_secure_key)
+uint32_t noise(const Rng& g, uint64_t dom, uint64_t obj, uint64_t t, double sigma);  // Box-Muller (R2, R3)
+
+int resolve_params(const vlp_params* params, vlp_params* out);
+void secret_keys(const Rng& g, vlp_sk* sk);
+void keygen_noise(const Rng& g, const vlp_params& p, uint32_t* bsk_noise, uint32_t* ksk_noise);
 int prepare_db_bits(const vlp_meta* meta, size_t count, const uint64_t* words, const uint64_t* payloads,
                     std::vector<uint8_t>& bits);
-int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
-                     std::vector<uint32_t>& nz, uint64_t* h1);
-int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, uint64_t seed, size_t first, size_t count,
+int prepare_pk_noise(const vlp_sk* sk, const vlp_meta* meta, const Rng& g, size_t first, size_t count,
+                     std::vector<uint32_t>& nz);
+int prepare_encrypt_db(const vlp_sk* sk, const vlp_meta* meta, const Rng& g, size_t first, size_t count,
                        const uint64_t* words, const uint64_t* payloads, std::vector<uint32_t>& nz,
-                       std::vector<uint8_t>& bits, uint64_t* h1);
+                       std::vector<uint8_t>& bits);
 
 int check_meta(const vlp_meta* m);
 // Bound words per record (R17) and query words.

@@ -641,6 +641,38 @@ def test_device_keygen_equals_host():
         assert np.array_equal(x, y)
 
 
+def _next_key(key):
+    k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32))
+    A.check(A.lib().vlp_debug_next_secure_key(A._u32p(k)))
+
+
+def test_device_secure_preprocessing_equals_host_secure(server):
+    """The secure device calls draw their masks from ChaCha20 on the device: under one key (the test hook
+    vlp_debug_next_secure_key) vlp_keygen_device_secure == vlp_keygen_secure and vlp_pubkeygen_device_secure ==
+    vlp_pubkeygen_secure, byte for byte; the default Python calls (no seed) give fresh samples that decrypt to the
+    records' bits."""
+    key = (np.arange(8, dtype=np.uint32) * 0x9E3779B9 + 17).astype(np.uint32)
+    _next_key(key)
+    kh = A.Keys()
+    _next_key(key)
+    kd = A.Keys(device=0)
+    for x, y in zip(kh.export(), kd.export()):
+        assert np.array_equal(x, y)
+    wl = make_workload(9, key_seed=SEED)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+    k = server.keys
+    _next_key(key)
+    host = k.encrypt_db(m, wl.records[:16], wl.payloads[:16], count=16)
+    _next_key(key)
+    pk = A.pubkeygen_device(k, m, None, 0, 16)
+    db = A.server_encrypt_db_device(m, pk, wl.records[:16], wl.payloads[:16])
+    assert np.array_equal(A.to_host(db), host)
+    fresh = A.to_host(A.server_encrypt_db_device(m, A.pubkeygen_device(k, m, None, 0, 16), wl.records[:16],
+                                                 wl.payloads[:16]))
+    assert not np.array_equal(fresh, host)
+    assert np.array_equal(k.decrypt_bits(fresh), k.decrypt_bits(host))
+
+
 @pytest.mark.parametrize("cfg,count", [(1, None), (9, 16), (3, 512)])
 def test_role_separated_device_preprocessing(server, cfg, count):
     """P:192 roles on the GPU: the client's device PubKeyGen (takes sk) then the server's device ServerEnc (takes

@@ -253,3 +253,31 @@ def test_secure_calls_are_fresh_and_correct():
     db = k1.encrypt_db(m, np.array([[3, 9], [0, 200]], np.uint64), np.array([5, 10], np.uint64))
     want = [(3 >> j) & 1 for j in range(8)] + [(9 >> j) & 1 for j in range(8)] + [(5 >> j) & 1 for j in range(4)]
     assert list(k1.decrypt_bits(db[:20])) == want
+
+
+def _next_key(key):
+    k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32))
+    A.check(A.lib().vlp_debug_next_secure_key(A._u32p(k)))
+
+
+def test_secure_key_hook_is_single_use():
+    """vlp_debug_next_secure_key (test hook): the next secure call of this thread takes the given ChaCha20 key --
+    the same key gives the same keys and pk bytes --, and the call after it is back on getrandom."""
+    key = np.arange(1, 9, dtype=np.uint32) * 0x01010101
+    _next_key(key)
+    k1 = A.Keys()
+    _next_key(key)
+    k2 = A.Keys()
+    k3 = A.Keys()
+    for x, y in zip(k1.export(), k2.export()):
+        assert np.array_equal(x, y)
+    assert not np.array_equal(k1.export()[0], k3.export()[0])
+    m = A.meta(L.MODE_INTV, 2, 8, 4, 1)
+    words, pays = np.array([[3, 9], [0, 200]], np.uint64), np.array([5, 10], np.uint64)
+    _next_key(key)
+    db1 = k1.encrypt_db(m, words, pays)
+    _next_key(key)
+    db2 = k1.encrypt_db(m, words, pays)
+    db3 = k1.encrypt_db(m, words, pays)
+    assert np.array_equal(db1, db2) and not np.array_equal(db1, db3)
+    assert list(k1.decrypt_bits(db1[:20])) == list(k1.decrypt_bits(db3[:20]))
