@@ -302,6 +302,11 @@ int vlp_debug_keyswitch(vlp_server* server, const uint32_t* nlwe_dev, size_t cou
  * VLP_BR_BOOT meaning: 1-5 bootstraps per CTA, -1 latency, -2 2-CTA cluster, -3 6-CTA cluster);
  * 2 = K2F with param warps (1-8) per CTA for whole levels.  Returns VLP_EINVAL on other values. */
 int vlp_debug_route(int engine, int param);
+/* Test hook (process-wide): while err_dev != NULL, every K2F launch (the FP64 FFT engine)
+ * runs its monitoring build and atomically raises *err_dev to the largest distance |V - round(V)| between a limb
+ * result and the integer it rounds to, as the bit pattern of a non-negative double (the exactness margin is 1/2).
+ * err_dev: caller-owned device memory (8 bytes, zero it first).  NULL turns the monitor off. */
+int vlp_debug_fft_error(uint64_t* err_dev);
 
 /* ---- The problem-statement calls (the north star's keygen / encrypt_query / server_eval /
  * decrypt_result).  They wrap the program calls above: the schedule for a (meta, first, count) shard, a

@@ -105,6 +105,7 @@ SIGNATURES = {
     "vlp_debug_blind_rotate": (_i, [_vp, _vp, _sz, _i, _vp, _vp, _u64]),
     "vlp_debug_keyswitch": (_i, [_vp, _vp, _sz, _vp, _vp, _u64]),
     "vlp_debug_route": (_i, [_i, _i]),
+    "vlp_debug_fft_error": (_i, [_vp]),
     "vlp_server_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t),
                                         ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_server_eval": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _vp, _vp, _vp, _vp, _sz, _u64]),

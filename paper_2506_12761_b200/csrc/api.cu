@@ -736,6 +736,11 @@ int vlp_program_profile_read(vlp_program* p, double* br_ms, double* ks_ms, uint6
   return VLP_OK;
 }
 
+int vlp_debug_fft_error(uint64_t* err_dev) {
+  set_fft_error_monitor(reinterpret_cast<unsigned long long*>(err_dev));
+  return VLP_OK;
+}
+
 int vlp_debug_route(int engine, int param) {
   return set_br_route(engine, param) == 0 ? VLP_OK : fail(VLP_EINVAL, "vlp_debug_route: bad engine / param");
 }

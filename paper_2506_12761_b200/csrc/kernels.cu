@@ -1622,6 +1622,10 @@ int set_br_route(int engine, int param) {
   }
   return 0;
 }
+// vlp_debug_fft_error: every K2F launch records its largest rounding distance (debug; nullptr = off)
+static std::atomic<unsigned long long*> g_fft_err{nullptr};
+void set_fft_error_monitor(unsigned long long* err_dev) { g_fft_err.store(err_dev); }
+
 static int forced_boot() { return route().boot; }
 static int forced_fft_warps() { return route().fft_warps; }
 static bool fft_engine() { return route().engine == 1; }
@@ -1637,10 +1641,15 @@ int br_launch_count(uint32_t njobs, int sm_count) {
   return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
 }
 
+static cudaError_t launch_blind_rotate_fft_mon(BrArgs a, int warps, int sm_count, cudaStream_t st) {
+  a.fft_err = g_fft_err.load();
+  return launch_blind_rotate_fft(a, warps, sm_count, st);
+}
+
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) {
   if (a.njobs == 0) return cudaSuccess;
   const int forced = forced_boot();
-  if (forced_fft_warps()) return launch_blind_rotate_fft(a, forced_fft_warps(), sm_count, st);
+  if (forced_fft_warps()) return launch_blind_rotate_fft_mon(a, forced_fft_warps(), sm_count, st);
   if (forced >= 1 && forced <= kBrBoot) return launch_br_width(a, forced, sm_count, st);
   if (forced == -1) return launch_br_width(a, 0, sm_count, st);   // VLP_BR_BOOT=-1: latency mode
   if (forced == -2) return launch_br_width(a, -1, sm_count, st);  // VLP_BR_BOOT=-2: cluster latency mode
@@ -1653,7 +1662,7 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
   if (full) {
     BrArgs f = a;
     f.njobs = full;
-    e = fft ? launch_blind_rotate_fft(f, kFftMaxWarps, sm_count, st) : launch_br_width(f, kBrBoot, sm_count, st);
+    e = fft ? launch_blind_rotate_fft_mon(f, kFftMaxWarps, sm_count, st) : launch_br_width(f, kBrBoot, sm_count, st);
     if (e != cudaSuccess) return e;
   }
   if (tail) {
@@ -1666,7 +1675,7 @@ cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st) 
     const uint32_t per = (tail + sm_count - 1) / sm_count;
     // K2F's single-warp bootstraps have a long per-step latency (one bootstrap per SM takes ~11 ms for 630 steps,
     // 2-4 per SM about the same), so tails of at most kBrBoot per SM run on the NTT kernels (K2<b>: 6.1-12.7 ms)
-    if (fft && per > static_cast<uint32_t>(kBrBoot)) return launch_blind_rotate_fft(r, static_cast<int>(per), sm_count, st);
+    if (fft && per > static_cast<uint32_t>(kBrBoot)) return launch_blind_rotate_fft_mon(r, static_cast<int>(per), sm_count, st);
     const int b = tail <= c6_max_clusters() ? -2
                   : tail <= static_cast<uint32_t>(sm_count / 2) ? -1
                   : tail <= static_cast<uint32_t>(sm_count) ? 0

@@ -60,6 +60,7 @@ struct BrArgs {
   const uint2* twl_inv;
   const double2* bskf;  // FFT-domain bsk (K2F engine), layout [i][chunk 12][rho' 8][o*2 + l][lane 32] complex
   const double2* psi;   // psi^e = exp(i pi e / 1024), e < 2048 (K2F per-lane twiddles)
+  unsigned long long* fft_err;  // debug (vlp_debug_fft_error): max |V - round(V)| of K2F's roundings, double bits
   uint32_t zero;  // always 0 (a runtime zero; see add_alu in kernels.cu)
   uint32_t p2;    // always 2p, set by launch_blind_rotate (a runtime constant; see ct_bfly in kernels.cu)
 };
@@ -90,6 +91,7 @@ void set_const_twiddles(const uint2* fwd16, const uint2* inv16);
 // one level: whole waves of kBrBoot bootstraps per CTA + a narrower tail wave (1 or 2 kernel launches)
 cudaError_t launch_blind_rotate(const BrArgs& a, int sm_count, cudaStream_t st);
 int set_br_route(int engine, int param);  // vlp_debug_route
+void set_fft_error_monitor(unsigned long long* err_dev);  // vlp_debug_fft_error
 int br_launch_count(uint32_t njobs, int sm_count);
 // The mask generator a device kernel continues (host.cpp's Rng of the call): seeded, h1 = mix(seed ^ dom * C1)
 // (R3); secure, ChaCha20 under `key` with nonce (dom, obj lo, obj hi) and block counter word / 8.

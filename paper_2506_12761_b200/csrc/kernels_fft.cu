@@ -321,7 +321,7 @@ __device__ unsigned long long g_phase[8];
 //   for o in {0, 1}: inverse FFT of acc4[o][0], acc4[o][1] -> round -> acc_o += R_lo + 2^16 R_hi (mod 2^32).
 // The key of a step is 12 chunks of 16 KB (digit row r, register half h: [rho' 8][o*2 + l][lane 32]) streamed by
 // TMA into a ring shared by the CTA's warps; the last warp to release a chunk refills its slot.
-template <int W>
+template <int W, bool ERR = false>
 __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const BrArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   double2* ring = reinterpret_cast<double2*>(smem);
@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
     __syncwarp();
 
     // ---- S5: CMux steps
+    double err = 0.0;  // ERR: this lane's largest rounding distance
     VLP_PHASE_DECL
     for (uint32_t i = 0; i < steps; i++) {
       const uint32_t ab = abar[i];
@@ -497,6 +498,10 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
         for (int q = 0; q < 16; q++) {
           const uint32_t rx = (q & 1) ? round_u32s<1>(V[q].x, lc) : round_u32s<0>(V[q].x, lc);
           const uint32_t ry = (q & 1) ? round_u32s<1>(V[q].y, lc) : round_u32s<0>(V[q].y, lc);
+          if (ERR) {  // distance of each limb result to the integer it rounds to (exactness margin: < 1/2)
+            err = fmax(err, fabs(V[q].x - rint(V[q].x)));
+            err = fmax(err, fabs(V[q].y - rint(V[q].y)));
+          }
           ao[32 * q] += rx << sh;
           ao[512 + 32 * q] += ry << sh;
         }
@@ -505,6 +510,11 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
       __syncwarp();
     }
     VLP_PHASE_OUT
+    if (ERR) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, o));
+      if (lane == 0) atomicMax(a.fft_err, static_cast<unsigned long long>(__double_as_longlong(err)));
+    }
 
     // ---- S6 SampleExtract: a'_0 = a_0, a'_k = -a_{N-k}, b' = b_0
     if (a.raw_acc) {
@@ -581,8 +591,8 @@ void set_fft_constants(const double2* psi) {
   cudaMemcpyToSymbol(c_w32, w32, sizeof(w32));
 }
 
-template <int W>
-static cudaError_t launch_fft_w(const BrArgs& a, int sm_count, cudaStream_t st) {
+template <int W, bool ERR>
+static cudaError_t launch_fft_wk(const BrArgs& a, int sm_count, cudaStream_t st) {
   static std::atomic<uint64_t> attr_set{0};
   const int smem = fft_smem_bytes(W) > kFSmemMin ? fft_smem_bytes(W) : kFSmemMin;
   int dev = 0;
@@ -590,7 +600,7 @@ static cudaError_t launch_fft_w(const BrArgs& a, int sm_count, cudaStream_t st) 
   if (e != cudaSuccess) return e;
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_set.load() & bit)) {
-    e = cudaFuncSetAttribute(vlp_blind_rotate_fft_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = cudaFuncSetAttribute(vlp_blind_rotate_fft_kernel<W, ERR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit);
   }
@@ -599,8 +609,12 @@ static cudaError_t launch_fft_w(const BrArgs& a, int sm_count, cudaStream_t st) 
   const int grid = static_cast<int>(groups < static_cast<uint64_t>(sm_count) ? groups : sm_count);
   if (grid <= 0 || (groups + grid - 1) / grid * static_cast<uint64_t>(a.steps) * kFftChunks >= (1ull << 32))
     return cudaErrorInvalidValue;
-  vlp_blind_rotate_fft_kernel<W><<<grid, W * 32, smem, st>>>(a);
+  vlp_blind_rotate_fft_kernel<W, ERR><<<grid, W * 32, smem, st>>>(a);
   return cudaGetLastError();
+}
+template <int W>
+static cudaError_t launch_fft_w(const BrArgs& a, int sm_count, cudaStream_t st) {
+  return a.fft_err ? launch_fft_wk<W, true>(a, sm_count, st) : launch_fft_wk<W, false>(a, sm_count, st);
 }
 
 cudaError_t launch_blind_rotate_fft(const BrArgs& a, int warps, int sm_count, cudaStream_t st) {

@@ -387,6 +387,32 @@ def test_all_trivial_extreme_widths(server, case):
     assert [int(x) for x in out[:, 630]] == [0x20000000 if (want >> j) & 1 else 0xE0000000 for j in range(l_S)]
 
 
+def test_fft_rounding_margin_at_scale(server, route):
+    """K2F's exactness argument measured on the product kernel: with the rounding monitor on
+    (vlp_debug_fft_error), every limb result of a full config-2 evaluation (132,080 bootstraps x 630 steps x 4,096
+    roundings = 3.4e11) and of a wave of extreme-digit inputs (accumulator words near +-2^31: digits of magnitude
+    64) lies within 2^-10 of the integer it rounds to -- the margin is 1/2 -- and the monitored build gives the same
+    bytes as the product build."""
+    err = torch.zeros(1, dtype=torch.int64, device="cuda:0")
+    wl = make_workload(2, key_seed=SEED)
+    k = server.keys
+    _, _, _, plain = _run_config(server, wl)
+    A.check(A.lib().vlp_debug_fft_error(ctypes.c_void_p(err.data_ptr())))
+    try:
+        _, _, _, mon = _run_config(server, wl)
+        assert np.array_equal(mon, plain)
+        cts = k.encrypt_bits(np.random.default_rng(8).integers(0, 2, 1184, dtype=np.uint8), 41)
+        cts[:, 631] = 0x80000000  # acc = +-mu everywhere after the test-vector rotation: D = +-2 mu
+        route(2, 8)
+        server.debug_blind_rotate(A.to_device(cts), 630)
+        torch.cuda.synchronize()
+    finally:
+        A.check(A.lib().vlp_debug_fft_error(None))
+    worst = float(np.array([int(err.item())], dtype=np.int64).view(np.float64)[0])
+    print(f"K2F largest rounding distance: {worst:.3e}")
+    assert 0.0 < worst < 2.0 ** -10
+
+
 def test_config2_full_size_sampled(server):
     """Config 2 at full size (IntV 1D, 1024 records, 132,080 BR) in the production layout (rows recycled by
     liveness, as bench.py runs it): predicate + records 3 and 1023 byte-equal."""
