@@ -511,7 +511,8 @@ def main():
                          "impl_achieved": fp64, "impl_peak": fp64_peak(), "impl_ops_per_br": FP64_PER_BR,
                          "br_kernel_ms_per_step": br_ms / args.steps, "ks_kernel_ms_per_step": ks_ms / args.steps,
                          "br_share_of_step": br_ms / args.steps / ms_per_step,
-                         "br_launch_avg_ms": br_launch_ms,
+                         # one blind-rotation call per level (its whole waves launch one kernel each, plus a tail)
+                         "br_level_call_avg_ms": br_launch_ms,
                          "traffic": TRAFFIC_BYTES_PER_WAVE, "traffic_source": TRAFFIC_SOURCE,
                          "traffic_unit": "bytes per whole-wave K2F launch"},
             # bootstrapping-key streaming against HBM (north star): one FFT-domain key pass per wave of 8 bootstraps

@@ -1636,9 +1636,13 @@ static bool forced_any() {
 
 int br_launch_count(uint32_t njobs, int sm_count) {
   if (njobs == 0) return 0;
+  if (forced_fft_warps()) return static_cast<int>(fft_launch_count(njobs, forced_fft_warps(), sm_count));
   if (forced_any()) return 1;
-  const uint32_t wave = static_cast<uint32_t>(fft_engine() ? kFftMaxWarps : kBrBoot) * static_cast<uint32_t>(sm_count);
-  return (njobs >= wave ? 1 : 0) + (njobs % wave ? 1 : 0);
+  const bool fft = fft_engine();
+  const uint32_t wave = static_cast<uint32_t>(fft ? kFftMaxWarps : kBrBoot) * static_cast<uint32_t>(sm_count);
+  const uint32_t full = njobs / wave * wave;
+  const int nfull = full == 0 ? 0 : (fft ? static_cast<int>(fft_launch_count(full, kFftMaxWarps, sm_count)) : 1);
+  return nfull + (njobs % wave ? 1 : 0);
 }
 
 static cudaError_t launch_blind_rotate_fft_mon(BrArgs a, int warps, int sm_count, cudaStream_t st) {

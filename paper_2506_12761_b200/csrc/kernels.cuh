@@ -84,6 +84,7 @@ constexpr size_t kPsiBytes = 2048 * sizeof(double2);
 void launch_bsk_fft(const uint32_t* raw, double2* out, const double2* psi, cudaStream_t st);
 void set_fft_constants(const double2* psi_host);
 cudaError_t launch_blind_rotate_fft(const BrArgs& a, int warps, int sm_count, cudaStream_t st);
+uint32_t fft_launch_count(uint32_t njobs, int warps, int sm_count);  // kernel launches of one K2F level
 
 void launch_bsk_convert(const uint32_t* raw, uint32_t* out, const uint2* tw_fwd, uint32_t c_mont,
                         cudaStream_t st);

@@ -20,7 +20,9 @@
 //    accumulators per point parked in TMEM (tcgen05.ld / st, 256 columns per warp; no MMA).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 
 #include "devcommon.cuh"
@@ -612,8 +614,43 @@ static cudaError_t launch_fft_wk(const BrArgs& a, int sm_count, cudaStream_t st)
   vlp_blind_rotate_fft_kernel<W, ERR><<<grid, W * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
+static int waves_per_launch() {
+  // One launch per wave (default; VLP_FFT_WAVES=k: at most k waves per launch, 0: one persistent launch): the CTAs
+  // of a persistent multi-wave launch drift apart by whole groups, so the key chunks they stream span many CMux
+  // steps and miss in L2; relaunching per wave keeps all CTAs on the same steps (221-wave level: 17.02 -> 16.57 ms
+  // per wave, tools/wave_drift.py).
+  static const int per_launch = [] {
+    const char* e = getenv("VLP_FFT_WAVES");
+    return e ? atoi(e) : 1;
+  }();
+  return per_launch;
+}
+
+uint32_t fft_launch_count(uint32_t njobs, int warps, int sm_count) {
+  if (njobs == 0) return 0;
+  const uint64_t wave = static_cast<uint64_t>(warps) * static_cast<uint64_t>(sm_count);
+  const int k = waves_per_launch();
+  if (k <= 0 || njobs <= wave * k) return 1;
+  const uint64_t span = wave * static_cast<uint64_t>(k);
+  return static_cast<uint32_t>((njobs + span - 1) / span);
+}
+
 template <int W>
 static cudaError_t launch_fft_w(const BrArgs& a, int sm_count, cudaStream_t st) {
+  const int per_launch = waves_per_launch();
+  const uint64_t wave = static_cast<uint64_t>(W) * static_cast<uint64_t>(sm_count);
+  if (per_launch > 0 && a.njobs > wave * per_launch) {
+    const uint64_t span = wave * static_cast<uint64_t>(per_launch);
+    for (uint64_t off = 0; off < a.njobs; off += span) {
+      BrArgs b = a;
+      b.jobs = a.jobs + off;
+      b.njobs = static_cast<uint32_t>(std::min<uint64_t>(span, a.njobs - off));
+      if (a.raw_acc) b.raw_acc = a.raw_acc + off * 2 * N;
+      const cudaError_t e = a.fft_err ? launch_fft_wk<W, true>(b, sm_count, st) : launch_fft_wk<W, false>(b, sm_count, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   return a.fft_err ? launch_fft_wk<W, true>(a, sm_count, st) : launch_fft_wk<W, false>(a, sm_count, st);
 }
 
