@@ -298,6 +298,25 @@ __device__ __forceinline__ void mac_half(const cd (&X)[16], int h, const double2
 // the warps of a launch (read by vlp_debug_phase_read).  Compiled out of the product library.
 #ifdef VLP_PHASE_TIMING
 __device__ unsigned long long g_phase[8];
+__device__ unsigned long long g_cta[3 * 1024];  // per CTA: start, end (globaltimer ns), SM id
+__device__ unsigned long long g_cta_ph[8 * 1024];  // per CTA: phase cycles summed over its warps
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define VLP_CTA_START \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta[3 * blockIdx.x] = gtimer();
+#define VLP_CTA_END                                      \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {           \
+    g_cta[3 * blockIdx.x + 1] = gtimer();                \
+    g_cta[3 * blockIdx.x + 2] = smid();                  \
+  }
 #define VLP_PHASE_DECL \
   unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; \
   long long ph_t = clock64();
@@ -307,13 +326,18 @@ __device__ unsigned long long g_phase[8];
     ph_acc[k] += static_cast<unsigned long long>(t_ - ph_t); \
     ph_t = t_;                                               \
   }
-#define VLP_PHASE_OUT \
-  if (lane == 0)      \
-    for (int k_ = 0; k_ < 8; k_++) atomicAdd(&g_phase[k_], ph_acc[k_]);
+#define VLP_PHASE_OUT                                                                 \
+  if (lane == 0) {                                                                    \
+    for (int k_ = 0; k_ < 8; k_++) atomicAdd(&g_phase[k_], ph_acc[k_]);              \
+    if (blockIdx.x < 1024)                                                            \
+      for (int k_ = 0; k_ < 8; k_++) atomicAdd(&g_cta_ph[8 * blockIdx.x + k_], ph_acc[k_]); \
+  }
 #else
 #define VLP_PHASE_DECL
 #define VLP_PHASE_MARK(k)
 #define VLP_PHASE_OUT
+#define VLP_CTA_START
+#define VLP_CTA_END
 #endif
 
 // ================================================================================ K2F blind rotation
@@ -360,6 +384,7 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  VLP_CTA_START
   // this warp's 256 TMEM columns in its lane quadrant: column rho * 16 + (o * 2 + l) * 4 + {re lo, re hi, im lo, im hi}
   const uint32_t tm = *tmem_base_sh + ((32u * (w & 3u)) << 16) + (w >> 2) * 256u;
 
@@ -531,6 +556,7 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  VLP_CTA_END
   if (tid < 32)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base_sh), "n"(kCols) : "memory");
 }
@@ -571,6 +597,13 @@ __global__ void __launch_bounds__(512) vlp_bsk_fft_kernel(const uint32_t* __rest
 }
 
 #ifdef VLP_PHASE_TIMING
+extern "C" int vlp_debug_cta_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_cta, sizeof(unsigned long long) * 3 * 1024);
+  cudaMemcpyFromSymbol(out + 3 * 1024, g_cta_ph, sizeof(unsigned long long) * 8 * 1024);
+  const unsigned long long z[8 * 1024] = {};
+  cudaMemcpyToSymbol(g_cta_ph, z, sizeof(z));
+  return 0;
+}
 extern "C" int vlp_debug_phase_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 8);
   const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
