@@ -106,6 +106,27 @@ def test_default_route_wave_and_tail_bit_exact(server, okeys, extra):
         assert np.array_equal(got[i], w), (extra, i)
 
 
+def test_multi_wave_level_one_launch_per_wave(server, okeys, route):
+    """A level of 3 whole K2F waves + 100 (one kernel launch per wave, then the tail): every row byte-equal to the
+    same level on the NTT engine (K2 waves + K2 tail) after 3 CMux steps, and sampled rows (first / last of each
+    wave, the ragged end) byte-equal to the oracle."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    count = 3 * 8 * sms + 100
+    rng = np.random.default_rng(77)
+    cts = rand_tlwe(rng, count)
+    cts[:, 631] = 0
+    dev = A.to_device(cts)
+    got = A.to_host(server.debug_blind_rotate(dev, 3))
+    route(1, 0)
+    ntt = A.to_host(server.debug_blind_rotate(dev, 3))
+    assert np.array_equal(got, ntt)
+    w = 8 * sms
+    idx = sorted(set([0, w - 1, w, 2 * w - 1, 2 * w, 3 * w - 1, 3 * w, count - 1]))
+    want = list(POOL.map(lambda i: okeys.blind_rotate(cts[i, :631], 3), idx))
+    for i, x in zip(idx, want):
+        assert np.array_equal(got[i], x), i
+
+
 def test_blind_rotate_steps_bit_exact(server, okeys, route):
     """K2 (NTT engine, forced) after 1, 2 and 7 CMux steps (raw TRLWE accumulator) == oracle BlindRotate, 9 inputs (3 CTAs,
     ragged), uniformly random masks (every abar_i != 0 path) plus one trivial input."""
