@@ -18,6 +18,10 @@
 //    path: the warps of a CTA meet only at the shared key ring (TMA bulk copies, mbarriers).
 //  * per digit row, the MAC acc[o][l] += X_r * B_r[o][l] runs right after the row's FFT with the four complex
 //    accumulators per point parked in TMEM (tcgen05.ld / st, 256 columns per warp; no MMA).
+//  * one kernel launch per wave of 8 x SMs bootstraps (launch_fft_w): all CTAs of a launch walk the 630 steps
+//    together, so each key chunk is fetched from DRAM once and served to the other CTAs from L2.
+//  * the <W, true> instantiations are the rounding monitor (vlp_debug_fft_error): they also record the largest
+//    |V - round(V)| of every limb result (the exactness margin is 1/2).
 #include <cuda_runtime.h>
 
 #include <algorithm>
