@@ -150,7 +150,8 @@ int vlp_pubkeygen_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, s
 int vlp_debug_chacha20_block(const uint32_t* key, uint32_t counter, const uint32_t* nonce, uint32_t* out);
 /* Test hook: the calling thread's NEXT *_secure call (host or device) uses key[8] instead of a getrandom key, then
  * the hook is cleared.  Lets a test compare a device secure call with the host secure call under one key; never
- * use it to protect data (the key is whatever the caller passed). */
+ * use it to protect data (the key is whatever the caller passed).  Disabled (VLP_EINVAL) unless the environment
+ * variable VLP_TEST_HOOKS is "1". */
 int vlp_debug_next_secure_key(const uint32_t* key);
 /* Ciphertexts per record in the encrypted DB: W * l_I + l_S. */
 int vlp_db_record_cts(const vlp_meta* meta, size_t* per_record);

@@ -10,6 +10,7 @@
 
 #include <cerrno>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <thread>
@@ -396,6 +397,9 @@ int vlp_pubkeygen_secure(const vlp_sk* sk, const vlp_meta* meta, size_t first, s
 
 int vlp_debug_next_secure_key(const uint32_t* key) {
   if (!key) return fail(VLP_EINVAL, "null argument");
+  const char* on = getenv("VLP_TEST_HOOKS");
+  if (!on || std::strcmp(on, "1") != 0)
+    return fail(VLP_EINVAL, "vlp_debug_next_secure_key is a test hook: set VLP_TEST_HOOKS=1 to enable it");
   std::memcpy(g_next_key, key, sizeof(g_next_key));
   g_next_key_set = true;
   return VLP_OK;

@@ -689,6 +689,7 @@ def test_device_keygen_equals_host():
 
 
 def _next_key(key):
+    os.environ["VLP_TEST_HOOKS"] = "1"  # the hook is disabled without it
     k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32))
     A.check(A.lib().vlp_debug_next_secure_key(A._u32p(k)))
 

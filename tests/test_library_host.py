@@ -256,8 +256,19 @@ def test_secure_calls_are_fresh_and_correct():
 
 
 def _next_key(key):
+    os.environ["VLP_TEST_HOOKS"] = "1"  # the hook is disabled without it
     k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32))
     A.check(A.lib().vlp_debug_next_secure_key(A._u32p(k)))
+
+
+def test_secure_key_hook_needs_the_test_switch(monkeypatch):
+    """vlp_debug_next_secure_key is refused (VLP_EINVAL) unless VLP_TEST_HOOKS=1: a production process cannot have
+    its secure calls' keys injected."""
+    monkeypatch.delenv("VLP_TEST_HOOKS", raising=False)
+    k = np.zeros(8, np.uint32)
+    assert A.lib().vlp_debug_next_secure_key(A._u32p(k)) == L.VLP_EINVAL
+    k1, k2 = A.Keys(), A.Keys()  # still fresh OS randomness
+    assert not np.array_equal(k1.export()[0], k2.export()[0])
 
 
 def test_secure_key_hook_is_single_use():
