@@ -1,5 +1,6 @@
-"""Developer tool: K3T (tcgen05 int8 key switch) against the oracle on random N-LWE rows, plus the time of a
-2048-wide and a 16384-wide level of key switches (CUDA events).  Tests live in tests/test_gpu_parity.py.
+"""Developer tool: the time of 2048- and 16384-wide K3T (tcgen05 int8 key switch) launches through the debug call
+(CUDA events), and with --level the key-switch time inside a NAND program.  The oracle parity tests of K3T live in
+tests/test_gpu_parity.py.
     python tools/ks_check.py"""
 import os
 import sys
@@ -8,28 +9,13 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle as O  # noqa: E402
 from paper_2506_12761_b200 import api as A  # noqa: E402
 
 
 def main():
     keys = A.Keys(123)
     srv = A.Server(keys, 0)
-    ok = O.OracleKeys(123)
     rng = np.random.default_rng(3)
-    for count in (1, 17, 130):
-        nl = rng.integers(0, 2 ** 32, (count, 1028), dtype=np.uint64).astype(np.uint32)
-        nl[:, 1025:] = 0
-        got = A.to_host(srv.debug_keyswitch(A.to_device(nl)))
-        bad = 0
-        for i in range(count):
-            want = ok.keyswitch(nl[i, :1025])
-            if not np.array_equal(got[i, :631], want) or got[i, 631] != 0:
-                bad += 1
-                if bad <= 2:
-                    d = np.flatnonzero(got[i, :631] != want)
-                    print(f"count {count} row {i}: {len(d)} words differ, first {d[:6]} got {got[i, d[:3]]} want {want[d[:3]]}")
-        print(f"count {count}: {count - bad}/{count} rows byte-equal", flush=True)
     for count in (2048, 16384):
         nl = A.to_device(rng.integers(0, 2 ** 32, (count, 1028), dtype=np.uint64).astype(np.uint32))
         srv.debug_keyswitch(nl)
