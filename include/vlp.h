@@ -325,6 +325,14 @@ int vlp_server_workspace_bytes(const vlp_meta* meta, size_t count, size_t* evk_b
 int vlp_server_eval(vlp_server* server, const vlp_meta* meta, size_t first, size_t count,
                     const uint32_t* query_dev, const uint32_t* db_dev, uint32_t* out_dev, void* scratch_dev,
                     size_t scratch_bytes, uint64_t stream);
+/* server_eval with HOST query and result buffers (the end-to-end call of one query): copies query_host
+ * ([query cts][632] u32, vlp_encrypt_query layout; pinned memory recommended) into scratch, runs vlp_server_eval
+ * against the device-resident DB, and copies the l_S result ciphertexts to out_host ([l_S][632]); returns after the
+ * result is on the host.  scratch_dev >= vlp_server_eval_host_workspace_bytes(meta, count). */
+int vlp_server_eval_host_workspace_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes);
+int vlp_server_eval_host(vlp_server* server, const vlp_meta* meta, size_t first, size_t count,
+                         const uint32_t* query_host, const uint32_t* db_dev, uint32_t* out_host, void* scratch_dev,
+                         size_t scratch_bytes, uint64_t stream);
 /* server_eval for nq queries at once (multi-query packing): queries_dev [nq][query cts][632],
  * out_dev [nq][l_S][632]; scratch from vlp_server_batch_workspace_bytes. */
 int vlp_server_batch_workspace_bytes(const vlp_meta* meta, size_t count, uint32_t nq, size_t* scratch_bytes);

@@ -109,6 +109,8 @@ SIGNATURES = {
     "vlp_server_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t),
                                         ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_server_eval": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _vp, _vp, _vp, _vp, _sz, _u64]),
+    "vlp_server_eval_host_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.POINTER(ctypes.c_size_t)]),
+    "vlp_server_eval_host": (_i, [_vp, ctypes.POINTER(VlpMeta), _sz, _sz, _u32p, _vp, _u32p, _vp, _sz, _u64]),
     "vlp_server_batch_workspace_bytes": (_i, [ctypes.POINTER(VlpMeta), _sz, ctypes.c_uint32,
                                               ctypes.POINTER(ctypes.c_size_t)]),
     "vlp_server_eval_batch": (_i, [_vp, ctypes.POINTER(VlpMeta), ctypes.c_uint32, _sz, _sz, _vp, _vp, _vp, _vp, _sz,

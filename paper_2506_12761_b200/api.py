@@ -303,6 +303,23 @@ class Server:
                                     ctypes.c_void_p(db_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
                                     ctypes.c_void_p(sc.data_ptr()), sc.numel(), sh))
 
+    def eval_host(self, m: VlpMeta, query_host: np.ndarray, db_dev, out_host: np.ndarray, first: int = 0,
+                  count: int | None = None, stream=None):
+        """server_eval with host buffers (vlp_server_eval_host): query_host [query cts, 632] u32 in, the l_S result
+        ciphertexts into out_host [l_S, 632] u32 (both C-contiguous; pinned memory makes the copies asynchronous).
+        Returns once the result is on the host."""
+        count = m.M - first if count is None else count
+        key = ("eval_host", bytes(m), first, count)
+        if key not in self.__dict__.setdefault("_ws", {}):
+            sb = ctypes.c_size_t()
+            check(lib().vlp_server_eval_host_workspace_bytes(ctypes.byref(m), count, ctypes.byref(sb)))
+            self._ws[key] = sb.value
+        sh = _stream_handle(stream, self.device)
+        sc = self._scratch(key, self._ws[key], sh)
+        check(lib().vlp_server_eval_host(self.h, ctypes.byref(m), first, count, _u32p(query_host),
+                                         ctypes.c_void_p(db_dev.data_ptr()), _u32p(out_host),
+                                         ctypes.c_void_p(sc.data_ptr()), sc.numel(), sh))
+
     def eval_batch(self, m: VlpMeta, queries_dev, db_dev, out_dev, nq: int, first: int = 0,
                    count: int | None = None, stream=None):
         """Multi-query packing: nq queries (queries_dev [nq * query cts, 632]) -> out_dev [nq * l_S, 632]."""

@@ -863,6 +863,41 @@ int vlp_server_eval(vlp_server* s, const vlp_meta* meta, size_t first, size_t co
   return vlp_program_eval(p.get(), scratch, scratch_bytes, query_dev, db_dev, out_dev, stream);
 }
 
+int vlp_server_eval_host_workspace_bytes(const vlp_meta* meta, size_t count, size_t* scratch_bytes) {
+  if (!meta || !scratch_bytes) return fail(VLP_EINVAL, "null argument");
+  size_t prog = 0;
+  if (int rc = vlp_server_workspace_bytes(meta, count, nullptr, nullptr, &prog)) return rc;
+  *scratch_bytes = align256(prog) + align256(query_words(*meta) * meta->l_I * kCt * 4) +
+                   align256(static_cast<size_t>(meta->l_S) * kCt * 4);
+  return VLP_OK;
+}
+
+int vlp_server_eval_host(vlp_server* s, const vlp_meta* meta, size_t first, size_t count, const uint32_t* query_host,
+                         const uint32_t* db_dev, uint32_t* out_host, void* scratch, size_t scratch_bytes,
+                         uint64_t stream) {
+  if (!s || !meta || !query_host || !out_host || !scratch) return fail(VLP_EINVAL, "null argument");
+  if (int rc = check_meta(meta)) return rc;
+  std::shared_ptr<vlp_program> p;
+  if (int rc = cached_program(s, meta_key("eval", *meta, first, count),
+                              [&](vlp_program** o) { return vlp_program_create(s, meta, first, count, o); }, &p))
+    return rc;
+  const size_t qbytes = query_words(*meta) * meta->l_I * kCt * 4, obytes = static_cast<size_t>(meta->l_S) * kCt * 4;
+  const size_t prog = align256(p->bytes);
+  if (scratch_bytes < prog + align256(qbytes) + align256(obytes)) return fail(VLP_ENOMEM, "scratch too small");
+  uint8_t* sc = static_cast<uint8_t*>(scratch);
+  uint32_t* qd = reinterpret_cast<uint32_t*>(sc + prog);
+  uint32_t* od = reinterpret_cast<uint32_t*>(sc + prog + align256(qbytes));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DeviceGuard dg;
+  cudaError_t e;
+  if ((e = dg.set(s->device))) return cuda_fail(e, "cudaSetDevice");
+  if ((e = cudaMemcpyAsync(qd, query_host, qbytes, cudaMemcpyHostToDevice, st))) return cuda_fail(e, "query upload");
+  if (int rc = vlp_program_eval(p.get(), scratch, prog, qd, db_dev, od, stream)) return rc;
+  if ((e = cudaMemcpyAsync(out_host, od, obytes, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "result download");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "server eval sync");
+  return VLP_OK;
+}
+
 int vlp_server_batch_workspace_bytes(const vlp_meta* meta, size_t count, uint32_t nq, size_t* scratch_bytes) {
   if (!meta || !scratch_bytes) return fail(VLP_EINVAL, "null argument");
   vlp_program* p = nullptr;

@@ -1,7 +1,8 @@
 /* Plain-C user of the server half of the C ABI (include/vlp.h) on a GPU: device memory from the CUDA runtime
  * (the library never allocates it), vlp_server_create, vlp_gate_batch (8 NAND gates), vlp_server_eval on two
  * record shards + vlp_server_combine (G = 2) versus one vlp_server_eval over all records: the two
- * results are byte-identical (R15) and decrypt to the plain predicate (R = XOR of the matching payloads).
+ * results are byte-identical (R15) and decrypt to the plain predicate (R = XOR of the matching payloads); and
+ * vlp_server_eval_host (host query in, host result out) gives the same bytes.
  * Built and run by tests/test_c_abi.py (-m gpu) against libvlp.so. */
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -115,6 +116,16 @@ int main(void) {
     fprintf(stderr, "sharded + combine != single evaluation\n");
     return 4;
   }
+  /* the same query through the host-buffer call: query from host memory, result to host memory */
+  size_t sb_host = 0;
+  CHECK(vlp_server_eval_host_workspace_bytes(&m, 4, &sb_host));
+  void* s_host = dev_alloc(sb_host);
+  uint32_t* hhost = (uint32_t*)calloc(m.l_S, ct_bytes);
+  CHECK(vlp_server_eval_host(srv, &m, 0, 4, hq, ddb, hhost, s_host, sb_host, 0));
+  if (memcmp(hall, hhost, m.l_S * ct_bytes) != 0) {
+    fprintf(stderr, "vlp_server_eval_host != vlp_server_eval\n");
+    return 6;
+  }
   uint8_t rbits[3];
   uint64_t value = 0;
   CHECK(vlp_decrypt_result(sk, hall, m.l_S, rbits, &value));
@@ -128,7 +139,7 @@ int main(void) {
   vlp_free_server(srv);
   vlp_free_sk(sk);
   vlp_free_evk(evk);
-  printf("c abi server ok: NAND x%d, IntV M=4 sharded x2 + combine == single, R=%llu\n", G,
+  printf("c abi server ok: NAND x%d, IntV M=4 sharded x2 + combine == single == host-buffer call, R=%llu\n", G,
          (unsigned long long)value);
   return 0;
 }

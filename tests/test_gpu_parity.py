@@ -434,6 +434,24 @@ def test_fft_rounding_margin_at_scale(server, route):
     assert 0.0 < worst < 2.0 ** -10
 
 
+def test_server_eval_host_equals_device_call(server):
+    """vlp_server_eval_host (the e2e call of bench.py at N = 1: host query in, host result out) gives the bytes of
+    vlp_server_eval on device buffers, on config 1 and on a 512-record shard of config 2."""
+    k = server.keys
+    for cfg, first, count in ((1, 0, None), (2, 512, 512)):
+        wl = make_workload(cfg, key_seed=SEED)
+        count = wl.M if count is None else count
+        m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags)
+        q = k.encrypt_query(m, wl.query, 7)
+        db = A.to_device(k.encrypt_db(m, wl.records[first:first + count], wl.payloads[first:first + count],
+                                      pk_seed=9, first=first, count=count))
+        dev_out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+        server.eval(m, A.to_device(q), db, dev_out, first=first, count=count)
+        host_out = np.zeros((wl.l_S, 632), np.uint32)
+        server.eval_host(m, np.ascontiguousarray(q, dtype=np.uint32), db, host_out, first=first, count=count)
+        assert np.array_equal(host_out, A.to_host(dev_out)), cfg
+
+
 def test_config2_full_size_sampled(server):
     """Config 2 at full size (IntV 1D, 1024 records, 132,080 BR) in the production layout (rows recycled by
     liveness, as bench.py runs it): predicate + records 3 and 1023 byte-equal."""
