@@ -49,6 +49,7 @@ __constant__ cd c_w16[16];    // w16^k = psi^(128 k)
 __constant__ cd c_w32[8];     // w32^r = psi^(64 r)
 
 constexpr int kFSlots = 5;                         // key ring depth (chunks of 16 KB)
+constexpr long long kDesyncCycles = 3500;          // start offset of warps 4-7 (see the step loop)
 constexpr int kTrStride = 17;                      // complex per transpose row (one pad: conflict-free LDS.128)
 constexpr int kTrBytes = 2 * 16 * kTrStride * 16;  // T[g 2][k1 16][i 16 + 1]: 8704
 constexpr int kFWarpBytes = 2 * N * 4 + kTrBytes + 640 * 2;  // accumulator + transpose buffer + abar: 18,176
@@ -469,6 +470,15 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
     }
     __syncwarp();
 
+    // The two warps of a scheduler (w, w + 4) run the same step sequence; started together they hit their MAC
+    // phases (key LDS bursts, shared by all 8 warps) at the same time.  Starting the second one ~half an
+    // FFT + MAC period later interleaves one warp's MAC with the other's FFT: 16.58 -> 16.37 ms per wave
+    // (profiles/r2_k2f_phases.txt; 2500-4500 cycles all help, 3500 best).
+    if (w >= 4) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < kDesyncCycles) {
+      }
+    }
     // ---- S5: CMux steps
     double err = 0.0;  // ERR: this lane's largest rounding distance
     VLP_PHASE_DECL
