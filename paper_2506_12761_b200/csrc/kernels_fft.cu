@@ -49,7 +49,10 @@ __constant__ cd c_w16[16];    // w16^k = psi^(128 k)
 __constant__ cd c_w32[8];     // w32^r = psi^(64 r)
 
 constexpr int kFSlots = 5;                         // key ring depth (chunks of 16 KB)
-constexpr long long kDesyncCycles = 3500;          // start offset of warps 4-7 (see the step loop)
+#ifndef VLP_DESYNC
+#define VLP_DESYNC 3500
+#endif
+constexpr long long kDesyncCycles = VLP_DESYNC;    // start offset of warps 4-7 (see the step loop)
 constexpr int kTrStride = 17;                      // complex per transpose row (one pad: conflict-free LDS.128)
 constexpr int kTrBytes = 2 * 16 * kTrStride * 16;  // T[g 2][k1 16][i 16 + 1]: 8704
 constexpr int kFWarpBytes = 2 * N * 4 + kTrBytes + 640 * 2;  // accumulator + transpose buffer + abar: 18,176
@@ -119,15 +122,22 @@ __device__ __forceinline__ cd shfl16(cd v) {
 //    rho then holds k1 = mrev(rho) ^ 8h.  So the registers rho with mrev(rho) < 8 ("A": rho & 2 == 0) hold each
 //    lane's own 8 k1 values and the lane-pair partner (b ^ 16) holds the matching values in register rho | 2 --
 //    the lane-pair radix-2 stage needs no lane-dependent selects (tools/emulate_br_fft.py --v3).
-//  * tw[r] = psi^{b (1 + 4 k1(rho = r))} (the fold twist's psi^b merged in), all 16 held in registers.
+//  * tw[r] = psi^{b (1 + 4 k1(rho = r))} (the fold twist's psi^b merged in); the 8 with mrev(r) < 8 held in registers.
 //  * tau = (h ? -1 : 1) w32^bb, the twiddle of the pair's difference (the sign makes both lanes use own - partner).
 struct Lane {
-  cd tw[16];
+  cd tw[8];  // tw of the registers ra = (q & 1) | (q >> 1) << 2 (mrev(ra) < 8), indexed by q
+  cd c32;    // psi^{32 b (h ? -1 : 1)}: tw[ra | 2] = tw[ra] c32 (their k1 differ by 8)
   cd tau;
   double sgn, off;  // sgn = h ? -1 : 1; off = -sgn (2^52 + 64) (odd-a digit conversion)
   uint32_t lane, tbase;  // tbase: this lane's transpose offset (8h * kTrStride + bb) in complex
 };
-__device__ __forceinline__ cd twid(const Lane& c, int r) { return c.tw[r]; }
+// Half the per-lane twiddles are held (8 complex + c32) and the other half formed by one complex product per
+// transform pair: 4 more FP64 instructions per pair, 28 fewer registers held across the step (255-register
+// kernel): 16.36 -> 16.06 ms per wave (tools/variant_time.sh; a quarter of them, c16 for odd q: 16.20 ms).
+__device__ __forceinline__ cd twid(const Lane& c, int r) {
+  const cd t = c.tw[(r & 1) | ((r >> 2) << 1)];
+  return (r & 2) ? cmul(t, c.c32) : t;
+}
 
 // Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
 // 32 q + lane, q < 32) -> v[rho] = point lane + 32 mrev(rho).
@@ -398,9 +408,14 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
   {
     const uint32_t h = lane >> 4;
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int q = 0; q < 8; q++) {
+      const int r = (q & 1) | ((q >> 1) << 2);
       const double2 t = a.psi[(lane * (1u + 4u * (static_cast<uint32_t>(mrev(r)) ^ (8u * h)))) & 2047u];
-      lc.tw[r] = {t.x, t.y};
+      lc.tw[q] = {t.x, t.y};
+    }
+    {
+      const double2 t = a.psi[(h ? 2048u - 32u * lane : 32u * lane) & 2047u];
+      lc.c32 = {t.x, t.y};
     }
     const double2 w32 = a.psi[(64u * (lane & 15u)) & 2047u];
     lc.sgn = h ? -1.0 : 1.0;
@@ -486,8 +501,8 @@ __global__ void __launch_bounds__(W * 32, 1) vlp_blind_rotate_fft_kernel(const B
       const uint32_t ab = abar[i];
 #pragma unroll 1
       for (int u = 0; u < 2; u++) {
-        uint32_t wv[32];
         const uint32_t* au = acc + u * N;
+        uint32_t wv[32];
 #pragma unroll
         for (int q = 0; q < 32; q++) {
           const uint32_t j = 32u * q + lane;
