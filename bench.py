@@ -33,12 +33,12 @@ METRIC = "gate bootstraps/sec and records/sec per query at 1/2/4/8 B200"
 UNIT = "gate bootstraps/s"
 CONFIG_BR = {1: 252, 2: 132080, 3: 1060832, 4: 6750176}
 # dram__bytes_read.sum + dram__bytes_write.sum of one K2F launch (one whole wave of 8 x 148 = 1184 bootstraps,
-# 630 CMux steps) from `ncu --set full` (profiles/r2_k2f_ncu_summary.txt): ~one pass over the 123.9 MB FFT-domain
+# 630 CMux steps) from `ncu --set full` (profiles/r2_k2f_twh_ncu_summary.txt): ~one pass over the 123.9 MB FFT-domain
 # key per launch (the key stays in the 126 MB L2 across the wave's CTAs) plus the ciphertexts.
-TRAFFIC_BYTES_PER_WAVE = (127.971840 + 4.631040) * 1e6
-TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_fft_kernel<8>, 1184-bootstrap launch (profiles/r2_k2f_ncu_summary.txt)"
+TRAFFIC_BYTES_PER_WAVE = (127.907072 + 4.489728) * 1e6
+TRAFFIC_SOURCE = "ncu --set full, vlp_blind_rotate_fft_kernel<8>, 1184-bootstrap launch (profiles/r2_k2f_twh_ncu_summary.txt)"
 BSK_FFT_BYTES = 630 * 12 * 16384   # FFT-domain key streamed per pass (kernels.cuh kBskFftBytes)
-FP64_PER_BR = 4.375e6 * 32         # FP64 lane-ops per blind rotation in K2F (ncu SASS histogram, profiles/)
+FP64_PER_BR = 4.373e6 * 32         # FP64 lane-ops per blind rotation in K2F (ncu source page, profiles/r2_k2f_twh_ncu_summary.txt)
 
 
 def alg_ops_per_br():
