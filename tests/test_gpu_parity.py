@@ -1109,3 +1109,32 @@ def test_dataset_shapes_with_options_predicate(server, cfg):
     L.check(L.lib().vlp_program_get_info(h, ctypes.byref(info)))
     L.lib().vlp_free_program(h)
     assert prog.info.levels < info.levels
+
+
+def test_config2_engines_agree_on_every_gate(route):
+    """Config 2 at full size (132,080 BR) evaluated twice with VLP_F_KEEP_ALL (every intermediate keeps its own
+    scratch row): the default routing (K2F waves + tails) and the integer-NTT engine alone (vlp_debug_route(1, 5)).
+    The two exact engines share no arithmetic, so every gate output row must be byte-equal
+    between them (tools/engine_crosscheck.py runs the same check on configs 3, 4 and 10)."""
+    wl = make_workload(2)
+    m = A.meta(wl.mode, wl.M, wl.l_I, wl.l_S, wl.d, wl.flags | L.F_KEEP_ALL)
+    keys = A.Keys(wl.key_seed)
+    srv = A.Server(keys, 0)
+    pk = A.pubkeygen_device(keys, m, wl.key_seed + 1, 0, wl.M)
+    db = A.server_encrypt_db_device(m, pk, wl.records, wl.payloads)
+    q = A.to_device(keys.encrypt_query(m, wl.query, 7))
+    prog = A.Program.velopir(srv, m)
+    rows, outs = [], []
+    for eng, par in ((0, 0), (1, 5)):
+        route(eng, par)
+        out = torch.zeros((wl.l_S, 632), dtype=torch.int32, device="cuda:0")
+        prog.scratch.zero_()
+        prog.eval(q, db, out)
+        torch.cuda.synchronize()
+        assert keys.decrypt_value(A.to_host(out)) == expected_result(wl)
+        rows.append(prog.intermediate().clone())
+        outs.append(out)
+    written = int(((rows[0] != 0).any(dim=1) | (rows[1] != 0).any(dim=1)).sum())
+    assert written > prog.info.ks  # every gate output row (plus the constants) was written
+    assert torch.equal(rows[0], rows[1]), int((rows[0] != rows[1]).any(dim=1).sum())
+    assert torch.equal(outs[0], outs[1])
