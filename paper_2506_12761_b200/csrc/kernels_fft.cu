@@ -115,8 +115,6 @@ __device__ __forceinline__ cd shfl16(cd v) {
 // Gadget digit field f = (w >> s) & 127 (R5: w = D + 0x81020400) enters the FFT as the double f - 64, exactly:
 // (2^52 + f) - (2^52 + 64), the first term built by putting f into the low mantissa word of 2^52 (fft_fwd).
 
-// Forward transform of one digit polynomial of this lane's 32 coefficients (wv[q] = offset D at coefficient
-// 32 q + lane, q < 32) -> X[rho] = point lane + 32 mrev(rho).
 // Per-lane constants of the transform (lane b = 16 h + bb).
 //  * Lanes with h = 1 negate the odd inputs a of their first 16-point DFT, which shifts its output by 8: register
 //    rho then holds k1 = mrev(rho) ^ 8h.  So the registers rho with mrev(rho) < 8 ("A": rho & 2 == 0) hold each
