@@ -296,7 +296,8 @@ def main():
                          "(synth/workloads.py)")
     ap.add_argument("--nand", type=int, default=1 << 17, help="config 5: NAND gates per step (split over ranks)")
     ap.add_argument("--queries", type=int, default=1,
-                    help="queries per step (multi-query packing on one GPU: every level launch carries all of them)")
+                    help="queries per step (multi-query packing: every level launch carries all of them; with N > 1 each "
+                         "rank packs them against its shard and rank 0 combines every query)")
     ap.add_argument("--prefix-comparator", action="store_true",
                     help="R23 (not in the paper): log-depth prefix comparators (VLP_F_PREFIX_COMP) for IntV configs")
     ap.add_argument("--linear-sum", action="store_true",
@@ -359,16 +360,14 @@ def main():
     # the host calls (tests/test_gpu_parity.py)
     pk = A.pubkeygen_device(keys, m, wl.key_seed + 1, first, shard, device=local)
     db = A.server_encrypt_db_device(m, pk, wl.records[first:first + shard], wl.payloads[first:first + shard])
-    nq = args.queries
-    if nq > 1 and world > 1:
-        raise SystemExit("--queries > 1 is single-GPU (multi-query packing of one shard)")
+    nq = args.queries  # with N > 1 every rank packs the nq queries against its shard; rank 0 combines each query
     qvals = [list(wl.query)] + extra_queries(wl, nq - 1)
     q_host = np.concatenate([keys.encrypt_query(m, qv, 7 + i) for i, qv in enumerate(qvals)])
     q = A.to_device(q_host, local)
-    prog = A.Program.velopir(srv, m, first, shard) if nq == 1 else A.Program.queries(srv, m, nq)
+    prog = A.Program.velopir(srv, m, first, shard) if nq == 1 else A.Program.queries(srv, m, nq, first, shard)
     comb = A.Program.combine(srv, m, world) if (world > 1 and rank == 0) else None
-    part = torch.zeros((wl.l_S, 632), dtype=torch.int32, device=dev)
-    gathered = torch.zeros((world * wl.l_S, 632), dtype=torch.int32, device=dev) if world > 1 else None
+    part = torch.zeros((nq * wl.l_S, 632), dtype=torch.int32, device=dev)
+    gathered = torch.zeros((world * nq * wl.l_S, 632), dtype=torch.int32, device=dev) if world > 1 else None
     out = torch.zeros((nq * wl.l_S, 632), dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     setup_s = time.time() - t_setup
@@ -377,8 +376,13 @@ def main():
         prog.eval(qdev, db, part if world > 1 else out, stream)
         return part if world > 1 else out
 
+    def per_query_roots(roots):  # gathered [rank][query][l_S] -> query i's G shard roots, contiguous
+        r4 = roots.view(world, nq, wl.l_S, 632)
+        return [(r4[:, i].contiguous(), out[i * wl.l_S:(i + 1) * wl.l_S]) for i in range(nq)]
+
     def combine(roots):
-        comb.eval(roots, None, out, stream)
+        for ri, oi in per_query_roots(roots):
+            comb.eval(ri, None, oi, stream)
         return out
 
     def step(qdev):  # broadcast query -> shard eval -> gather shard roots -> top tree levels on rank 0
@@ -439,13 +443,14 @@ def main():
 
         def eval_api(qdev):
             if nq > 1:
-                srv.eval_batch(m, qdev, db, out, nq, stream=stream)
-                return out
+                srv.eval_batch(m, qdev, db, part if world > 1 else out, nq, first=first, count=shard, stream=stream)
+                return part if world > 1 else out
             srv.eval(m, qdev, db, part if world > 1 else out, first=first, count=shard, stream=stream)
             return part if world > 1 else out
 
         def combine_api(roots):
-            srv.combine(m, world, roots, out, stream=stream)
+            for ri, oi in per_query_roots(roots):
+                srv.combine(m, world, ri, oi, stream=stream)
             return out
 
         def step(qdev):  # noqa: F811 -- the e2e step goes through the public calls
@@ -480,7 +485,7 @@ def main():
         e2e = {"value": nq * br_per_query / (e2e_ms / 1e3), "unit": UNIT, "records_per_s": nq * wl.M / (e2e_ms / 1e3),
                # the query, plus the job tables every server_eval / combine copies into its scratch
                "h2d_bytes_per_step": int(q_host.nbytes) + int(prog.info.table_bytes)
-                                     + (int(comb.info.table_bytes) if comb else 0),
+                                     + (int(comb.info.table_bytes) * nq if comb else 0),
                "d2h_bytes_per_step": int(nq * wl.l_S * 632 * 4), "steps": e2e_steps,
                "call": "vlp_server_eval_host (host query in, host result out)" if host_call else
                        "query H2D + vlp_server_eval per shard (+ NCCL broadcast / gather, vlp_server_combine) + result D2H"}
@@ -501,8 +506,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "records_per_s": records_per_s, "ks_per_s": (prog.info.ks * world + (comb.info.ks if comb else 0)) / (ms_per_step / 1e3),  # all queries
-            "gates_per_s": (prog.info.gates * world + (comb.info.gates if comb else 0)) / (ms_per_step / 1e3),  # MUX = 1
+            "records_per_s": records_per_s, "ks_per_s": (prog.info.ks * world + (comb.info.ks * nq if comb else 0)) / (ms_per_step / 1e3),  # all queries
+            "gates_per_s": (prog.info.gates * world + (comb.info.gates * nq if comb else 0)) / (ms_per_step / 1e3),  # MUX = 1
             "config": {"workload": f"cfg{args.config}_{wname}", "M": wl.M, "l_I": wl.l_I, "l_S": wl.l_S,
                        "d": wl.d, "br_per_query": br_per_query, "levels": prog.info.levels, "queries_per_step": nq,
                        "parallelism": f"records sharded x{world}" if world > 1 else "single GPU",
@@ -535,7 +540,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
-            "gpu_launches": prog.info.kernel_launches * args.steps + (comb.info.kernel_launches * args.steps if comb else 0),
+            "gpu_launches": prog.info.kernel_launches * args.steps + (comb.info.kernel_launches * nq * args.steps if comb else 0),
             "setup_s": setup_s, "wall_s_timed": wall,
         }
         print(json.dumps(line), flush=True)

@@ -88,3 +88,22 @@ def test_bench_multi_rank_path_on_one_gpu(cfg, world):
         assert d["e2e"]["value"] > 0
     else:
         assert d["config"]["gates"] == 1 << 12
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_multi_query_on_one_gpu():
+    """SURVEY 8(f) NEXT 2 at G > 1: two ranks (one GPU, gloo, as above) each pack 2 queries against their shard of
+    config 2 (vlp_program_create_queries on [first, first + count)), rank 0 gathers the 2 x 2 shard roots and combines
+    each query; bench.py checks both queries' decrypted results against the plain predicate."""
+    env = dict(os.environ, VLP_BENCH_ONE_GPU_GLOO="1")
+    args = ["--config", "2", "--queries", "2", "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+                        os.path.join(ROOT, "bench.py"), "--gpus", "2", *args],
+                       capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["queries_per_step"] == 2
+    assert d["config"]["parallelism"] == "records sharded x2" and d["e2e"]["value"] > 0
