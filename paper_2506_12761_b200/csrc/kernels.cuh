@@ -63,6 +63,7 @@ struct BrArgs {
   unsigned long long* fft_err;  // debug (vlp_debug_fft_error): max |V - round(V)| of K2F's roundings, double bits
   uint32_t zero;  // always 0 (a runtime zero; see add_alu in kernels.cu)
   uint32_t p2;    // always 2p, set by launch_blind_rotate (a runtime constant; see ct_bfly in kernels.cu)
+  uint32_t pdl_at;  // K2F: CMux step at which a CTA lets the next wave's launch start (kernels_fft.cu; set there)
 };
 
 struct KsArgs {
